@@ -1,0 +1,361 @@
+#!/usr/bin/env python3
+"""Tree-attention decode benchmark (BASELINE.json metric: decode-attention
+latency in us per decoded token at 1/2/4/8 B200, plus HBM GB/s).
+
+Workload (default): Llama-3-8B attention shape -- 32 q / 8 kv heads, d 128,
+bf16, 1,048,576-token KV cache sharded over the N GPUs (BASELINE.json
+configs[2], the north-star target). A step is one decode of one new token:
+K1+K2 on every rank's shard, allreduce(max), K3, allreduce(sum), K4.
+Total work is fixed as N grows ("scaling": "strong").
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--workload cfg1|cfg2|cfg3|cfg4] [--seq-len N] [--algo tree|ring]
+
+Multi-GPU: launched by torchrun, one rank per GPU, NCCL. The timed region is
+bracketed by a barrier + cuda synchronize on both sides; every step is timed
+with CUDA events on the library's stream; the reported time is the max over
+ranks. Inputs are generated on the device with the reference generator
+(synthetic data, bit-exact with the CPU reference); the KV shard of every
+rank exceeds L2 at the default workload, otherwise L2 is flushed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (description, b, n_q, n_kv, seq_len, d, dtype)
+    "cfg1": ("single-head decode, 64K-token KV, d=128, fp32 (configs[0])", 1, 1, 1, 65536, 128, "f32"),
+    "cfg2": ("32-head MHA decode, batch 1, 256K tokens, bf16 (configs[1])", 1, 32, 32, 262144, 128, "bf16"),
+    "cfg3": ("Llama-3-8B attention (32q/8kv GQA, d=128), 1M-token KV, bf16 (configs[2])", 1, 32, 8, 1048576, 128,
+             "bf16"),
+    "cfg4": ("batch 16 decode, 128K tokens per sequence, GQA 8:1 (64q/8kv), bf16 (configs[3])", 16, 64, 8, 131072,
+             128, "bf16"),
+}
+METRIC = "decode-attn latency (µs/token) vs seq len at 1/2/4/8 B200; HBM GB/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--seq-len", type=int, default=None)
+    ap.add_argument("--algo", choices=["tree", "ring"], default="tree")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-heads", type=int, default=None)
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload, algo, n):
+    """dram bytes per K1 launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get(f"{workload}/{algo}/p{n}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[1]) for s in self.samples if len(s) > 2 and s[1].replace(".", "").isdigit())
+        mx = max((float(s[2]) for s in self.samples if len(s) > 2 and s[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 9 for i in range(4)
+                          if s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- CPU reference (oracle/_ref)
+def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1):
+    """Times the reference's own tree_decode (compiled from /root/reference by
+    oracle/Makefile) on a bounded sample: `sample_heads` q-heads of one kv
+    group at the full sequence length, p = n_gpus workers, rows spread over
+    nthreads host threads; scaled to the full head count."""
+    import numpy as np
+
+    from oracle.oracle import BF16, F32, HIER, Oracle, Reference
+    _, b, n_q, n_kv, n, d, dt = wl
+    n = args.seq_len or n
+    orc, ref = Oracle(), Reference()
+    dtc = BF16 if dt == "bf16" else F32
+    seed = orc.mix64(0, n)
+    g = n_q // n_kv
+    sample_heads = max(1, min(sample_heads, g))
+    qh = orc.seeded(orc.mix64(seed, 1), sample_heads * d, dtc).reshape(1, sample_heads, d)
+    k0 = orc.seeded(orc.mix64(seed, 2), n * d, dtc).reshape(1, 1, n, d)
+    v0 = orc.seeded(orc.mix64(seed, 3), n * d, dtc).reshape(1, 1, n, d)
+    times = []
+    with ref.prepare(qh, k0, v0, n_gpus, dtc) as pr:
+        for _ in range(steps):
+            _, secs, _ = pr.decode(0, HIER, args.scale, parallel=n_gpus > 1, nthreads=nthreads)
+            times.append(secs)
+    per_row = min(times) / sample_heads
+    rows = b * n_q
+    us_per_token = per_row * rows * 1e6 / b  # one decoded token per sequence per step
+    return us_per_token, times, {
+        "sample": f"{sample_heads} q-head(s) of kv head 0 at N={n}, p={n_gpus} workers, "
+                  f"scaled x{rows / sample_heads:g} to b*n_q={rows} rows; best of {steps}",
+        "cores": nthreads * (n_gpus if n_gpus > 1 else 1),
+    }
+
+
+def run_reference_arm(args, wl, world, rank):
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    _, b, n_q, n_kv, n, d, dt = wl
+    g = n_q // n_kv
+    # all host threads: rows (q-heads) in parallel, p workers each; bounded sample
+    heads = min(g, max(1, nthreads // max(1, args.gpus)))
+    vals = []
+    t0 = time.time()
+    for i in range(args.warmup + args.steps):
+        v, _, info = reference_cpu(args, wl, args.gpus, heads, max(1, nthreads // max(1, args.gpus)), steps=1)
+        if i >= args.warmup:
+            vals.append(v)
+    value = sum(vals) / len(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "µs/token", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * b / 1000.0, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": dt, "data": "synthetic (reference generator)",
+        "config": {"workload": args.workload, "seq_len": args.seq_len or n, "batch": b, "q_heads": n_q,
+                   "kv_heads": n_kv, "head_dim": d, "shards": args.gpus, "algo": "tree"},
+        "cpu_baseline": {"value": value, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
+                         "sample": info["sample"] + f"; host nproc={os.cpu_count()}"},
+        "e2e": {"value": value, "unit": "µs/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    wl = WORKLOADS[args.workload]
+    desc, b, n_q, n_kv, n, d, dt = wl
+    n = args.seq_len or n
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference_arm(args, wl, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+
+    import paper_2408_04093_b200 as td
+    from paper_2408_04093_b200 import _capi
+    torch.cuda.set_device(local)
+    dtype = td.DType.Bf16 if dt == "bf16" else td.DType.Float32
+    esz = 2 if dt == "bf16" else 4
+
+    def mix64(seed, c):  # numerics.cpp:30-35 (seeding convention only, bench.cpp:73)
+        m = (1 << 64) - 1
+        z = (seed + ((c + 1) * 0x9E3779B97F4A7C15)) & m
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+        return z ^ (z >> 31)
+
+    seed = mix64(0, n)
+    w = td.Worker.from_torch_distributed(local) if world > 1 else td.Worker(local)
+    w.generate_kv(dtype, b, n_kv, n, d, mix64(seed, 2), mix64(seed, 3))
+    start, shard_len, shard_bytes = w.kv_info()
+    q = td.seeded_tensor([b, n_q, d], mix64(seed, 1), 1.0, dtype)
+    out = torch.empty(b, n_q, d, dtype=torch.float32, device="cuda")
+    stream_ptr = w.stream
+    stream = torch.cuda.ExternalStream(stream_ptr)
+    flush = shard_bytes < 4 * L2_BYTES
+    scratch = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if flush else None
+    decode = w.tree_decode_async if args.algo == "tree" else w.ring_decode_async
+    flags_timed = _capi.TD_TIME_KERNELS
+
+    def step(flags):
+        decode(q.data_ptr(), n_q, out.data_ptr(), args.scale, flags)
+
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 3)):
+        step(0)
+    barrier(world)
+
+    # ---- device-timed region: K steps, per-step CUDA events on the library stream
+    w.reset_kernel_timer()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier(world)
+        for i in range(args.steps):
+            if flush:
+                with torch.cuda.stream(stream):
+                    scratch.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step(flags_timed)
+            evs[i][1].record(stream)
+        barrier(world)
+    step_ms = [a.elapsed_time(bb) for a, bb in evs]
+    ms_local = sum(step_ms) / len(step_ms)
+    k1_ms, k1_calls = w.kernel_time()
+    kernels_per_step, kv_bytes_step, split_kernel = w.last_launch_stats()
+    ms = max_over_ranks(ms_local, world)
+    k1_ms_max = max_over_ranks(k1_ms, world)
+
+    # ---- end-to-end through the public API with host buffers (pinned)
+    q_host = q.cpu().pin_memory()
+    out_host = torch.empty(b, n_q, d, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier(world)
+    e2e_times = []
+    for i in range(e2e_steps):
+        if flush:
+            with torch.cuda.stream(stream):
+                scratch.fill_(i & 0xFF)
+            stream.synchronize()
+        t0 = time.perf_counter()
+        decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_ms = max_over_ranks(1000.0 * sum(e2e_times) / len(e2e_times), world)
+    ok = torch.allclose(out_host, out.cpu())
+
+    # ---- CPU reference baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            heads = args.cpu_sample_heads or (n_q // n_kv)
+            v, _, info = reference_cpu(args, wl, 1, heads, min(os.cpu_count() or 1, heads), steps=2)
+            cpu = {"value": v, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
+                   "sample": info["sample"] + f"; host nproc={os.cpu_count()}"}
+        except Exception as e:  # the reference library may be absent on a foreign box
+            cpu = {"value": None, "unit": "µs/token", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        kv_per_rank = 2 * b * n_kv * math.ceil(n / world) * d * esz
+        achieved = kv_per_rank / (k1_ms_max * 1e-3) / 1e9 if k1_ms_max > 0 else None
+        line = {
+            "metric": METRIC, "value": ms * 1000.0 / b, "unit": "µs/token", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": dt,
+            "data": "synthetic (reference SplitMix64 generator, generated on device)",
+            "config": {"workload": args.workload, "desc": desc, "seq_len": n, "batch": b, "q_heads": n_q,
+                       "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": shard_len,
+                       "algo": args.algo, "scale": args.scale,
+                       "l2": "flushed between steps" if flush else "inputs larger than L2 (KV shard > 4x126 MB)",
+                       "parallelism": f"sp{world} (sequence-sharded KV)"},
+            "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None,
+                         "traffic": load_traffic(args.workload, args.algo, world),
+                         "kernel": {1: "k1_bf16 (split-KV, TMA + mma.sync)", 2: "k1_f32 (split-KV, bulk copy)",
+                                    0: "k1_generic"}.get(split_kernel), "kernel_ms": k1_ms_max,
+                         "bytes_per_launch": kv_per_rank, "peak_kind": peak_kind,
+                         "step_frac": kv_per_rank / (ms * 1e-3) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_ms * 1000.0 / b, "unit": "µs/token",
+                    "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
+                    "matches_device_output": bool(ok)},
+            "gpu_launches": kernels_per_step * args.steps,
+            "kernels_per_step": kernels_per_step,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    w.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

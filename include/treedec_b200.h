@@ -1,0 +1,172 @@
+/*
+ * treedec_b200.h -- C-ABI of the B200 tree-decode library
+ * (paper_2408_04093_b200/libtreedec_b200.so).
+ *
+ * Drop-in boundary for the reference's decode path (namespace treedec,
+ * /root/reference/proj/core). Plain pointers and sizes, no C++ or torch
+ * types; every call returns a td_status and td_last_error() describes the
+ * last failure on the calling thread. Status codes map onto the reference's
+ * exception types (decode.cpp:14-24, numerics.cpp:13-23):
+ *   TD_EINVAL  -> std::invalid_argument    TD_EDOMAIN -> std::domain_error
+ *   TD_ECUDA / TD_ENCCL / TD_ESTATE -> std::runtime_error
+ *
+ * Tensor layouts are the reference's row-major ones (tensor.hpp:16-19,46-48):
+ *   q    [b, n_q, d]        the single query row of each head (N_q = 1)
+ *   k, v [b, n_kv, t, d]    one worker's contiguous sequence shard
+ *   out  [b, n_q, d]        fp32
+ * GQA: q head h attends kv head h / (n_q / n_kv); n_q == n_kv is the
+ * reference's MHA contract (attention.cpp:18-28).
+ * dtype codes follow treedec::DType (dtype.hpp:13): 0 f64, 1 f32, 2 bf16.
+ * The GPU path computes on f32 or bf16 inputs with fp32 accumulation.
+ *
+ * Threading: stateless calls are thread-safe. A td_context is used by one
+ * host thread at a time (one context per GPU / rank), the analogue of one
+ * reference worker (decode.cpp:28-46).
+ */
+#ifndef TREEDEC_B200_H
+#define TREEDEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TD_OK = 0,
+    TD_EINVAL = 1,  /* invalid_argument: shapes, dtype, topology, p > N  */
+    TD_EDOMAIN = 2, /* domain_error: NaN / no attended key            */
+    TD_ECUDA = 3,
+    TD_ENCCL = 4,
+    TD_ESTATE = 5 /* call order (e.g. decode before td_kv_place)     */
+} td_status;
+
+typedef enum { TD_F64 = 0, TD_F32 = 1, TD_BF16 = 2 } td_dtype;
+
+/* treedec::ReduceStrategy (reduce.hpp:10). On the GPU the collective is one
+ * NCCL allreduce over NVLink; the strategy selects NCCL's algorithm hint. */
+typedef enum { TD_TREE_BINARY = 0, TD_RING_ALLREDUCE = 1, TD_HIERARCHICAL = 2 } td_strategy;
+
+/* flags for td_tree_decode / td_ring_decode */
+enum {
+    TD_HOST_IO = 1,      /* q and out are host pointers (copies inside the call) */
+    TD_TIME_KERNELS = 2, /* record CUDA events around the split-KV kernel (K1) */
+    TD_BF16_OUT = 4      /* also write a bf16 copy of out (td_output_bf16)      */
+};
+
+typedef struct td_context td_context;
+
+int td_version(void);
+const char* td_last_error(void);
+
+/* ---------------------------------------------------------------------
+ * Stateless device primitives (device pointers; stream may be NULL).
+ * ------------------------------------------------------------------- */
+
+/* Elements [start, start+len) of every row of seeded_random_tensor(
+ * [bh_count, seq, d], seed, scale, dtype), written as [bh_count, len, d].
+ * Bit-exact with numerics.cpp:41-50 + dtype.cpp:13-42 (double -> dtype
+ * directly). Replaces: seeded_random_tensor + slice_seq. */
+int td_seeded_fill(int dtype, void* dst, uint64_t seed, double scale, int64_t bh_count,
+                   int64_t seq, int64_t start, int64_t len, int64_t d, void* stream);
+
+/* Workspace bytes td_decode_partial needs for this shard shape. */
+int td_decode_workspace_bytes(int dtype, int64_t b, int64_t n_q, int64_t n_kv, int64_t t,
+                              int64_t d, size_t* bytes);
+
+/* attention_chunk_partial (attention.hpp:49-50, attention.cpp:146-168) of q
+ * against one shard: fp32 row_max [b,n_q], lse [b,n_q], out [b,n_q,d].
+ * Empty shard (t = 0) gives the identity (-inf, -inf, 0). */
+int td_decode_partial(int dtype, const void* q, const void* k, const void* v, int64_t b,
+                      int64_t n_q, int64_t n_kv, int64_t t, int64_t d, double scale,
+                      float* row_max, float* lse, float* out, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* combine_partials (attention.hpp:65, attention.cpp:207-241): lse [P][rows],
+ * out [P][rows][d] -> result [rows][d]. TD_EINVAL if a row attends no key. */
+int td_combine_partials(int P, const float* lse, const float* out, int64_t rows, int64_t d,
+                        float* result, void* stream);
+
+/* partial_to_numerator (attention.hpp:70, attention.cpp:243-266):
+ * nd = [num rows*d | den rows] against a common shift [rows]. */
+int td_partial_to_numerator(const float* lse, const float* out, const float* shift,
+                            int64_t rows, int64_t d, float* nd, void* stream);
+
+/* combine_pair (attention.hpp:59, attention.cpp:178-205), in place into
+ * left; left covers lower key indices. */
+int td_combine_pair(float* l_max, float* l_lse, float* l_out, const float* r_max,
+                    const float* r_lse, const float* r_out, int64_t rows, int64_t d,
+                    void* stream);
+
+/* out = num / den over nd = [num | den] (decode.cpp:165-173). */
+int td_finalize(const float* nd, int64_t rows, int64_t d, float* out, void* out_bf16,
+                void* stream);
+
+/* ---------------------------------------------------------------------
+ * Context: one per GPU / rank. Owns the stream, the KV shard placed in HBM,
+ * workspaces and the NCCL communicator of the tree / ring collectives.
+ * ------------------------------------------------------------------- */
+int td_create(int device, td_context** ctx);
+int td_destroy(td_context* ctx);
+int td_stream(td_context* ctx, void** stream);
+
+/* NCCL bootstrap (one process per GPU): rank 0 calls td_comm_unique_id and
+ * ships the 128 bytes to the other ranks; every rank calls td_comm_init.
+ * Without td_comm_init the context is a world of one (p = 1). */
+int td_comm_unique_id(unsigned char id[128]);
+int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[128]);
+int td_comm_info(td_context* ctx, int* nranks, int* rank);
+
+/* shard_kv (decode.hpp:24, decode.cpp:68-85) for this rank: places rows
+ * [start, start+len) of every (batch, kv-head) of a cache of seq_len tokens.
+ * k/v are [b, n_kv, len, d] on the host (from_host = 1) or device. */
+int td_kv_place(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len,
+                int64_t d, int64_t start, int64_t len, const void* k, const void* v,
+                int from_host);
+
+/* Generates this rank's shard in place with the seeded generator: k, v =
+ * seeded_random_tensor([b, n_kv, seq_len, d], seed_k / seed_v, scale, dtype)
+ * restricted to chunk_extents(seq_len, nranks)[rank] (attention.cpp:268-275). */
+int td_kv_generate(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len,
+                   int64_t d, uint64_t seed_k, uint64_t seed_v, double scale);
+
+/* Shard geometry of the placed cache. */
+int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes);
+/* Device pointers of the placed shard (for tests). */
+int td_kv_pointers(td_context* ctx, void** k, void** v);
+
+/* tree_decode (decode.hpp:70-72, decode.cpp:100-184): local partial (K1+K2),
+ * allreduce(max) of lse, rescale (K3), one fused sum-allreduce of [n|d],
+ * out = n/d (K4). q [b, n_q, d] in the cache dtype; out [b, n_q, d] fp32,
+ * identical on every rank. p = nranks must not exceed seq_len. */
+int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
+                   float* out, int flags);
+
+/* ring_decode (decode.hpp:77-78, decode.cpp:186-251): p-1 rotations of the
+ * KV shards around the ring (NCCL send/recv over NVLink), each rank folding
+ * the received chunk's partial with combine_pair in the reference order
+ * (own chunk, then chunks rank-1, rank-2, ...). out is identical on all
+ * ranks (the reference returns worker 0's). */
+int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
+                   int flags);
+
+/* bf16 copy of the last output (TD_BF16_OUT), device pointer. */
+int td_output_bf16(td_context* ctx, const void** out_bf16);
+
+/* Mean duration (ms) of K1 over the calls made with TD_TIME_KERNELS since
+ * the last td_reset_kernel_timer, and the number of timed calls. */
+int td_kernel_time(td_context* ctx, double* mean_ms, int* calls);
+int td_reset_kernel_timer(td_context* ctx);
+
+/* Kernels of this library launched by the last decode call, and the
+ * algorithmic HBM bytes of its K1 launch(es) (K + V of the shard). */
+int td_last_launch_stats(td_context* ctx, int* kernels, double* kv_bytes, int* split_kernel);
+
+/* Peak device bytes held by the context (KV shard, ring buffers, workspaces). */
+int td_memory_bytes(td_context* ctx, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TREEDEC_B200_H */

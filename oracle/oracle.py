@@ -179,7 +179,7 @@ class Reference:
         lib.ref_prepare.argtypes = [_c_double_p] * 3 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int]
         lib.ref_release.argtypes = [ctypes.c_void_p]
         lib.ref_decode.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
-                                   _i64, _i64, _c_double_p, _c_double_p, _c_double_p]
+                                   _i64, _i64, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p]
         self.lib = lib
 
     def error(self) -> str:
@@ -255,13 +255,13 @@ class PreparedRef:
             self.ref.lib.ref_release(self.handle)
             self.handle = None
 
-    def decode(self, algo, strategy=HIER, scale=1.0, parallel=False, row0=0, row1=None):
+    def decode(self, algo, strategy=HIER, scale=1.0, parallel=False, row0=0, row1=None, nthreads=1):
         """Returns (out, seconds, counters); out covers rows [row0, row1)."""
         row1 = self.rows if row1 is None else row1
         out = np.empty((row1 - row0) * self.d)
         secs = ctypes.c_double()
         counters = np.zeros(4)
-        rc = self.ref.lib.ref_decode(self.handle, algo, strategy, scale, int(parallel), row0, row1, _dp(out),
+        rc = self.ref.lib.ref_decode(self.handle, algo, strategy, scale, int(parallel), row0, row1, nthreads, _dp(out),
                                      ctypes.byref(secs), _dp(counters))
         if rc != 0:
             raise ValueError(self.ref.error())

@@ -17,6 +17,7 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace treedec;
@@ -167,41 +168,62 @@ void* ref_prepare(const double* q, const double* k, const double* v, std::int64_
 void ref_release(void* handle) { delete static_cast<Prepared*>(handle); }
 
 // Runs tree_decode (algo 0) or ring_decode (algo 1) over rows [row0, row1)
-// of a prepared problem, writing out [rows][d]. *seconds = wall time of the
-// decode calls alone. counters (optional, 4 doubles): elems_sent_total,
-// wire_elems_total, peak_elems_per_worker, rounds -- of the last row's call.
+// of a prepared problem, writing out [rows][d]. Rows are spread over
+// `nthreads` host threads (each row is an independent reference call; the
+// reference functions are pure). *seconds = wall time of the decode calls
+// alone. counters (optional, 4 doubles): elems_sent_total, wire_elems_total,
+// peak_elems_per_worker, rounds -- of the first row's call.
 int ref_decode(void* handle, int algo, int strategy, double scale, int parallel,
-               std::int64_t row0, std::int64_t row1, double* out, double* seconds,
+               std::int64_t row0, std::int64_t row1, int nthreads, double* out, double* seconds,
                double* counters) {
-    try {
-        auto* pr = static_cast<Prepared*>(handle);
-        double total = 0.0;
-        for (std::int64_t r = row0; r < row1; ++r) {
-            const Tensor& q = pr->q[static_cast<std::size_t>(r)];
-            const ShardedKVCache& cache =
-                pr->caches[static_cast<std::size_t>(pr->cache_of_row[static_cast<std::size_t>(r)])];
-            const auto t0 = std::chrono::steady_clock::now();
-            const DecodeResult res =
-                algo == 0 ? tree_decode(q, cache, pr->topo, to_strategy(strategy), scale, parallel != 0)
-                          : ring_decode(q, cache, pr->topo, scale, parallel != 0);
-            total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            const std::int64_t d = q.extent(3);
-            std::memcpy(out + (r - row0) * d, res.output.data().data(),
-                        sizeof(double) * static_cast<std::size_t>(d));
-            if (counters) {
-                counters[0] = res.cost.elems_sent_total();
-                counters[1] = static_cast<double>(res.cost.wire_elems_total());
-                counters[2] = static_cast<double>(res.cost.peak_elems_per_worker);
-                counters[3] = static_cast<double>(res.cost.rounds);
+    auto* pr = static_cast<Prepared*>(handle);
+    std::vector<std::string> errs(static_cast<std::size_t>(nthreads > 0 ? nthreads : 1));
+    std::vector<int> codes(errs.size(), 0);
+    auto work = [&](int tid, std::int64_t a, std::int64_t b) {
+        try {
+            for (std::int64_t r = a; r < b; ++r) {
+                const Tensor& q = pr->q[static_cast<std::size_t>(r)];
+                const ShardedKVCache& cache =
+                    pr->caches[static_cast<std::size_t>(pr->cache_of_row[static_cast<std::size_t>(r)])];
+                const DecodeResult res =
+                    algo == 0 ? tree_decode(q, cache, pr->topo, to_strategy(strategy), scale, parallel != 0)
+                              : ring_decode(q, cache, pr->topo, scale, parallel != 0);
+                const std::int64_t d = q.extent(3);
+                std::memcpy(out + (r - row0) * d, res.output.data().data(),
+                            sizeof(double) * static_cast<std::size_t>(d));
+                if (counters && r == row0) {
+                    counters[0] = res.cost.elems_sent_total();
+                    counters[1] = static_cast<double>(res.cost.wire_elems_total());
+                    counters[2] = static_cast<double>(res.cost.peak_elems_per_worker);
+                    counters[3] = static_cast<double>(res.cost.rounds);
+                }
             }
+        } catch (const std::invalid_argument& e) {
+            errs[static_cast<std::size_t>(tid)] = e.what();
+            codes[static_cast<std::size_t>(tid)] = -1;
+        } catch (const std::exception& e) {
+            errs[static_cast<std::size_t>(tid)] = e.what();
+            codes[static_cast<std::size_t>(tid)] = -2;
         }
-        if (seconds) *seconds = total;
-        return 0;
-    } catch (const std::invalid_argument& e) {
-        return fail(e, -1);
-    } catch (const std::exception& e) {
-        return fail(e, -2);
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    const int nt = static_cast<int>(errs.size());
+    if (nt == 1) {
+        work(0, row0, row1);
+    } else {
+        std::vector<std::thread> pool;
+        const std::int64_t n = row1 - row0;
+        for (int i = 0; i < nt; ++i)
+            pool.emplace_back(work, i, row0 + n * i / nt, row0 + n * (i + 1) / nt);
+        for (auto& th : pool) th.join();
     }
+    if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (std::size_t i = 0; i < errs.size(); ++i)
+        if (codes[i] != 0) {
+            g_err = errs[i];
+            return codes[i];
+        }
+    return 0;
 }
 
 } // extern "C"

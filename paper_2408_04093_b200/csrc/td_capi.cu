@@ -1,0 +1,719 @@
+// td_capi.cu -- C-ABI of the B200 tree-decode library (include/treedec_b200.h).
+//
+// One td_context per GPU / rank. The tree path is the paper's Algorithm 3
+// as the reference implements it in tree_decode
+// (decode.cpp:100-184): local partial (K1+K2) -> nccl().AllReduce(max) of lse
+// -> K3 rescale -> one fused nccl().AllReduce(sum) of [n|d] -> K4 n/d. The ring
+// path is ring_decode (decode.cpp:186-251) with the KV shards really moving
+// (ncclSend/ncclRecv), overlapped with the partial of the chunk in hand.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "../../include/treedec_b200.h"
+#include "td_internal.h"
+
+using td::SplitPlan;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define TD_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return set_err(TD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define TD_NCCL(call)                                                                    \
+    do {                                                                                 \
+        if (!nccl().ok) return set_err(TD_ENCCL, nccl().err);                            \
+        ncclResult_t r_ = (call);                                                        \
+        if (r_ != ncclSuccess)                                                           \
+            return set_err(TD_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+    } while (0)
+
+// NCCL is resolved at run time: if the process already holds a libnccl.so.2
+// (torch loads its own), that copy is used, so the library never forces a
+// second, older NCCL into a torch process.
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetVersion)(int*) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.err = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        bool all = true;
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            all = all && fn != nullptr;
+        };
+        sym(a.GetUniqueId, "ncclGetUniqueId");
+        sym(a.CommInitRank, "ncclCommInitRank");
+        sym(a.CommDestroy, "ncclCommDestroy");
+        sym(a.AllReduce, "ncclAllReduce");
+        sym(a.Send, "ncclSend");
+        sym(a.Recv, "ncclRecv");
+        sym(a.GroupStart, "ncclGroupStart");
+        sym(a.GroupEnd, "ncclGroupEnd");
+        sym(a.GetErrorString, "ncclGetErrorString");
+        sym(a.GetVersion, "ncclGetVersion");
+        a.ok = all;
+        if (!all) a.err = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+int sm_count_of(int device) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+std::vector<int64_t> chunk_extents(int64_t n, int p) {  // attention.cpp:268-275
+    std::vector<int64_t> ext(static_cast<size_t>(p), n / p);
+    for (int64_t i = 0; i < n % p; ++i) ext[static_cast<size_t>(i)] += 1;
+    return ext;
+}
+
+}  // namespace
+
+struct td_context {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;  // compute
+    cudaStream_t xfer = nullptr;    // ring send/recv
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+
+    // placed KV shard ([b][n_kv][len][d])
+    bool kv_ok = false;
+    int dtype = td::kBF16;
+    int64_t b = 0, n_kv = 0, seq_len = 0, d = 0, start = 0, len = 0;
+    DevBuf k, v;
+    CUtensorMap tmk{}, tmv{};
+    bool tm_ok = false;
+
+    DevBuf ws;                                   // split slots
+    DevBuf rows;                                 // per-row fp32 buffers
+    float *row_max = nullptr, *lse = nullptr, *out_local = nullptr, *shift = nullptr,
+          *nd = nullptr, *out = nullptr, *r_max = nullptr, *r_lse = nullptr, *r_out = nullptr;
+    DevBuf q_dev, out_bf16;
+    DevBuf ring[2][2];                           // [buffer][k|v]
+    std::vector<cudaEvent_t> ring_ev;            // compute-done / recv-done
+
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
+    size_t timers_used = 0;
+
+    int last_kernels = 0;
+    double last_kv_bytes = 0.0;
+    int last_split_kernel = -1;
+};
+
+namespace {
+
+int require_ctx(td_context* ctx) {
+    if (!ctx) return set_err(TD_EINVAL, "null td_context");
+    cudaSetDevice(ctx->device);
+    return TD_OK;
+}
+
+// per-row buffers for rows = b * n_q (max) and d
+int ensure_rows(td_context* ctx, int64_t rows, int64_t d) {
+    const size_t rd = size_t(rows) * size_t(d), r = size_t(rows);
+    // row_max, lse, shift, r_max, r_lse: r each; out_local, out, r_out: rd; nd: rd + r
+    const size_t floats = 5 * r + 3 * rd + (rd + r) + 64;
+    TD_CUDA(ctx->rows.ensure(floats * sizeof(float)));
+    float* f = ctx->rows.as<float>();
+    auto take = [&](size_t n) {
+        float* p = f;
+        f += (n + 15) / 16 * 16;
+        return p;
+    };
+    ctx->row_max = take(r);
+    ctx->lse = take(r);
+    ctx->shift = take(r);
+    ctx->r_max = take(r);
+    ctx->r_lse = take(r);
+    ctx->out_local = take(rd);
+    ctx->out = take(rd);
+    ctx->r_out = take(rd);
+    ctx->nd = take(rd + r);
+    return TD_OK;
+}
+
+int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan) {
+    std::string msg;
+    if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
+    if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), t,
+                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg))
+        return set_err(TD_EINVAL, msg);
+    TD_CUDA(ctx->ws.ensure(plan.workspace_bytes()));
+    return TD_OK;
+}
+
+cudaEvent_t* next_timer(td_context* ctx) {
+    if (ctx->timers_used == ctx->timers.size()) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        ctx->timers.emplace_back(a, b);
+    }
+    return &ctx->timers[ctx->timers_used++].first;
+}
+
+// K1 + K2 over a [b][n_kv][t][d] buffer.
+int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const void* kb,
+                const void* vb, int64_t t, double scale, bool own_maps, float* rmax, float* lse,
+                float* out, bool timed) {
+    CUtensorMap mk, mv;
+    const CUtensorMap *pk = nullptr, *pv = nullptr;
+    if (plan.kernel == 1) {
+        if (own_maps) {
+            pk = &ctx->tmk;
+            pv = &ctx->tmv;
+        } else {
+            std::string msg;
+            const int64_t rows = ctx->b * ctx->n_kv * t;
+            if (!td::make_tensor_map(&mk, kb, rows, static_cast<int>(ctx->d), plan.tile, msg) ||
+                !td::make_tensor_map(&mv, vb, rows, static_cast<int>(ctx->d), plan.tile, msg))
+                return set_err(TD_ECUDA, msg);
+            pk = &mk;
+            pv = &mv;
+        }
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        cudaEvent_t* pr = next_timer(ctx);
+        e0 = pr[0];
+        e1 = pr[1];
+    }
+    TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
+                                      ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
+    ctx->last_kernels += 2;
+    ctx->last_kv_bytes += 2.0 * double(ctx->b) * double(ctx->n_kv) * double(t) * double(ctx->d) *
+                          td::dtype_bytes(ctx->dtype);
+    ctx->last_split_kernel = plan.kernel;
+    return TD_OK;
+}
+
+const void* stage_q(td_context* ctx, const void* q, int64_t n_q, int flags, int* rc) {
+    *rc = TD_OK;
+    if (!(flags & TD_HOST_IO)) return q;
+    const size_t bytes = size_t(ctx->b) * size_t(n_q) * size_t(ctx->d) * td::dtype_bytes(ctx->dtype);
+    cudaError_t e = ctx->q_dev.ensure(bytes);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->q_dev.p, q, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) {
+        *rc = set_err(TD_ECUDA, std::string("q upload: ") + cudaGetErrorString(e));
+        return nullptr;
+    }
+    return ctx->q_dev.p;
+}
+
+int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int flags) {
+    const size_t bytes = size_t(rows) * size_t(ctx->d) * sizeof(float);
+    if (flags & TD_BF16_OUT) {
+        TD_CUDA(ctx->out_bf16.ensure(size_t(rows) * size_t(ctx->d) * 2));
+        TD_CUDA(td::launch_to_bf16(src, rows * ctx->d, ctx->out_bf16.p, ctx->stream));
+        ctx->last_kernels += 1;
+    }
+    if (flags & TD_HOST_IO) {
+        TD_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else if (out != src) {
+        TD_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    return TD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int td_version(void) { return 1; }
+const char* td_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- stateless
+int td_seeded_fill(int dtype, void* dst, uint64_t seed, double scale, int64_t bh_count,
+                   int64_t seq, int64_t start, int64_t len, int64_t d, void* stream) {
+    if (!(scale > 0.0)) return set_err(TD_EINVAL, "seeded_random_tensor: scale must be positive");
+    if (dtype < 0 || dtype > 2 || bh_count < 0 || d < 0 || len < 0 || start < 0 ||
+        start + len > seq)
+        return set_err(TD_EINVAL, "td_seeded_fill: bad arguments");
+    TD_CUDA(td::launch_seeded_fill(dtype, dst, seed, scale, bh_count, seq, start, len, d,
+                                   static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+int td_decode_workspace_bytes(int dtype, int64_t b, int64_t n_q, int64_t n_kv, int64_t t,
+                              int64_t d, size_t* bytes) {
+    SplitPlan plan;
+    std::string msg;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
+                        static_cast<int>(d), sm_count_of(dev), plan, msg))
+        return set_err(TD_EINVAL, msg);
+    *bytes = plan.workspace_bytes();
+    return TD_OK;
+}
+
+int td_decode_partial(int dtype, const void* q, const void* k, const void* v, int64_t b,
+                      int64_t n_q, int64_t n_kv, int64_t t, int64_t d, double scale,
+                      float* row_max, float* lse, float* out, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+    SplitPlan plan;
+    std::string msg;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
+                        static_cast<int>(d), sm_count_of(dev), plan, msg))
+        return set_err(TD_EINVAL, msg);
+    if (workspace_bytes < plan.workspace_bytes())
+        return set_err(TD_EINVAL, "td_decode_partial: workspace too small");
+    CUtensorMap mk, mv;
+    if (plan.kernel == 1) {
+        const int64_t rows = b * n_kv * t;
+        if (!td::make_tensor_map(&mk, k, rows, static_cast<int>(d), plan.tile, msg) ||
+            !td::make_tensor_map(&mv, v, rows, static_cast<int>(d), plan.tile, msg))
+            return set_err(TD_ECUDA, msg);
+    }
+    TD_CUDA(td::launch_decode_partial(plan, q, k, v, static_cast<float>(scale), &mk, &mv, workspace,
+                                      row_max, lse, out, static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+int td_combine_partials(int P, const float* lse, const float* out, int64_t rows, int64_t d,
+                        float* result, void* stream) {
+    if (P < 1) return set_err(TD_EINVAL, "combine_partials: no parts");
+    int* bad = nullptr;
+    TD_CUDA(cudaMalloc(&bad, sizeof(int)));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    cudaError_t e = td::launch_combine_partials(P, lse, out, rows, static_cast<int>(d), result, bad, st);
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(bad);
+    TD_CUDA(e);
+    if (hbad) return set_err(TD_EINVAL, "combine_partials: no keys attended");
+    return TD_OK;
+}
+
+int td_partial_to_numerator(const float* lse, const float* out, const float* shift,
+                            int64_t rows, int64_t d, float* nd, void* stream) {
+    TD_CUDA(td::launch_to_numerator(lse, out, shift, rows, static_cast<int>(d), nd,
+                                    static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+int td_combine_pair(float* l_max, float* l_lse, float* l_out, const float* r_max,
+                    const float* r_lse, const float* r_out, int64_t rows, int64_t d,
+                    void* stream) {
+    TD_CUDA(td::launch_combine_pair(l_max, l_lse, l_out, r_max, r_lse, r_out, rows,
+                                    static_cast<int>(d), static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+int td_finalize(const float* nd, int64_t rows, int64_t d, float* out, void* out_bf16,
+                void* stream) {
+    TD_CUDA(td::launch_finalize(nd, rows, static_cast<int>(d), out, out_bf16,
+                                static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+// ---------------------------------------------------------------- context
+int td_create(int device, td_context** out) {
+    if (!out) return set_err(TD_EINVAL, "td_create: null output");
+    int n = 0;
+    TD_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return set_err(TD_EINVAL, "td_create: no such device");
+    TD_CUDA(cudaSetDevice(device));
+    auto* ctx = new td_context;
+    ctx->device = device;
+    ctx->sm_count = sm_count_of(device);
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->xfer, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return set_err(TD_ECUDA, std::string("td_create: ") + cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return TD_OK;
+}
+
+int td_destroy(td_context* ctx) {
+    if (!ctx) return TD_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->xfer);
+    if (ctx->comm) nccl().CommDestroy(ctx->comm);
+    ctx->k.release();
+    ctx->v.release();
+    ctx->ws.release();
+    ctx->rows.release();
+    ctx->q_dev.release();
+    ctx->out_bf16.release();
+    for (auto& rb : ctx->ring)
+        for (auto& x : rb) x.release();
+    for (auto& ev : ctx->ring_ev) cudaEventDestroy(ev);
+    for (auto& pr : ctx->timers) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->xfer);
+    delete ctx;
+    return TD_OK;
+}
+
+int td_stream(td_context* ctx, void** stream) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *stream = ctx->stream;
+    return TD_OK;
+}
+
+int td_comm_unique_id(unsigned char id[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId uid;
+    TD_NCCL(nccl().GetUniqueId(&uid));
+    std::memcpy(id, &uid, 128);
+    return TD_OK;
+}
+
+int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[128]) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(TD_EINVAL, "td_comm_init: bad rank");
+    if (ctx->comm) {
+        nccl().CommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+    }
+    if (nranks > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        TD_NCCL(nccl().CommInitRank(&ctx->comm, nranks, uid, rank));
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return TD_OK;
+}
+
+int td_comm_info(td_context* ctx, int* nranks, int* rank) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *nranks = ctx->nranks;
+    *rank = ctx->rank;
+    return TD_OK;
+}
+
+static int kv_alloc(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len,
+                    int64_t d, int64_t start, int64_t len) {
+    if (dtype != TD_F32 && dtype != TD_BF16)
+        return set_err(TD_EINVAL, "kv: the GPU path stores f32 or bf16 caches");
+    if (b < 1 || n_kv < 1 || d < 1 || d > 256 || seq_len < 1)
+        return set_err(TD_EINVAL, "kv: dimensions must be positive (head_dim <= 256)");
+    if (start < 0 || len < 0 || start + len > seq_len)
+        return set_err(TD_EINVAL, "kv: shard range out of bounds");
+    const size_t bytes = size_t(b) * size_t(n_kv) * size_t(len) * size_t(d) * td::dtype_bytes(dtype);
+    TD_CUDA(ctx->k.ensure(bytes > 0 ? bytes : 16));
+    TD_CUDA(ctx->v.ensure(bytes > 0 ? bytes : 16));
+    ctx->dtype = dtype;
+    ctx->b = b;
+    ctx->n_kv = n_kv;
+    ctx->seq_len = seq_len;
+    ctx->d = d;
+    ctx->start = start;
+    ctx->len = len;
+    ctx->kv_ok = false;
+    ctx->tm_ok = false;
+    return TD_OK;
+}
+
+static int kv_finish(td_context* ctx) {
+    ctx->tm_ok = false;
+    if (ctx->dtype == TD_BF16 && (ctx->d == 64 || ctx->d == 128 || ctx->d == 256) && ctx->len > 0) {
+        std::string msg;
+        const int64_t rows = ctx->b * ctx->n_kv * ctx->len;
+        SplitPlan plan;
+        if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(ctx->n_kv), static_cast<int>(ctx->n_kv),
+                            ctx->len, static_cast<int>(ctx->d), ctx->sm_count, plan, msg))
+            return set_err(TD_EINVAL, msg);
+        if (!td::make_tensor_map(&ctx->tmk, ctx->k.p, rows, static_cast<int>(ctx->d), plan.tile, msg) ||
+            !td::make_tensor_map(&ctx->tmv, ctx->v.p, rows, static_cast<int>(ctx->d), plan.tile, msg))
+            return set_err(TD_ECUDA, msg);
+        ctx->tm_ok = true;
+    }
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->kv_ok = true;
+    return TD_OK;
+}
+
+int td_kv_place(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len, int64_t d,
+                int64_t start, int64_t len, const void* k, const void* v, int from_host) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (int rc = kv_alloc(ctx, dtype, b, n_kv, seq_len, d, start, len)) return rc;
+    const size_t bytes = size_t(b) * size_t(n_kv) * size_t(len) * size_t(d) * td::dtype_bytes(dtype);
+    const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (bytes) {
+        TD_CUDA(cudaMemcpyAsync(ctx->k.p, k, bytes, kind, ctx->stream));
+        TD_CUDA(cudaMemcpyAsync(ctx->v.p, v, bytes, kind, ctx->stream));
+    }
+    return kv_finish(ctx);
+}
+
+int td_kv_generate(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len,
+                   int64_t d, uint64_t seed_k, uint64_t seed_v, double scale) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (ctx->nranks > seq_len) return set_err(TD_EINVAL, "shard_kv: more workers than keys");
+    const std::vector<int64_t> ext = chunk_extents(seq_len, ctx->nranks);
+    int64_t start = 0;
+    for (int w = 0; w < ctx->rank; ++w) start += ext[static_cast<size_t>(w)];
+    const int64_t len = ext[static_cast<size_t>(ctx->rank)];
+    if (int rc = kv_alloc(ctx, dtype, b, n_kv, seq_len, d, start, len)) return rc;
+    if (int rc = td_seeded_fill(dtype, ctx->k.p, seed_k, scale, b * n_kv, seq_len, start, len, d,
+                                ctx->stream))
+        return rc;
+    if (int rc = td_seeded_fill(dtype, ctx->v.p, seed_v, scale, b * n_kv, seq_len, start, len, d,
+                                ctx->stream))
+        return rc;
+    return kv_finish(ctx);
+}
+
+int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "no KV shard placed");
+    *start = ctx->start;
+    *len = ctx->len;
+    *bytes = 2 * size_t(ctx->b) * size_t(ctx->n_kv) * size_t(ctx->len) * size_t(ctx->d) *
+             td::dtype_bytes(ctx->dtype);
+    return TD_OK;
+}
+
+int td_kv_pointers(td_context* ctx, void** k, void** v) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "no KV shard placed");
+    *k = ctx->k.p;
+    *v = ctx->v.p;
+    return TD_OK;
+}
+
+int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
+                   float* out, int flags) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "tree_decode: no KV shard placed");
+    if (strategy < 0 || strategy > 2) return set_err(TD_EINVAL, "tree_decode: unknown strategy");
+    if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "tree_decode: more workers than keys");
+    if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "tree_decode: q/kv head mismatch");
+    ctx->last_kernels = 0;
+    ctx->last_kv_bytes = 0.0;
+    const int64_t rows = ctx->b * n_q;
+    const int64_t d = ctx->d;
+    if (int rc = ensure_rows(ctx, rows, d)) return rc;
+    SplitPlan plan;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan)) return rc;
+    int rc = TD_OK;
+    const void* qd = stage_q(ctx, q, n_q, flags, &rc);
+    if (rc) return rc;
+    // 1. local partial (out, lse) of this shard
+    if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
+                          ctx->row_max, ctx->lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0)))
+        return rc;
+    const float* result = ctx->out_local;
+    if (ctx->nranks > 1) {
+        // 2. allreduce(max) over lse -> common shift (decode.cpp:129-139)
+        TD_NCCL(nccl().AllReduce(ctx->lse, ctx->shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm,
+                              ctx->stream));
+        // 3. n = o e^(lse-m), d = e^(lse-m) (decode.cpp:150-153)
+        TD_CUDA(td::launch_to_numerator(ctx->lse, ctx->out_local, ctx->shift, rows,
+                                        static_cast<int>(d), ctx->nd, ctx->stream));
+        // 4. one fused sum-allreduce over [n|d] (decode.cpp:154-160); fp32 wire
+        TD_NCCL(nccl().AllReduce(ctx->nd, ctx->nd, size_t(rows * d + rows), ncclFloat32, ncclSum,
+                              ctx->comm, ctx->stream));
+        // 5. out = n / d (decode.cpp:165-173)
+        TD_CUDA(td::launch_finalize(ctx->nd, rows, static_cast<int>(d), ctx->out, nullptr,
+                                    ctx->stream));
+        ctx->last_kernels += 2;
+        result = ctx->out;
+    }
+    return deliver_out(ctx, result, rows, out, flags);
+}
+
+int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
+                   int flags) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "ring_decode: no KV shard placed");
+    if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "ring_decode: more workers than keys");
+    if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "ring_decode: q/kv head mismatch");
+    ctx->last_kernels = 0;
+    ctx->last_kv_bytes = 0.0;
+    const int p = ctx->nranks, w = ctx->rank;
+    const int64_t rows = ctx->b * n_q, d = ctx->d;
+    if (int rc = ensure_rows(ctx, rows, d)) return rc;
+    int rc = TD_OK;
+    const void* qd = stage_q(ctx, q, n_q, flags, &rc);
+    if (rc) return rc;
+    const bool timed = (flags & TD_TIME_KERNELS) != 0;
+    const std::vector<int64_t> ext = chunk_extents(ctx->seq_len, p);
+    const int64_t max_len = ext[0];
+    const size_t esz = td::dtype_bytes(ctx->dtype);
+    const size_t row_bytes = size_t(ctx->b) * size_t(ctx->n_kv) * size_t(d) * esz;
+
+    // own chunk first: root = parts[w]
+    SplitPlan plan;
+    if ((rc = plan_for(ctx, n_q, ctx->len, plan))) return rc;
+    if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
+                          ctx->r_max, ctx->r_lse, ctx->r_out, timed)))
+        return rc;
+    if (p > 1) {
+        for (auto& rb : ctx->ring)
+            for (auto& x : rb) TD_CUDA(x.ensure(max_len * row_bytes > 0 ? max_len * row_bytes : 16));
+        while (ctx->ring_ev.size() < 4) {  // start, recv-done, computed[buf 0], computed[buf 1]
+            cudaEvent_t e;
+            TD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->ring_ev.push_back(e);
+        }
+        const int next = (w + 1) % p, prev = (w - 1 + p) % p;
+        const void* cur_k = ctx->k.p;
+        const void* cur_v = ctx->v.p;
+        int64_t cur_len = ctx->len;
+        // the transfer stream may start only once q/kv are ready on the compute stream
+        TD_CUDA(cudaEventRecord(ctx->ring_ev[0], ctx->stream));
+        TD_CUDA(cudaStreamWaitEvent(ctx->xfer, ctx->ring_ev[0], 0));
+        for (int r = 0; r + 1 < p; ++r) {
+            // worker w holds chunk (w - r) mod p, sends it to w+1, receives (w-1-r) mod p
+            const int in_chunk = ((w - 1 - r) % p + p) % p;
+            const int64_t in_len = ext[static_cast<size_t>(in_chunk)];
+            DevBuf* dst = ctx->ring[r % 2];
+            const size_t out_bytes = size_t(cur_len) * row_bytes, in_bytes = size_t(in_len) * row_bytes;
+            // dst was last read by the partial of step r-2: wait for that compute only,
+            // so this transfer overlaps the partial of step r-1 on the other buffer
+            if (r >= 2) TD_CUDA(cudaStreamWaitEvent(ctx->xfer, ctx->ring_ev[2 + r % 2], 0));
+            TD_NCCL(nccl().GroupStart());
+            TD_NCCL(nccl().Send(cur_k, out_bytes, ncclUint8, next, ctx->comm, ctx->xfer));
+            TD_NCCL(nccl().Send(cur_v, out_bytes, ncclUint8, next, ctx->comm, ctx->xfer));
+            TD_NCCL(nccl().Recv(dst[0].p, in_bytes, ncclUint8, prev, ctx->comm, ctx->xfer));
+            TD_NCCL(nccl().Recv(dst[1].p, in_bytes, ncclUint8, prev, ctx->comm, ctx->xfer));
+            TD_NCCL(nccl().GroupEnd());
+            TD_CUDA(cudaEventRecord(ctx->ring_ev[1], ctx->xfer));
+            // compute on the received chunk once it lands, fold into the root
+            TD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ring_ev[1], 0));
+            SplitPlan pl;
+            if ((rc = plan_for(ctx, n_q, in_len, pl))) return rc;
+            if ((rc = run_partial(ctx, pl, qd, dst[0].p, dst[1].p, in_len, scale, false, ctx->row_max,
+                                  ctx->lse, ctx->out_local, timed)))
+                return rc;
+            TD_CUDA(td::launch_combine_pair(ctx->r_max, ctx->r_lse, ctx->r_out, ctx->row_max,
+                                            ctx->lse, ctx->out_local, rows, static_cast<int>(d),
+                                            ctx->stream));
+            ctx->last_kernels += 1;
+            TD_CUDA(cudaEventRecord(ctx->ring_ev[2 + r % 2], ctx->stream));
+            cur_k = dst[0].p;
+            cur_v = dst[1].p;
+            cur_len = in_len;
+        }
+    }
+    if (p > 1) {  // the last transfer must be done before the next call reuses buffers
+        TD_CUDA(cudaEventRecord(ctx->ring_ev[0], ctx->xfer));
+        TD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ring_ev[0], 0));
+    }
+    return deliver_out(ctx, ctx->r_out, rows, out, flags);
+}
+
+int td_output_bf16(td_context* ctx, const void** out_bf16) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *out_bf16 = ctx->out_bf16.p;
+    return TD_OK;
+}
+
+int td_kernel_time(td_context* ctx, double* mean_ms, int* calls) {
+    if (int rc = require_ctx(ctx)) return rc;
+    double total = 0.0;
+    for (size_t i = 0; i < ctx->timers_used; ++i) {
+        float ms = 0.f;
+        TD_CUDA(cudaEventSynchronize(ctx->timers[i].second));
+        TD_CUDA(cudaEventElapsedTime(&ms, ctx->timers[i].first, ctx->timers[i].second));
+        total += ms;
+    }
+    *calls = static_cast<int>(ctx->timers_used);
+    *mean_ms = ctx->timers_used ? total / double(ctx->timers_used) : 0.0;
+    return TD_OK;
+}
+
+int td_reset_kernel_timer(td_context* ctx) {
+    if (int rc = require_ctx(ctx)) return rc;
+    ctx->timers_used = 0;
+    return TD_OK;
+}
+
+int td_last_launch_stats(td_context* ctx, int* kernels, double* kv_bytes, int* split_kernel) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *kernels = ctx->last_kernels;
+    *kv_bytes = ctx->last_kv_bytes;
+    *split_kernel = ctx->last_split_kernel;
+    return TD_OK;
+}
+
+int td_memory_bytes(td_context* ctx, size_t* bytes) {
+    if (int rc = require_ctx(ctx)) return rc;
+    size_t s = ctx->k.cap + ctx->v.cap + ctx->ws.cap + ctx->rows.cap + ctx->q_dev.cap +
+               ctx->out_bf16.cap;
+    for (auto& rb : ctx->ring)
+        for (auto& x : rb) s += x.cap;
+    *bytes = s;
+    return TD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// td_internal.h -- host-side declarations shared by the kernel launchers
+// (td_kernels.cu) and the C-ABI / context layer (td_capi.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace td {
+
+enum DType { kF64 = 0, kF32 = 1, kBF16 = 2 };
+
+inline int dtype_bytes(int dt) { return dt == kBF16 ? 2 : (dt == kF32 ? 4 : 8); }
+
+// Split-KV work decomposition of one shard (K1). The shard holds bh_count
+// = b * n_kv contiguous rows of t tokens ([bh][t][d], the reference's
+// [b, h, seq, d] row-major layout restricted to this worker's seq range).
+// Tiles of `tile` tokens are numbered bh-major; CTA c owns the contiguous
+// range [c*total/ctas, (c+1)*total/ctas), so every SM gets the same number
+// of tiles (+-1) whatever b, n_kv and t are.
+struct SplitPlan {
+    int64_t bh_count = 0, t = 0, tiles_per_bh = 0, total_tiles = 0;
+    int d = 0, n_q = 0, n_kv = 0, group = 0;
+    int tile = 0, warps = 0, ctas = 0, maxseg = 0;
+    int kernel = 0;  // 0 generic, 1 bf16 mma (TMA), 2 f32 (bulk)
+    int dtype = kBF16;
+    int64_t slots() const { return int64_t(ctas) * warps * maxseg; }
+    // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32)
+    size_t workspace_bytes() const {
+        return sizeof(float) * size_t(slots()) * size_t(group) * size_t(2 + d);
+    }
+};
+
+// Chooses the kernel and grid for a shard. Returns false (with msg) when the
+// shape is unsupported.
+bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
+                SplitPlan& plan, std::string& msg);
+
+// K1 + K2: attention_chunk_partial of q against one shard, written as fp32
+// (row_max, lse, out) rows [b][n_q] / [b][n_q][d]. tmk/tmv are the shard's
+// tensor maps (bf16 mma kernel only; may be null otherwise).
+cudaError_t launch_decode_partial(const SplitPlan& plan, const void* q, const void* k,
+                                  const void* v, float scale, const CUtensorMap* tmk,
+                                  const CUtensorMap* tmv, void* workspace, float* row_max,
+                                  float* lse, float* out, cudaStream_t stream,
+                                  cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+
+// Builds the 2-D tensor map used by the bf16 kernel over rows x d elements.
+bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,
+                     std::string& msg);
+
+// K3: partial_to_numerator; nd = [num rows*d | den rows].
+cudaError_t launch_to_numerator(const float* lse, const float* out, const float* shift,
+                                int64_t rows, int d, float* nd, cudaStream_t stream);
+// K4: out = num / den (+ optional bf16 copy).
+cudaError_t launch_finalize(const float* nd, int64_t rows, int d, float* out, void* out_bf16,
+                            cudaStream_t stream);
+cudaError_t launch_to_bf16(const float* src, int64_t n, void* dst, cudaStream_t stream);
+// K5: combine_pair (left covers lower key indices). In-place into left.
+cudaError_t launch_combine_pair(float* l_max, float* l_lse, float* l_out, const float* r_max,
+                                const float* r_lse, const float* r_out, int64_t rows, int d,
+                                cudaStream_t stream);
+// combine_partials over P partials ([P][rows], [P][rows][d]); *bad_row set
+// to 1 (device int) when some row has no attended key.
+cudaError_t launch_combine_partials(int P, const float* lse, const float* out, int64_t rows,
+                                    int d, float* result, int* bad_row, cudaStream_t stream);
+// K6: element (bh, start+i, j) of seeded_random_tensor([bh_count, seq, d]).
+cudaError_t launch_seeded_fill(int dtype, void* dst, uint64_t seed, double scale,
+                               int64_t bh_count, int64_t seq, int64_t start, int64_t len,
+                               int64_t d, cudaStream_t stream);
+// Casts host-visible f32 to bf16 etc. are not needed on the hot path.
+
+}  // namespace td

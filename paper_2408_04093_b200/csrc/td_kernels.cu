@@ -1,0 +1,1004 @@
+// td_kernels.cu -- sm_100a kernels of the tree-decode hot path.
+//
+//   K1  split-KV flash-decode partial over one KV shard
+//         k1_bf16   bf16 K/V: per-warp TMA (SWIZZLE_128B) pipeline, q.K^T and
+//                   P.V on mma.sync m16n8k16 with tokens on M and the GQA
+//                   group on N; P is split hi+lo bf16 so the P.V product keeps
+//                   fp32 accuracy.
+//         k1_f32    fp32 K/V: per-warp bulk-copy pipeline, CUDA-core FMA,
+//                   batched butterfly reduce-scatter for the scores.
+//         k1_generic any head dim <= 256 (test shapes), plain loads.
+//       contract: attention_chunk_partial, attention.cpp:146-168.
+//   K2  logsumexp combine of the per-warp split states into the shard's
+//       (row_max, lse, out)            -- combine_partials, attention.cpp:207-241
+//   K3  rescale n = o*e^(lse-m), d = e^(lse-m) -- partial_to_numerator :243-266
+//   K4  finalize out = n/d               -- decode.cpp:165-173
+//   K5  pairwise merge                   -- combine_pair, attention.cpp:178-205
+//   K6  seeded generator                 -- seeded_random_tensor, numerics.cpp:41-50
+//
+// Split state ("slot") format shared by all K1 variants: m = running max of
+// the scaled scores in log2 units, l = sum 2^(s - m), o = sum 2^(s - m) v
+// (unnormalised), fp32, one per (cta, warp, segment, head-of-group).
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "td_device.cuh"
+#include "td_internal.h"
+
+namespace td {
+
+struct K1Args {
+    const void* q;  // [b][n_q][d], kv dtype
+    const void* k;  // [bh][t][d]
+    const void* v;
+    int64_t bh_count, t, tiles_per_bh, total_tiles;
+    int d, n_q, n_kv, group, ctas, maxseg;
+    float scale_log2;
+    float* slot_m;  // [slots][group]
+    float* slot_l;
+    float* slot_o;  // [slots][group][d]
+};
+
+__device__ __forceinline__ int64_t cta_begin(int64_t total, int c, int ctas) {
+    return total * c / ctas;
+}
+
+// =========================================================================
+// K1, bf16: tokens on M (16 per m-tile), heads on N (8), d on K.
+// S^T[tok][head] = K[tok][:] . Q[head][:]   (A = K via ldmatrix, B = Q^T regs)
+// O^T[d][head]  += V^T[d][tok] . P^T[tok][head] (A = V^T via ldmatrix.trans)
+// Each warp owns S stages of (K tile, V tile) in shared memory, filled by
+// its lane 0 with 128-B-swizzled TMA boxes; no block-wide sync in the loop.
+// =========================================================================
+template <int D, int T, int W, int S>
+__global__ void __launch_bounds__(W * 32, 1)
+    k1_bf16(const K1Args a, const __grid_constant__ CUtensorMap tmk,
+            const __grid_constant__ CUtensorMap tmv) {
+    constexpr int BOXES = D / 64;           // 128-byte boxes per row
+    constexpr int BOX_BYTES = T * 128;
+    constexpr int TILE_BYTES = BOXES * BOX_BYTES;
+    constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+    constexpr int MT = T / 16;   // m-tiles (tokens) per tile
+    constexpr int KS = D / 16;   // k-steps of q.K
+    constexpr int MD = D / 16;   // m-tiles (d) of P.V
+
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[W][S];
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x;
+    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int64_t span = x1 - x0;
+    const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
+    const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
+    uint8_t* wsm = smem + size_t(warp) * S * STAGE_BYTES;
+
+    if (lane == 0) {
+        if (warp == 0) {
+            prefetch_tmap(&tmk);
+            prefetch_tmap(&tmv);
+        }
+        for (int s = 0; s < S; ++s) mbar_init(&bars[warp][s], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol = policy_evict_first();
+
+    auto issue = [&](int64_t kk, int s) {
+        const int64_t x = x0 + warp + kk * W;
+        const int64_t bh = x / a.tiles_per_bh;
+        const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
+        const int row = static_cast<int>(bh * a.t + tok0);
+        uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
+        uint8_t* vd = kd + TILE_BYTES;
+        mbar_expect_tx(&bars[warp][s], STAGE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < BOXES; ++bx) {
+            tma_load_2d(kd + bx * BOX_BYTES, &tmk, &bars[warp][s], bx * 64, row, pol);
+            tma_load_2d(vd + bx * BOX_BYTES, &tmv, &bars[warp][s], bx * 64, row, pol);
+        }
+    };
+    if (lane == 0)
+        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
+
+    const int hA = 2 * (lane & 3), hB = hA + 1;  // this lane's heads (N columns)
+    const int eta = lane >> 2;                   // B-fragment head / C-fragment row
+    const int srcA = ((lane & 3) << 3) + (eta >> 1), srcB = srcA + 4;
+    const uint32_t sel = (eta & 1) ? 0x7632u : 0x5410u;
+    const int r8 = lane & 7, i4 = lane >> 3;
+
+    float o[MD][4];
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+    uint32_t qf[KS][2];
+    int64_t cur_bh = -1;
+    uint32_t flushed = 0;
+
+    auto load_q = [&](int64_t bh) {
+        const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
+        const bool ok = eta < a.group;
+        const uint16_t* qrow = static_cast<const uint16_t*>(a.q) +
+                               ((b * a.n_q) + kvh * a.group + (ok ? eta : 0)) * int64_t(D);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int col = ks * 16 + 2 * (lane & 3);
+            qf[ks][0] = ok ? *reinterpret_cast<const uint32_t*>(qrow + col) : 0u;
+            qf[ks][1] = ok ? *reinterpret_cast<const uint32_t*>(qrow + col + 8) : 0u;
+        }
+    };
+    auto reset = [&]() {
+#pragma unroll
+        for (int md = 0; md < MD; ++md) o[md][0] = o[md][1] = o[md][2] = o[md][3] = 0.f;
+        m0 = m1 = -CUDART_INF_F;
+        l0 = l1 = 0.f;
+    };
+    auto flush = [&](int seg) {
+        float la = l0, lb = l1;
+        la += __shfl_xor_sync(0xffffffffu, la, 4);
+        la += __shfl_xor_sync(0xffffffffu, la, 8);
+        la += __shfl_xor_sync(0xffffffffu, la, 16);
+        lb += __shfl_xor_sync(0xffffffffu, lb, 4);
+        lb += __shfl_xor_sync(0xffffffffu, lb, 8);
+        lb += __shfl_xor_sync(0xffffffffu, lb, 16);
+        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+        float* sm = a.slot_m + slot * a.group;
+        float* sl = a.slot_l + slot * a.group;
+        float* so = a.slot_o + slot * a.group * int64_t(D);
+        if (lane < 4) {
+            if (hA < a.group) { sm[hA] = m0; sl[hA] = la; }
+            if (hB < a.group) { sm[hB] = m1; sl[hB] = lb; }
+        }
+#pragma unroll
+        for (int md = 0; md < MD; ++md) {
+            const int d0 = md * 16 + eta;
+            if (hA < a.group) {
+                so[hA * D + d0] = o[md][0];
+                so[hA * D + d0 + 8] = o[md][2];
+            }
+            if (hB < a.group) {
+                so[hB * D + d0] = o[md][1];
+                so[hB * D + d0 + 8] = o[md][3];
+            }
+        }
+        flushed |= 1u << seg;
+    };
+
+    reset();
+    for (int64_t kk = 0; kk < nmine; ++kk) {
+        const int s = static_cast<int>(kk % S);
+        const uint32_t phase = static_cast<uint32_t>((kk / S) & 1);
+        const int64_t x = x0 + warp + kk * W;
+        const int64_t bh = x / a.tiles_per_bh;
+        const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
+        if (bh != cur_bh) {
+            if (cur_bh >= 0) {
+                flush(static_cast<int>(cur_bh - bh_first));
+                reset();
+            }
+            cur_bh = bh;
+            load_q(bh);
+        }
+        const int64_t rem = a.t - tok0;
+        const int nvalid = rem < T ? static_cast<int>(rem) : T;
+
+        mbar_wait(&bars[warp][s], phase);
+        const uint32_t kb = smem_u32(wsm + size_t(s) * STAGE_BYTES);
+        const uint32_t vb = kb + TILE_BYTES;
+
+        // ---- S^T = K . Q^T ------------------------------------------------
+        float sc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int bx = (ks * 16) / 64;
+            const int chunk = (((ks * 16) % 64) >> 3) + (i4 >> 1);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int tok = mt * 16 + r8 + (i4 & 1) * 8;
+                const uint32_t addr = kb + bx * BOX_BYTES + tok * 128 + ((chunk ^ r8) << 4);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(addr, a0, a1, a2, a3);
+                mma_bf16(sc[mt], a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
+            }
+        }
+        // ---- online softmax (log2 domain) -----------------------------------
+        float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int tk = mt * 16 + eta;
+            sc[mt][0] = tk < nvalid ? sc[mt][0] * a.scale_log2 : -CUDART_INF_F;
+            sc[mt][1] = tk < nvalid ? sc[mt][1] * a.scale_log2 : -CUDART_INF_F;
+            sc[mt][2] = tk + 8 < nvalid ? sc[mt][2] * a.scale_log2 : -CUDART_INF_F;
+            sc[mt][3] = tk + 8 < nvalid ? sc[mt][3] * a.scale_log2 : -CUDART_INF_F;
+            mx0 = fmaxf(mx0, fmaxf(sc[mt][0], sc[mt][2]));
+            mx1 = fmaxf(mx1, fmaxf(sc[mt][1], sc[mt][3]));
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 4));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 8));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 16));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 4));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 8));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 16));
+        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+        const float c0 = fast_exp2(m0 - n0), c1 = fast_exp2(m1 - n1);
+        m0 = n0;
+        m1 = n1;
+        float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            sc[mt][0] = fast_exp2(sc[mt][0] - n0);
+            sc[mt][1] = fast_exp2(sc[mt][1] - n1);
+            sc[mt][2] = fast_exp2(sc[mt][2] - n0);
+            sc[mt][3] = fast_exp2(sc[mt][3] - n1);
+            ps0 += sc[mt][0] + sc[mt][2];
+            ps1 += sc[mt][1] + sc[mt][3];
+        }
+        l0 = l0 * c0 + ps0;
+        l1 = l1 * c1 + ps1;
+#pragma unroll
+        for (int md = 0; md < MD; ++md) {
+            o[md][0] *= c0;
+            o[md][1] *= c1;
+            o[md][2] *= c0;
+            o[md][3] *= c1;
+        }
+        // ---- P^T as B fragments: hi + lo bf16, transposed with shuffles ------
+        uint32_t bh_[MT][2], bl_[MT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const uint32_t h01 = pack_bf16(sc[mt][0], sc[mt][1]);
+            const uint32_t h23 = pack_bf16(sc[mt][2], sc[mt][3]);
+            const uint32_t g01 = pack_bf16(sc[mt][0] - bf16_lo(h01), sc[mt][1] - bf16_hi(h01));
+            const uint32_t g23 = pack_bf16(sc[mt][2] - bf16_lo(h23), sc[mt][3] - bf16_hi(h23));
+            uint32_t xa = __shfl_sync(0xffffffffu, h01, srcA), xb = __shfl_sync(0xffffffffu, h01, srcB);
+            bh_[mt][0] = __byte_perm(xa, xb, sel);
+            xa = __shfl_sync(0xffffffffu, h23, srcA);
+            xb = __shfl_sync(0xffffffffu, h23, srcB);
+            bh_[mt][1] = __byte_perm(xa, xb, sel);
+            xa = __shfl_sync(0xffffffffu, g01, srcA);
+            xb = __shfl_sync(0xffffffffu, g01, srcB);
+            bl_[mt][0] = __byte_perm(xa, xb, sel);
+            xa = __shfl_sync(0xffffffffu, g23, srcA);
+            xb = __shfl_sync(0xffffffffu, g23, srcB);
+            bl_[mt][1] = __byte_perm(xa, xb, sel);
+        }
+        // ---- O^T += V^T . P^T ------------------------------------------------
+#pragma unroll
+        for (int md = 0; md < MD; ++md) {
+            const int bx = (md * 16) / 64;
+            const int chunk = (((md * 16) % 64) >> 3) + (i4 & 1);
+#pragma unroll
+            for (int kt = 0; kt < MT; ++kt) {
+                const int tok = kt * 16 + r8 + (i4 >> 1) * 8;
+                const uint32_t addr = vb + bx * BOX_BYTES + tok * 128 + ((chunk ^ r8) << 4);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(addr, a0, a1, a2, a3);
+                mma_bf16(o[md], a0, a1, a2, a3, bh_[kt][0], bh_[kt][1]);
+                mma_bf16(o[md], a0, a1, a2, a3, bl_[kt][0], bl_[kt][1]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+    }
+    if (cur_bh >= 0) flush(static_cast<int>(cur_bh - bh_first));
+    // untouched segments are empty partials (m = -inf)
+    for (int seg = 0; seg < a.maxseg; ++seg) {
+        if (flushed & (1u << seg)) continue;
+        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+        for (int h = lane; h < a.group; h += 32) {
+            a.slot_m[slot * a.group + h] = -CUDART_INF_F;
+            a.slot_l[slot * a.group + h] = 0.f;
+        }
+    }
+}
+
+// =========================================================================
+// K1, fp32 (d = 128): lane j owns dims [4j, 4j+4); per-warp bulk-copy ring.
+// Scores of the 32 tokens of a tile are formed with a butterfly
+// reduce-scatter (31 shuffles for 32 tokens) so lane j ends with token j.
+// =========================================================================
+template <int T, int W, int S, int G>
+__global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
+    constexpr int D = 128;
+    static_assert(T == 32, "one token per lane after the reduce-scatter");
+    constexpr int TILE_BYTES = T * D * 4;
+    constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[W][S];
+    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x;
+    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int64_t span = x1 - x0;
+    const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
+    const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
+    const int64_t rows_total = a.bh_count * a.t;
+    uint8_t* wsm = smem + size_t(warp) * S * STAGE_BYTES;
+    const float* kg = static_cast<const float*>(a.k);
+    const float* vg = static_cast<const float*>(a.v);
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[warp][s], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int64_t kk, int s) {
+        const int64_t x = x0 + warp + kk * W;
+        const int64_t bh = x / a.tiles_per_bh;
+        const int64_t row = bh * a.t + (x - bh * a.tiles_per_bh) * T;
+        const int64_t avail = rows_total - row;
+        const uint32_t bytes = static_cast<uint32_t>((avail < T ? avail : T) * D * 4);
+        uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
+        mbar_expect_tx(&bars[warp][s], 2 * bytes);
+        bulk_load(kd, kg + row * D, bytes, &bars[warp][s], pol);
+        bulk_load(kd + TILE_BYTES, vg + row * D, bytes, &bars[warp][s], pol);
+    };
+    if (lane == 0)
+        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
+
+    float qv[G][4], o[G][4], m[G], l[G];
+    int64_t cur_bh = -1;
+    uint32_t flushed = 0;
+    auto load_q = [&](int64_t bh) {
+        const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const float4 qq = reinterpret_cast<const float4*>(
+                static_cast<const float*>(a.q) + ((b * a.n_q) + kvh * G + h) * int64_t(D))[lane];
+            qv[h][0] = qq.x * a.scale_log2;
+            qv[h][1] = qq.y * a.scale_log2;
+            qv[h][2] = qq.z * a.scale_log2;
+            qv[h][3] = qq.w * a.scale_log2;
+        }
+    };
+    auto reset = [&]() {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            o[h][0] = o[h][1] = o[h][2] = o[h][3] = 0.f;
+            m[h] = -CUDART_INF_F;
+            l[h] = 0.f;
+        }
+    };
+    auto flush = [&](int seg) {
+        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            float lt = l[h];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
+            if (lane == 0) {
+                a.slot_m[slot * G + h] = m[h];
+                a.slot_l[slot * G + h] = lt;
+            }
+            reinterpret_cast<float4*>(a.slot_o + (slot * G + h) * int64_t(D))[lane] =
+                make_float4(o[h][0], o[h][1], o[h][2], o[h][3]);
+        }
+        flushed |= 1u << seg;
+    };
+
+    reset();
+    for (int64_t kk = 0; kk < nmine; ++kk) {
+        const int s = static_cast<int>(kk % S);
+        const uint32_t phase = static_cast<uint32_t>((kk / S) & 1);
+        const int64_t x = x0 + warp + kk * W;
+        const int64_t bh = x / a.tiles_per_bh;
+        const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
+        if (bh != cur_bh) {
+            if (cur_bh >= 0) {
+                flush(static_cast<int>(cur_bh - bh_first));
+                reset();
+            }
+            cur_bh = bh;
+            load_q(bh);
+        }
+        const int64_t rem = a.t - tok0;
+        const int nvalid = rem < T ? static_cast<int>(rem) : T;
+        mbar_wait(&bars[warp][s], phase);
+        const float* ks_ = reinterpret_cast<const float*>(wsm + size_t(s) * STAGE_BYTES);
+        const float* vs_ = ks_ + T * D;
+
+        float sc[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            float part[T];
+#pragma unroll
+            for (int tk = 0; tk < T; ++tk) {
+                const float4 kk4 = reinterpret_cast<const float4*>(ks_ + tk * D)[lane];
+                part[tk] = qv[h][0] * kk4.x + qv[h][1] * kk4.y + qv[h][2] * kk4.z + qv[h][3] * kk4.w;
+            }
+            // reduce-scatter: after step k, lane bit k selects the kept half
+#pragma unroll
+            for (int k = 16; k >= 1; k >>= 1) {
+                const bool up = (lane & k) != 0;
+#pragma unroll
+                for (int i = 0; i < k; ++i) {
+                    const float send = up ? part[i] : part[i + k];
+                    const float keep = up ? part[i + k] : part[i];
+                    part[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+                }
+            }
+            sc[h] = lane < nvalid ? part[0] : -CUDART_INF_F;
+        }
+        float p[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            float mx = sc[h];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            const float mn = fmaxf(m[h], mx);
+            const float cr = fast_exp2(m[h] - mn);
+            m[h] = mn;
+            p[h] = fast_exp2(sc[h] - mn);
+            l[h] = l[h] * cr + p[h];
+            o[h][0] *= cr;
+            o[h][1] *= cr;
+            o[h][2] *= cr;
+            o[h][3] *= cr;
+        }
+#pragma unroll 8
+        for (int tk = 0; tk < nvalid; ++tk) {
+            const float4 vv = reinterpret_cast<const float4*>(vs_ + tk * D)[lane];
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                const float pt = __shfl_sync(0xffffffffu, p[h], tk);
+                o[h][0] += pt * vv.x;
+                o[h][1] += pt * vv.y;
+                o[h][2] += pt * vv.z;
+                o[h][3] += pt * vv.w;
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+    }
+    if (cur_bh >= 0) flush(static_cast<int>(cur_bh - bh_first));
+    for (int seg = 0; seg < a.maxseg; ++seg) {
+        if (flushed & (1u << seg)) continue;
+        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+        if (lane < G) {
+            a.slot_m[slot * G + lane] = -CUDART_INF_F;
+            a.slot_l[slot * G + lane] = 0.f;
+        }
+    }
+}
+
+// =========================================================================
+// K1, generic: any d <= 256, bf16 or fp32, any group; one head at a time,
+// 32 tokens per tile (lane = token for scores, lane = dim for P.V).
+// =========================================================================
+template <typename TIn>
+__device__ __forceinline__ float to_f(TIn x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename TIn>
+__global__ void __launch_bounds__(128) k1_generic(const K1Args a, int W) {
+    constexpr int T = 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x;
+    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int64_t span = x1 - x0;
+    const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
+    const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
+    const TIn* q = static_cast<const TIn*>(a.q);
+    const TIn* kg = static_cast<const TIn*>(a.k);
+    const TIn* vg = static_cast<const TIn*>(a.v);
+    const int D = a.d;
+    const int nd = (D + 31) / 32;
+
+    for (int h = 0; h < a.group; ++h) {
+        float o[8], m = -CUDART_INF_F, l = 0.f;
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        int64_t cur_bh = -1;
+        uint32_t flushed = 0;
+        const TIn* qrow = nullptr;
+        auto flush = [&](int seg) {
+            float lt = l;
+            for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
+            const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+            if (lane == 0) {
+                a.slot_m[slot * a.group + h] = m;
+                a.slot_l[slot * a.group + h] = lt;
+            }
+            for (int i = 0; i < nd; ++i) {
+                const int j = lane + 32 * i;
+                if (j < D) a.slot_o[(slot * a.group + h) * D + j] = o[i];
+            }
+            flushed |= 1u << seg;
+        };
+        for (int64_t kk = 0; kk < nmine; ++kk) {
+            const int64_t x = x0 + warp + kk * W;
+            const int64_t bh = x / a.tiles_per_bh;
+            const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
+            if (bh != cur_bh) {
+                if (cur_bh >= 0) {
+                    flush(static_cast<int>(cur_bh - bh_first));
+                    m = -CUDART_INF_F;
+                    l = 0.f;
+                    for (int i = 0; i < 8; ++i) o[i] = 0.f;
+                }
+                cur_bh = bh;
+                const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
+                qrow = q + (b * a.n_q + kvh * a.group + h) * int64_t(D);
+            }
+            const int64_t rem = a.t - tok0;
+            const int nvalid = rem < T ? static_cast<int>(rem) : T;
+            const int64_t row0 = bh * a.t + tok0;
+            float s = -CUDART_INF_F;
+            if (lane < nvalid) {
+                const TIn* kr = kg + (row0 + lane) * D;
+                float acc = 0.f;
+                for (int j = 0; j < D; ++j) acc += to_f(qrow[j]) * to_f(kr[j]);
+                s = acc * a.scale_log2;
+            }
+            float mx = s;
+            for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            const float mn = fmaxf(m, mx);
+            const float cr = fast_exp2(m - mn);
+            m = mn;
+            const float p = fast_exp2(s - mn);
+            l = l * cr + p;
+            for (int i = 0; i < nd; ++i) o[i] *= cr;
+            for (int tk = 0; tk < nvalid; ++tk) {
+                const float pt = __shfl_sync(0xffffffffu, p, tk);
+                const TIn* vr = vg + (row0 + tk) * D;
+                for (int i = 0; i < nd; ++i) {
+                    const int j = lane + 32 * i;
+                    if (j < D) o[i] += pt * to_f(vr[j]);
+                }
+            }
+        }
+        if (cur_bh >= 0) flush(static_cast<int>(cur_bh - bh_first));
+        for (int seg = 0; seg < a.maxseg; ++seg) {
+            if (flushed & (1u << seg)) continue;
+            const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+            if (lane == 0) {
+                a.slot_m[slot * a.group + h] = -CUDART_INF_F;
+                a.slot_l[slot * a.group + h] = 0.f;
+            }
+        }
+    }
+}
+
+// =========================================================================
+// K2: merge the split states of one (b, q-head) row into the shard's
+// partial: out = O/L, lse = (M + log2 L) ln 2, row_max = M ln 2. Empty
+// rows give the identity (-inf, -inf, 0), like attention_chunk_partial on
+// an empty chunk (attention.cpp:56-61). One block of K2_THREADS per row;
+// warps stride over the candidate (cta, warp) slots.
+// =========================================================================
+constexpr int K2_THREADS = 512;
+
+__global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a, int W, float* row_max,
+                                                         float* lse, float* out) {
+    __shared__ float red[K2_THREADS / 32];
+    __shared__ float acc_l[K2_THREADS / 32];
+    __shared__ float acc_o[K2_THREADS / 32][256];
+    const int r = blockIdx.x;  // over bh_count * group
+    const int64_t bh = r / a.group;
+    const int h = r % a.group;
+    const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
+    const int64_t orow = b * a.n_q + kvh * a.group + h;
+    const int D = a.d;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+
+    int64_t c_lo = 0, c_hi = -1;
+    if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
+        const int64_t X = bh * a.tiles_per_bh, Xe = X + a.tiles_per_bh - 1;
+        c_lo = ((X + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
+        c_hi = ((Xe + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
+    }
+    const int64_t ncand = (c_hi - c_lo + 1) * W;
+    auto slot_of = [&](int64_t i) {
+        const int64_t cc = c_lo + i / W;
+        const int ww = static_cast<int>(i % W);
+        const int64_t seg = bh - cta_begin(a.total_tiles, static_cast<int>(cc), a.ctas) / a.tiles_per_bh;
+        return (cc * W + ww) * a.maxseg + seg;
+    };
+    // pass 1: M
+    float mloc = -CUDART_INF_F;
+    for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x)
+        mloc = fmaxf(mloc, a.slot_m[slot_of(i) * a.group + h]);
+    for (int off = 16; off >= 1; off >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
+    if (lane == 0) red[warp] = mloc;
+    __syncthreads();
+    float M = -CUDART_INF_F;
+    for (int i = 0; i < nw; ++i) M = fmaxf(M, red[i]);
+    // pass 2: weighted sums, warp per candidate slot, lanes over d
+    float lsum = 0.f, osum[8];
+    for (int i = 0; i < 8; ++i) osum[i] = 0.f;
+    if (M != -CUDART_INF_F) {
+        for (int64_t i = warp; i < ncand; i += nw) {
+            const int64_t slot = slot_of(i);
+            const float mm = a.slot_m[slot * a.group + h];
+            if (mm == -CUDART_INF_F) continue;
+            const float e = exp2f(mm - M);
+            lsum += e * a.slot_l[slot * a.group + h];
+            const float* so = a.slot_o + (slot * a.group + h) * int64_t(D);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int j = lane + 32 * k;
+                if (j < D) osum[k] += e * so[j];
+            }
+        }
+    }
+    if (lane == 0) acc_l[warp] = lsum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = lane + 32 * k;
+        if (j < D) acc_o[warp][j] = osum[k];
+    }
+    __syncthreads();
+    float L = 0.f;
+    for (int i = 0; i < nw; ++i) L += acc_l[i];
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        float O = 0.f;
+        for (int i = 0; i < nw; ++i) O += acc_o[i][j];
+        out[orow * D + j] = (M == -CUDART_INF_F) ? 0.f : O / L;
+    }
+    if (threadIdx.x == 0) {
+        lse[orow] = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
+        row_max[orow] = (M == -CUDART_INF_F) ? -CUDART_INF_F : M * kLn2;
+    }
+}
+
+// =========================================================================
+// K3 / K4 / K5 / combine_partials / K6
+// =========================================================================
+__global__ void k3_to_numerator(const float* lse, const float* out, const float* shift,
+                                int64_t rows, int d, float* nd) {
+    const int64_t n = rows * d;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n + rows;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i < n ? i / d : i - n;
+        const float l = lse[r];
+        const float w = l == -CUDART_INF_F ? 0.f : expf(l - shift[r]);
+        nd[i] = i < n ? out[i] * w : w;
+    }
+}
+
+__global__ void k4_finalize(const float* nd, int64_t rows, int d, float* out,
+                            __nv_bfloat16* out_bf16) {
+    const int64_t n = rows * d;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float y = nd[i] / nd[n + i / d];
+        out[i] = y;
+        if (out_bf16) out_bf16[i] = __float2bfloat16_rn(y);
+    }
+}
+
+__global__ void k5_combine_pair(float* lmax, float* llse, float* lout, const float* rmax,
+                                const float* rlse, const float* rout, int64_t rows, int d) {
+    const int64_t r = blockIdx.x;
+    if (r >= rows) return;
+    const float la = llse[r], lb = rlse[r];
+    float l;
+    if (la == -CUDART_INF_F) l = lb;
+    else if (lb == -CUDART_INF_F) l = la;
+    else {
+        const float mm = fmaxf(la, lb);
+        l = mm + logf(expf(la - mm) + expf(lb - mm));
+    }
+    const float wa = la == -CUDART_INF_F ? 0.f : expf(la - l);
+    const float wb = lb == -CUDART_INF_F ? 0.f : expf(lb - l);
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+        lout[r * d + j] = lout[r * d + j] * wa + rout[r * d + j] * wb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        llse[r] = l;
+        lmax[r] = fmaxf(lmax[r], rmax[r]);
+    }
+}
+
+__global__ void k_combine_partials(int P, const float* lse, const float* out, int64_t rows, int d,
+                                   float* result, int* bad_row) {
+    const int64_t r = blockIdx.x;
+    if (r >= rows) return;
+    float shift = -CUDART_INF_F;
+    for (int p = 0; p < P; ++p) shift = fmaxf(shift, lse[p * rows + r]);
+    if (shift == -CUDART_INF_F) {
+        if (threadIdx.x == 0) atomicExch(bad_row, 1);
+        for (int j = threadIdx.x; j < d; j += blockDim.x) result[r * d + j] = 0.f;
+        return;
+    }
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        float num = 0.f, den = 0.f;
+        for (int p = 0; p < P; ++p) {
+            const float l = lse[p * rows + r];
+            if (l == -CUDART_INF_F) continue;
+            const float w = expf(l - shift);
+            den += w;
+            num += out[(p * rows + r) * d + j] * w;
+        }
+        result[r * d + j] = num / den;
+    }
+}
+
+__global__ void k6_seeded_fill(int dtype, void* dst, uint64_t seed, double half_width,
+                               int64_t bh_count, int64_t seq, int64_t start, int64_t len,
+                               int64_t d) {
+    const int64_t n = bh_count * len * d;
+    const int64_t per_bh = len * d;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t bh = e / per_bh;
+        const int64_t rem = e - bh * per_bh;
+        const int64_t i = rem / d, j = rem - i * d;
+        const uint64_t gi = static_cast<uint64_t>((bh * seq + start + i) * d + j);
+        const double x = seeded_value(seed, gi, half_width);
+        if (dtype == kBF16) static_cast<uint16_t*>(dst)[e] = double_to_bf16_bits(x);
+        else if (dtype == kF32) static_cast<float*>(dst)[e] = __double2float_rn(x);
+        else static_cast<double*>(dst)[e] = x;
+    }
+}
+
+// =========================================================================
+// host side: planning and launchers
+// =========================================================================
+namespace {
+
+constexpr int kBf16Tile = 32;
+constexpr int kF32Tile = 32, kF32Warps = 3, kF32Stages = 2;
+constexpr int kGenTile = 32, kGenWarps = 4;
+constexpr int kSmemBudget = 192 * 1024;  // per CTA, one CTA per SM
+
+// bf16: W warps x S stages x (K + V tile of kBf16Tile tokens x D)
+constexpr int bf16_warps(int D) { return D >= 256 ? 2 : 4; }
+constexpr int bf16_stage_bytes(int D) { return 2 * (D / 64) * kBf16Tile * 128; }
+constexpr int bf16_stages(int D) { return kSmemBudget / (bf16_warps(D) * bf16_stage_bytes(D)); }
+template <int D>
+size_t bf16_smem() {
+    return size_t(bf16_warps(D)) * bf16_stages(D) * bf16_stage_bytes(D) + 1024;
+}
+size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 * 4 + 128; }
+
+K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
+                 void* ws) {
+    K1Args a{};
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.bh_count = p.bh_count;
+    a.t = p.t;
+    a.tiles_per_bh = p.tiles_per_bh;
+    a.total_tiles = p.total_tiles;
+    a.d = p.d;
+    a.n_q = p.n_q;
+    a.n_kv = p.n_kv;
+    a.group = p.group;
+    a.ctas = p.ctas;
+    a.maxseg = p.maxseg;
+    a.scale_log2 = scale * kLog2e;
+    float* f = static_cast<float*>(ws);
+    const int64_t ns = p.slots() * p.group;
+    a.slot_m = f;
+    a.slot_l = f + ns;
+    a.slot_o = f + 2 * ns;
+    return a;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes));
+}
+
+}  // namespace
+
+bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
+                SplitPlan& p, std::string& msg) {
+    if (b < 1 || n_q < 1 || n_kv < 1 || d < 1 || t < 0) {
+        msg = "decode: dimensions must be positive";
+        return false;
+    }
+    if (n_q % n_kv != 0) {
+        msg = "decode: q heads must be a multiple of kv heads (GQA group)";
+        return false;
+    }
+    if (dtype != kBF16 && dtype != kF32) {
+        msg = "decode: the GPU path computes on bf16 or f32 inputs (f64 unsupported)";
+        return false;
+    }
+    if (d > 256) {
+        msg = "decode: head_dim must be <= 256";
+        return false;
+    }
+    p = SplitPlan{};
+    p.dtype = dtype;
+    p.bh_count = b * n_kv;
+    p.t = t;
+    p.d = d;
+    p.n_q = n_q;
+    p.n_kv = n_kv;
+    p.group = n_q / n_kv;
+    const bool mma_ok = dtype == kBF16 && (d == 64 || d == 128 || d == 256) && p.group <= 8 &&
+                        p.bh_count * t < (int64_t(1) << 31);
+    const bool f32_ok = dtype == kF32 && d == 128 && (p.group == 1 || p.group == 2);
+    if (mma_ok) {
+        p.kernel = 1;
+        p.tile = kBf16Tile;
+        p.warps = bf16_warps(d);
+    } else if (f32_ok) {
+        p.kernel = 2;
+        p.tile = kF32Tile;
+        p.warps = kF32Warps;
+    } else {
+        p.kernel = 0;
+        p.tile = kGenTile;
+        p.warps = kGenWarps;
+    }
+    p.tiles_per_bh = (t + p.tile - 1) / p.tile;
+    p.total_tiles = p.bh_count * p.tiles_per_bh;
+    // one CTA per SM (the per-warp pipelines fill shared memory); never more
+    // CTAs than tiles.
+    int64_t ctas = sm_count;
+    if (p.total_tiles < ctas) ctas = p.total_tiles > 0 ? p.total_tiles : 1;
+    p.ctas = static_cast<int>(ctas);
+    const int64_t per_cta = (p.total_tiles + p.ctas - 1) / p.ctas;
+    const int64_t tpb = p.tiles_per_bh > 0 ? p.tiles_per_bh : 1;
+    p.maxseg = static_cast<int>((per_cta + tpb - 1) / tpb + 1);
+    if (p.maxseg > 32) {
+        msg = "decode: too many (batch, head) rows per CTA for a split plan";
+        return false;
+    }
+    return true;
+}
+
+bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,
+                     std::string& msg) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            !fn) {
+            msg = "cuTensorMapEncodeTiled unavailable";
+            return false;
+        }
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows > 0 ? rows : 1)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(tile_rows)};
+    const cuuint32_t estride[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim,
+                              gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        msg = "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")";
+        return false;
+    }
+    return true;
+}
+
+cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void* k,
+                                  const void* v, float scale, const CUtensorMap* tmk,
+                                  const CUtensorMap* tmv, void* ws, float* row_max, float* lse,
+                                  float* out, cudaStream_t st, cudaEvent_t ev0,
+                                  cudaEvent_t ev1) {
+    const K1Args a = make_args(p, q, k, v, scale, ws);
+    cudaError_t e = cudaSuccess;
+    if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
+    if (p.kernel == 1) {
+        if (!tmk || !tmv) return cudaErrorInvalidValue;
+        switch (p.d) {
+#define TD_LAUNCH_BF16(DD)                                                                  \
+    case DD: {                                                                              \
+        auto kern = k1_bf16<DD, kBf16Tile, bf16_warps(DD), bf16_stages(DD)>;                \
+        const size_t sm = bf16_smem<DD>();                                                  \
+        if ((e = set_smem(kern, sm)) != cudaSuccess) return e;                              \
+        kern<<<p.ctas, bf16_warps(DD) * 32, sm, st>>>(a, *tmk, *tmv);                       \
+        break;                                                                              \
+    }
+            TD_LAUNCH_BF16(64)
+            TD_LAUNCH_BF16(128)
+            TD_LAUNCH_BF16(256)
+#undef TD_LAUNCH_BF16
+        default: return cudaErrorInvalidValue;
+        }
+    } else if (p.kernel == 2) {
+        const size_t sm = f32_smem();
+        switch (p.group) {
+#define TD_LAUNCH_F32(GG)                                                   \
+    case GG: {                                                              \
+        auto kern = k1_f32<kF32Tile, kF32Warps, kF32Stages, GG>;            \
+        if ((e = set_smem(kern, sm)) != cudaSuccess) return e;              \
+        kern<<<p.ctas, kF32Warps * 32, sm, st>>>(a);                        \
+        break;                                                              \
+    }
+            TD_LAUNCH_F32(1)
+            TD_LAUNCH_F32(2)
+#undef TD_LAUNCH_F32
+        default: return cudaErrorInvalidValue;
+        }
+    } else {
+        if (p.dtype == kBF16) k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, 0, st>>>(a, kGenWarps);
+        else k1_generic<float><<<p.ctas, kGenWarps * 32, 0, st>>>(a, kGenWarps);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ev1 && (e = cudaEventRecord(ev1, st)) != cudaSuccess) return e;
+    k2_combine<<<static_cast<unsigned>(p.bh_count * p.group), K2_THREADS, 0, st>>>(a, p.warps, row_max,
+                                                                                   lse, out);
+    return cudaGetLastError();
+}
+
+namespace {
+unsigned grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > 148 * 16) g = 148 * 16;
+    return static_cast<unsigned>(g);
+}
+}  // namespace
+
+cudaError_t launch_to_numerator(const float* lse, const float* out, const float* shift,
+                                int64_t rows, int d, float* nd, cudaStream_t st) {
+    k3_to_numerator<<<grid_for(rows * d + rows, 256), 256, 0, st>>>(lse, out, shift, rows, d, nd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const float* nd, int64_t rows, int d, float* out, void* out_bf16,
+                            cudaStream_t st) {
+    k4_finalize<<<grid_for(rows * d, 256), 256, 0, st>>>(nd, rows, d, out,
+                                                          static_cast<__nv_bfloat16*>(out_bf16));
+    return cudaGetLastError();
+}
+
+__global__ void k_to_bf16(const float* src, int64_t n, __nv_bfloat16* dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+cudaError_t launch_to_bf16(const float* src, int64_t n, void* dst, cudaStream_t st) {
+    if (n < 1) return cudaSuccess;
+    k_to_bf16<<<grid_for(n, 256), 256, 0, st>>>(src, n, static_cast<__nv_bfloat16*>(dst));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine_pair(float* l_max, float* l_lse, float* l_out, const float* r_max,
+                                const float* r_lse, const float* r_out, int64_t rows, int d,
+                                cudaStream_t st) {
+    if (rows < 1) return cudaSuccess;
+    k5_combine_pair<<<static_cast<unsigned>(rows), 128, 0, st>>>(l_max, l_lse, l_out, r_max, r_lse,
+                                                                  r_out, rows, d);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine_partials(int P, const float* lse, const float* out, int64_t rows,
+                                    int d, float* result, int* bad_row, cudaStream_t st) {
+    if (rows < 1) return cudaSuccess;
+    k_combine_partials<<<static_cast<unsigned>(rows), 128, 0, st>>>(P, lse, out, rows, d, result,
+                                                                     bad_row);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seeded_fill(int dtype, void* dst, uint64_t seed, double scale,
+                               int64_t bh_count, int64_t seq, int64_t start, int64_t len,
+                               int64_t d, cudaStream_t st) {
+    const int64_t n = bh_count * len * d;
+    if (n == 0) return cudaSuccess;
+    const double half_width = __builtin_sqrt(3.0) * scale;
+    k6_seeded_fill<<<grid_for(n, 256), 256, 0, st>>>(dtype, dst, seed, half_width, bh_count, seq,
+                                                       start, len, d);
+    return cudaGetLastError();
+}
+
+}  // namespace td

@@ -1,0 +1,510 @@
+"""Host-side mirror of the reference decode API (namespace treedec,
+/root/reference/proj/core/include/treedec/decode.hpp) over the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow the reference:
+
+* ``chunk_extents`` / ``shard_kv``       attention.cpp:268-275, decode.cpp:68-85
+* ``attention_chunk_partial``            attention.cpp:146-168
+* ``combine_partials`` / ``combine_pair`` / ``partial_to_numerator``
+                                          attention.cpp:178-266
+* ``tree_decode`` / ``ring_decode``      decode.cpp:100-251 (single process,
+  p workers on one GPU, like the reference's in-process workers)
+* ``Worker``                             one rank of the real multi-GPU path
+  (one process per GPU, NCCL over NVLink)
+* cost counters                          cluster.cpp:106-131 closed forms
+
+Shape errors raise ``InvalidArgument`` (a ``ValueError``), like the
+reference's ``std::invalid_argument``. Every computation runs in
+libtreedec_b200.so; torch only provides device memory and streams.
+"""
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, field
+
+from . import _capi
+from ._capi import InvalidArgument, check, lib
+
+
+class DType(enum.IntEnum):  # dtype.hpp:13
+    Float64 = 0
+    Float32 = 1
+    Bf16 = 2
+
+
+class ReduceStrategy(enum.IntEnum):  # reduce.hpp:10
+    TreeBinary = 0
+    Ring = 1
+    Hierarchical = 2
+
+
+class DecodeAlgo(enum.IntEnum):  # cluster.hpp:241
+    Ring = 0
+    Tree = 1
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def torch_dtype(dt: DType):
+    torch = _torch()
+    return {DType.Float64: torch.float64, DType.Float32: torch.float32, DType.Bf16: torch.bfloat16}[DType(dt)]
+
+
+def dtype_of(t) -> DType:
+    torch = _torch()
+    m = {torch.float64: DType.Float64, torch.float32: DType.Float32, torch.bfloat16: DType.Bf16}
+    if t.dtype not in m:
+        raise InvalidArgument(_capi.TD_EINVAL, f"unsupported dtype {t.dtype}")
+    return m[t.dtype]
+
+
+def _stream_ptr():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------- host logic
+def chunk_extents(n: int, p: int) -> list[int]:
+    """ceil(n/p) for the first n % p chunks, floor(n/p) for the rest."""
+    if p < 1:
+        raise InvalidArgument(_capi.TD_EINVAL, "chunk_extents: p must be >= 1")
+    if n < 0:
+        raise InvalidArgument(_capi.TD_EINVAL, "chunk_extents: negative length")
+    base, rem = divmod(n, p)
+    return [base + (1 if i < rem else 0) for i in range(p)]
+
+
+def shard_range(n: int, p: int, w: int) -> tuple[int, int]:
+    """[start, start+len) of worker w's contiguous chunk (decode.cpp:68-85)."""
+    ext = chunk_extents(n, p)
+    return sum(ext[:w]), ext[w]
+
+
+@dataclass
+class Topology:  # cluster.hpp:172-183 (link parameters are not modelled on the GPU path)
+    nodes: int = 1
+    gpus_per_node: int = 8
+
+    def world_size(self) -> int:
+        return self.nodes * self.gpus_per_node
+
+
+def topology_for_workers(workers: int) -> Topology:  # cluster.cpp:11-22
+    if workers < 1:
+        raise InvalidArgument(_capi.TD_EINVAL, "topology_for_workers: workers must be >= 1")
+    if workers <= 8:
+        return Topology(1, workers)
+    if workers % 8:
+        raise InvalidArgument(_capi.TD_EINVAL, "topology_for_workers: workers not a multiple of gpus_per_node")
+    return Topology(workers // 8, 8)
+
+
+def peak_memory_formula(algo: DecodeAlgo, b: int, t: int, d: int, n_h: int) -> int:  # cluster.cpp:106-114
+    if algo == DecodeAlgo.Ring:
+        return 4 * b * t * d + 2 * b * d
+    return 2 * b * t * d + 2 * b * d + 2 * b * n_h
+
+
+def comm_volume_formula(algo: DecodeAlgo, b: int, t: float, d: int, n_h: int, p: int) -> float:  # :116-124
+    if algo == DecodeAlgo.Ring:
+        return 2.0 * b * t * d * p
+    return 2.0 * (p - 1) / p * (b * d + 2.0 * b * n_h)
+
+
+def comm_volume_formula_seq(algo: DecodeAlgo, b: int, seq_len: int, d: int, n_h: int, p: int) -> float:
+    if algo == DecodeAlgo.Ring:
+        return float(2 * b * d * seq_len)
+    return comm_volume_formula(algo, b, 0.0, d, n_h, p)
+
+
+def ring_schedule(p: int) -> list[list[tuple[int, int, int]]]:
+    """Per round r: (worker, chunk held, chunk received) -- decode.cpp:213-238."""
+    return [[(w, (w - r) % p, (w - 1 - r) % p) for w in range(p)] for r in range(p - 1)]
+
+
+def ring_fold_order(p: int, w: int = 0) -> list[int]:
+    """Chunk order worker w folds: its own chunk, then w-1, w-2, ... (decode.cpp:214-237)."""
+    return [(w - r) % p for r in range(p)]
+
+
+@dataclass
+class CostAccount:  # cluster.hpp:197-212, reporting conventions of decode.cpp:48-62
+    elems_sent_intra: float = 0.0
+    elems_sent_inter: float = 0.0
+    wire_elems_intra: int = 0
+    wire_elems_inter: int = 0
+    rounds: int = 0
+    peak_elems_per_worker: int = 0
+
+    def elems_sent_total(self) -> float:
+        return self.elems_sent_intra + self.elems_sent_inter
+
+    def wire_elems_total(self) -> int:
+        return self.wire_elems_intra + self.wire_elems_inter
+
+
+def tree_cost(b: int, n_q: int, n_kv: int, seq_len: int, d_h: int, p: int) -> CostAccount:
+    """Counters of one tree decode step (decode.cpp:110-177): convention volume
+    2(p-1)/p (b d + 2 b n_h); wire = 2(p-1) (b d + 2 b n_h) for the 2(p-1)-round
+    single-node schedules; peak = Mem_tree with GQA-corrected KV (n_kv heads)."""
+    d = n_q * d_h
+    t = math.ceil(seq_len / p)
+    vol = comm_volume_formula_seq(DecodeAlgo.Tree, b, seq_len, d, n_q, p)
+    wire = 2 * (p - 1) * (b * d + 2 * b * n_q)
+    peak = 2 * b * t * n_kv * d_h + 2 * b * d + 2 * b * n_q
+    return CostAccount(vol, 0.0, wire, 0, 0, peak)
+
+
+def ring_cost(b: int, n_q: int, n_kv: int, seq_len: int, d_h: int, p: int) -> CostAccount:
+    d_kv = n_kv * d_h
+    t = math.ceil(seq_len / p)
+    vol = float(2 * b * d_kv * seq_len) if p > 1 else 0.0
+    wire = 2 * b * d_kv * seq_len * (p - 1)
+    peak = 4 * b * t * d_kv + 2 * b * n_q * d_h if p > 1 else 2 * b * t * d_kv + 2 * b * n_q * d_h
+    return CostAccount(vol, 0.0, wire, 0, p - 1, peak)
+
+
+# ---------------------------------------------------------------- device primitives
+def seeded_tensor(shape, seed: int, scale: float = 1.0, dtype: DType = DType.Bf16, device="cuda",
+                  start: int = 0, length: int | None = None):
+    """seeded_random_tensor(shape, seed, scale, dtype) on the device, bit-exact
+    (numerics.cpp:41-50). shape is [..., seq, d]; with start/length only rows
+    [start, start+length) of the seq axis are produced (a shard)."""
+    torch = _torch()
+    shape = list(shape)
+    if len(shape) < 2:
+        shape = [1] * (2 - len(shape)) + shape
+    *lead, seq, d = shape
+    bh = math.prod(lead) if lead else 1
+    length = seq - start if length is None else length
+    out = torch.empty(*lead, length, d, dtype=torch_dtype(dtype), device=device)
+    check(lib().td_seeded_fill(int(dtype), out.data_ptr(), seed, scale, bh, seq, start, length, d, _stream_ptr()))
+    return out
+
+
+@dataclass
+class SoftmaxPartial:  # attention.hpp:22-30 (fp32 on the device)
+    row_max: object
+    lse: object
+    out: object
+
+
+def _check_qkv(q, k, v, what):
+    if q.dim() != 3 or k.dim() != 4 or v.shape != k.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: q [b,n_q,d] and k/v [b,n_kv,t,d] required")
+    if k.shape[0] != q.shape[0] or k.shape[3] != q.shape[2] or q.shape[1] % k.shape[1]:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: q/k shape mismatch")
+    if q.dtype != k.dtype or q.dtype != v.dtype:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: dtype mismatch")
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: tensors must live on the GPU")
+
+
+def attention_chunk_partial(q, k, v, scale: float = 1.0) -> SoftmaxPartial:
+    """q [b, n_q, d], k/v [b, n_kv, t, d] (contiguous, bf16 or f32) -> fp32 partial."""
+    torch = _torch()
+    _check_qkv(q, k, v, "attention_chunk_partial")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    b, n_q, d = q.shape
+    n_kv, t = k.shape[1], k.shape[2]
+    ws = _ctypes_size()
+    check(lib().td_decode_workspace_bytes(int(dtype_of(q)), b, n_q, n_kv, t, d, ws))
+    work = torch.empty(max(ws.value, 16), dtype=torch.uint8, device=q.device)
+    rm = torch.empty(b, n_q, dtype=torch.float32, device=q.device)
+    lse = torch.empty(b, n_q, dtype=torch.float32, device=q.device)
+    out = torch.empty(b, n_q, d, dtype=torch.float32, device=q.device)
+    check(lib().td_decode_partial(int(dtype_of(q)), q.data_ptr(), k.data_ptr(), v.data_ptr(), b, n_q, n_kv, t, d,
+                                  float(scale), rm.data_ptr(), lse.data_ptr(), out.data_ptr(), work.data_ptr(),
+                                  work.numel(), _stream_ptr()))
+    return SoftmaxPartial(rm, lse, out)
+
+
+def _ctypes_size():
+    import ctypes
+    return ctypes.c_size_t()
+
+
+def combine_partials(parts: list[SoftmaxPartial]):
+    """Exact n-way combine (attention.cpp:207-241); InvalidArgument if a row
+    attends no key."""
+    torch = _torch()
+    if not parts:
+        raise InvalidArgument(_capi.TD_EINVAL, "combine_partials: no parts")
+    first = parts[0].out
+    for p in parts:
+        if p.out.shape != first.shape:
+            raise InvalidArgument(_capi.TD_EINVAL, "combine_partials: shape mismatch")
+    d = first.shape[-1]
+    rows = first.numel() // d
+    lse = torch.stack([p.lse.reshape(-1) for p in parts]).contiguous()
+    out = torch.stack([p.out.reshape(rows, d) for p in parts]).contiguous()
+    res = torch.empty_like(first, dtype=torch.float32)
+    check(lib().td_combine_partials(len(parts), lse.data_ptr(), out.data_ptr(), rows, d, res.data_ptr(),
+                                    _stream_ptr()))
+    return res
+
+
+def partial_to_numerator(part: SoftmaxPartial, shift):
+    """(numerator, denominator) against a common shift (attention.cpp:243-266)."""
+    torch = _torch()
+    if shift.shape != part.lse.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, "partial_to_numerator: shift shape mismatch")
+    d = part.out.shape[-1]
+    rows = part.lse.numel()
+    nd = torch.empty(rows * d + rows, dtype=torch.float32, device=part.out.device)
+    check(lib().td_partial_to_numerator(part.lse.contiguous().data_ptr(), part.out.contiguous().data_ptr(),
+                                        shift.contiguous().data_ptr(), rows, d, nd.data_ptr(), _stream_ptr()))
+    return nd[: rows * d].view(part.out.shape), nd[rows * d:].view(part.lse.shape)
+
+
+def combine_pair(left: SoftmaxPartial, right: SoftmaxPartial) -> SoftmaxPartial:
+    """Pairwise merge (attention.cpp:178-205); returns a new partial."""
+    if left.out.shape != right.out.shape or left.lse.shape != right.lse.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, "combine_pair: shape mismatch")
+    res = SoftmaxPartial(left.row_max.clone(), left.lse.clone(), left.out.clone())
+    d = left.out.shape[-1]
+    check(lib().td_combine_pair(res.row_max.data_ptr(), res.lse.data_ptr(), res.out.data_ptr(),
+                                right.row_max.contiguous().data_ptr(), right.lse.contiguous().data_ptr(),
+                                right.out.contiguous().data_ptr(), left.lse.numel(), d, _stream_ptr()))
+    return res
+
+
+def finalize(num, den):
+    torch = _torch()
+    d = num.shape[-1]
+    rows = den.numel()
+    nd = torch.cat([num.reshape(-1), den.reshape(-1)]).float().contiguous()
+    out = torch.empty(num.shape, dtype=torch.float32, device=num.device)
+    check(lib().td_finalize(nd.data_ptr(), rows, d, out.data_ptr(), None, _stream_ptr()))
+    return out
+
+
+# ---------------------------------------------------------------- single-process reference API
+@dataclass
+class ShardedKVCache:  # decode.hpp:15-20
+    k_chunks: list
+    v_chunks: list
+    seq_len: int = 0
+
+    def workers(self) -> int:
+        return len(self.k_chunks)
+
+
+def shard_kv(k, v, p: int) -> ShardedKVCache:
+    """Contiguous chunks of the sequence axis (copies, like slice_seq)."""
+    if k.dim() != 4 or v.shape != k.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, "shard_kv: k/v must be rank-4 with equal shapes")
+    n = k.shape[2]
+    if p < 1:
+        raise InvalidArgument(_capi.TD_EINVAL, "shard_kv: p must be >= 1")
+    if p > n:
+        raise InvalidArgument(_capi.TD_EINVAL, "shard_kv: more workers than keys")
+    cache = ShardedKVCache([], [], n)
+    begin = 0
+    for ext in chunk_extents(n, p):
+        cache.k_chunks.append(k[:, :, begin:begin + ext].contiguous())
+        cache.v_chunks.append(v[:, :, begin:begin + ext].contiguous())
+        begin += ext
+    return cache
+
+
+@dataclass
+class DecodeResult:  # decode.hpp:32-38 (+ fp32 output of the GPU path)
+    output: object
+    cost: CostAccount = field(default_factory=CostAccount)
+    collectives: list = field(default_factory=list)
+
+
+def _require(q, cache: ShardedKVCache, topo: Topology, what: str):
+    if q.dim() != 3 and not (q.dim() == 4 and q.shape[2] == 1):
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: single query row required")
+    if cache.workers() == 0:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: empty cache")
+    if cache.workers() != topo.world_size():
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: cache/topology worker count mismatch")
+    return q.reshape(q.shape[0], q.shape[1], q.shape[-1])
+
+
+def tree_decode(q, cache: ShardedKVCache, topo: Topology, strategy: ReduceStrategy = ReduceStrategy.Hierarchical,
+                scale: float = 1.0) -> DecodeResult:
+    """Algorithm 3 with p in-process workers on one GPU: per-worker partials
+    (K1+K2), then max-shift / rescale / sum / divide fused in one combine
+    kernel (the single-device image of the two allreduces)."""
+    q3 = _require(q, cache, topo, "tree_decode")
+    parts = [attention_chunk_partial(q3, k, v, scale) for k, v in zip(cache.k_chunks, cache.v_chunks)]
+    out = combine_partials(parts)
+    b, n_q, d = q3.shape
+    n_kv = cache.k_chunks[0].shape[1]
+    p = cache.workers()
+    return DecodeResult(out, tree_cost(b, n_q, n_kv, cache.seq_len, d, p), [(p - 1, p - 1)] * 2)
+
+
+def ring_decode(q, cache: ShardedKVCache, topo: Topology, scale: float = 1.0) -> DecodeResult:
+    """Ring pass-KV fold order of the reference (worker 0's root)."""
+    q3 = _require(q, cache, topo, "ring_decode")
+    p = cache.workers()
+    parts = [attention_chunk_partial(q3, k, v, scale) for k, v in zip(cache.k_chunks, cache.v_chunks)]
+    root = parts[0]
+    for r in range(p - 1):
+        root = combine_pair(root, parts[(p - 1 - r) % p])
+    b, n_q, d = q3.shape
+    n_kv = cache.k_chunks[0].shape[1]
+    return DecodeResult(root.out, ring_cost(b, n_q, n_kv, cache.seq_len, d, p), [])
+
+
+def decode_tolerance_abs(dtype: DType, ref_max_abs: float) -> float:  # decode.cpp:253-260
+    if dtype == DType.Float32:
+        return 1e-4 * ref_max_abs
+    if dtype == DType.Bf16:
+        return 2e-2 * ref_max_abs
+    return 1e-10
+
+
+# ---------------------------------------------------------------- one rank of the multi-GPU path
+class Worker:
+    """One GPU (one process) holding one contiguous KV shard.
+
+    ``comm`` is None for a world of one, or (nranks, rank, unique_id bytes)
+    from ``Worker.unique_id()`` shared by the caller (torch.distributed is the
+    plumbing: see ``Worker.from_torch_distributed``)."""
+
+    def __init__(self, device: int = 0, comm: tuple[int, int, bytes] | None = None):
+        import ctypes
+        self._ct = ctypes
+        h = ctypes.c_void_p()
+        check(lib().td_create(device, ctypes.byref(h)))
+        self.h = h
+        self.device = device
+        self.nranks, self.rank = 1, 0
+        if comm is not None:
+            nranks, rank, uid = comm
+            check(lib().td_comm_init(self.h, nranks, rank, uid))
+            self.nranks, self.rank = nranks, rank
+        self.n_kv = self.d = self.b = self.seq_len = None
+        self.dtype = None
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        buf = ctypes.create_string_buffer(128)
+        check(lib().td_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, device: int):
+        import torch.distributed as dist
+        nranks, rank = dist.get_world_size(), dist.get_rank()
+        if nranks == 1:
+            return cls(device)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(device, (nranks, rank, obj[0]))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().td_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        s = self._ct.c_void_p()
+        check(lib().td_stream(self.h, self._ct.byref(s)))
+        return s.value or 0
+
+    def _meta(self, dtype, b, n_kv, seq_len, d):
+        self.dtype, self.b, self.n_kv, self.seq_len, self.d = DType(dtype), b, n_kv, seq_len, d
+
+    def generate_kv(self, dtype: DType, b: int, n_kv: int, seq_len: int, d: int, seed_k: int, seed_v: int,
+                    scale: float = 1.0):
+        """This rank's shard of seeded k/v (bit-exact with the reference generator)."""
+        check(lib().td_kv_generate(self.h, int(dtype), b, n_kv, seq_len, d, seed_k, seed_v, scale))
+        self._meta(dtype, b, n_kv, seq_len, d)
+
+    def place_kv(self, k, v, seq_len: int | None = None, start: int | None = None):
+        """Place a [b, n_kv, len, d] shard (torch tensor, host or device) that
+        covers rows [start, start+len) of a cache of seq_len tokens."""
+        b, n_kv, ln, d = k.shape
+        if seq_len is None:
+            seq_len = ln * self.nranks
+        if start is None:
+            start, ext = shard_range(seq_len, self.nranks, self.rank)
+            if ext != ln:
+                raise InvalidArgument(_capi.TD_EINVAL, "place_kv: shard length does not match chunk_extents")
+        k, v = k.contiguous(), v.contiguous()
+        check(lib().td_kv_place(self.h, int(dtype_of(k)), b, n_kv, seq_len, d, start, ln, k.data_ptr(),
+                                v.data_ptr(), 0 if k.is_cuda else 1))
+        self._meta(dtype_of(k), b, n_kv, seq_len, d)
+
+    def kv_info(self):
+        s, n, nb = self._ct.c_int64(), self._ct.c_int64(), self._ct.c_size_t()
+        check(lib().td_kv_info(self.h, self._ct.byref(s), self._ct.byref(n), self._ct.byref(nb)))
+        return s.value, n.value, nb.value
+
+    def _sync_in(self, x):
+        if x is not None and x.is_cuda:
+            _torch().cuda.current_stream().synchronize()
+
+    def _decode(self, fn, q, scale, out, flags, *extra):
+        torch = _torch()
+        q = q.reshape(q.shape[0], q.shape[1], q.shape[-1]).contiguous()
+        n_q = q.shape[1]
+        host = not q.is_cuda
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device="cpu" if host else q.device,
+                              pin_memory=host)
+        if host:
+            flags |= _capi.TD_HOST_IO
+        self._sync_in(q)
+        rc = fn(self.h, q.data_ptr(), n_q, float(scale), *extra, out.data_ptr(), flags)
+        check(rc)
+        if not host:
+            torch.cuda.ExternalStream(self.stream).synchronize()
+        return out
+
+    def tree_decode(self, q, scale: float = 1.0, strategy: ReduceStrategy = ReduceStrategy.Hierarchical,
+                    out=None, flags: int = 0):
+        """Algorithm 3 across the ranks (decode.cpp:100-184); fp32 output on every rank."""
+        L = lib()
+        return self._decode(lambda h, qp, nq, sc, st, op, fl: L.td_tree_decode(h, qp, nq, sc, st, op, fl),
+                            q, scale, out, flags, int(strategy))
+
+    def ring_decode(self, q, scale: float = 1.0, out=None, flags: int = 0):
+        """Ring pass-KV comparison (decode.cpp:186-251)."""
+        L = lib()
+        return self._decode(lambda h, qp, nq, sc, op, fl: L.td_ring_decode(h, qp, nq, sc, op, fl),
+                            q, scale, out, flags)
+
+    # -- async launch (no synchronisation) for timing loops ----------------
+    def tree_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0,
+                          strategy: int = 2):
+        check(lib().td_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags))
+
+    def ring_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0):
+        check(lib().td_ring_decode(self.h, q_ptr, n_q, float(scale), out_ptr, flags))
+
+    def kernel_time(self) -> tuple[float, int]:
+        ms, n = self._ct.c_double(), self._ct.c_int()
+        check(lib().td_kernel_time(self.h, self._ct.byref(ms), self._ct.byref(n)))
+        return ms.value, n.value
+
+    def reset_kernel_timer(self):
+        check(lib().td_reset_kernel_timer(self.h))
+
+    def last_launch_stats(self) -> tuple[int, float, int]:
+        k, by, sk = self._ct.c_int(), self._ct.c_double(), self._ct.c_int()
+        check(lib().td_last_launch_stats(self.h, self._ct.byref(k), self._ct.byref(by), self._ct.byref(sk)))
+        return k.value, by.value, sk.value
+
+    def memory_bytes(self) -> int:
+        n = self._ct.c_size_t()
+        check(lib().td_memory_bytes(self.h, self._ct.byref(n)))
+        return n.value

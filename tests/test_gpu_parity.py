@@ -1,0 +1,266 @@
+"""GPU parity of the B200 decode path against the CPU oracle.
+
+Parity rule: inputs are generated with the
+reference generator and rounded to the data dtype; the oracle is the
+reference algorithm run in Float64 on those same values; the GPU result is
+compared in fp32 with max|gpu - ref| <= tol * max|ref|, tol = 1e-3 for bf16
+inputs and 1e-5 for fp32 inputs (BASELINE.json north_star).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import make_inputs, rel_err
+from oracle.oracle import BF16, F32, F64, HIER
+
+pytestmark = pytest.mark.gpu
+
+TOL = {BF16: 1e-3, F32: 1e-5}
+
+
+@pytest.fixture(scope="module")
+def td(lib):
+    import paper_2408_04093_b200 as td
+    return td
+
+
+def dev(x, dtype):
+    import torch
+    tdt = {BF16: torch.bfloat16, F32: torch.float32, F64: torch.float64}[dtype]
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda").to(tdt)
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+# ---------------------------------------------------------------- K6 generator
+@pytest.mark.parametrize("dtype", [BF16, F32, F64])
+@pytest.mark.parametrize("seed", [0, 1, 2 ** 64 - 1, 0x9E3779B97F4A7C15])
+def test_generator_bit_exact(td, oracle, dtype, seed):
+    import torch
+    shape = [2, 3, 257, 16]
+    t = td.seeded_tensor(shape, seed, 1.0, td.DType(dtype))
+    want = oracle.seeded(seed, int(np.prod(shape)), dtype).reshape(shape)
+    got = t.double().cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    # a shard (rows [start, start+len) of every (b, h)) is the slice of the whole
+    sh = td.seeded_tensor(shape, seed, 0.5, td.DType(dtype), start=100, length=57)
+    whole = oracle.seeded(seed, int(np.prod(shape)), dtype, scale=0.5).reshape(shape)
+    assert np.array_equal(sh.double().cpu().numpy(), whole[:, :, 100:157])
+    torch.cuda.synchronize()
+
+
+def test_generator_rejects_bad_scale(td):
+    with pytest.raises(td.InvalidArgument):
+        td.seeded_tensor([4, 4], 1, 0.0)
+
+
+# ---------------------------------------------------------------- K1 + K2 partial
+PARTIAL_CASES = [
+    # dtype, b, n_q, n_kv, t, d, scale
+    (BF16, 1, 1, 1, 1, 128, 1.0),
+    (BF16, 1, 4, 1, 17, 128, 1.0),
+    (BF16, 1, 32, 8, 4096, 128, 1.0),
+    (BF16, 2, 8, 8, 1000, 128, 1 / math.sqrt(128)),
+    (BF16, 1, 64, 8, 3000, 128, 1.0),
+    (BF16, 3, 16, 2, 555, 64, 1.0),
+    (BF16, 1, 4, 2, 300, 256, 1.0),
+    (BF16, 1, 2, 1, 65536, 128, 1.0),
+    (F32, 1, 1, 1, 65536, 128, 1.0),
+    (F32, 2, 4, 2, 999, 128, 1.0),
+    (F32, 1, 2, 2, 33, 128, 1 / math.sqrt(128)),
+    (F32, 1, 2, 2, 40, 8, 1.0),       # generic kernel (reference test shapes)
+    (BF16, 1, 2, 2, 96, 8, 1.0),
+    (BF16, 1, 3, 1, 50, 4, 0.5),
+    (F32, 2, 16, 16, 64, 100, 1.0),   # ragged head dim
+    (BF16, 1, 16, 1, 200, 128, 1.0),  # group 16 -> generic
+]
+
+
+@pytest.mark.parametrize("case", PARTIAL_CASES, ids=lambda c: "-".join(map(str, c)))
+def test_chunk_partial_matches_oracle(td, oracle, case):
+    dtype, b, n_q, n_kv, t, d, scale = case
+    q, k, v = make_inputs(oracle, 7 + t, b, n_q, n_kv, t, d, dtype)
+    part = td.attention_chunk_partial(dev(q, dtype), dev(k, dtype), dev(v, dtype), scale)
+    m, lse, out = oracle.chunk_partial(q, k, v, 0, t, scale, F64, nthreads=8)
+    assert rel_err(host(part.out), out) <= TOL[dtype]
+    # lse / row_max are fp32 statistics: compare in absolute terms
+    assert np.max(np.abs(host(part.lse) - lse)) <= 1e-5 * max(1.0, np.max(np.abs(lse)))
+    assert np.max(np.abs(host(part.row_max) - m)) <= 1e-5 * max(1.0, np.max(np.abs(m)))
+
+
+def test_empty_chunk_is_identity(td, oracle):
+    import torch
+    q, k, v = make_inputs(oracle, 9, 1, 4, 1, 5, 128, BF16)
+    part = td.attention_chunk_partial(dev(q, BF16), dev(k, BF16)[:, :, :0], dev(v, BF16)[:, :, :0])
+    assert torch.isneginf(part.lse).all() and torch.isneginf(part.row_max).all()
+    assert (part.out == 0).all()
+
+
+def test_single_key_returns_value_row(td, oracle):
+    q, k, v = make_inputs(oracle, 1, 1, 8, 8, 1, 128, BF16)
+    part = td.attention_chunk_partial(dev(q, BF16), dev(k, BF16), dev(v, BF16))
+    assert np.array_equal(host(part.out), v[:, :, 0, :])
+
+
+def test_zero_query_averages_values(td, oracle):
+    q, k, v = make_inputs(oracle, 2, 1, 4, 4, 1000, 128, F32)
+    part = td.attention_chunk_partial(dev(np.zeros_like(q), F32), dev(k, F32), dev(v, F32))
+    assert rel_err(host(part.out), v.mean(axis=2)) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_large_score_is_stable(td, oracle, dtype):
+    """attention.cpp test: a +300 score must not overflow the accumulation."""
+    q, k, v = make_inputs(oracle, 55, 1, 1, 1, 600, 128, dtype)
+    q[:] = 0.0
+    q[0, 0, 0] = 1.0
+    k[0, 0, 5, 0] = 300.0
+    part = td.attention_chunk_partial(dev(q, dtype), dev(k, dtype), dev(v, dtype))
+    _, lse, out = oracle.chunk_partial(q, k, v, 0, 600, 1.0, F64)
+    got = host(part.out)
+    assert np.isfinite(got).all()
+    assert rel_err(got, out) <= TOL[dtype]
+
+
+def test_partial_rejects_bad_shapes(td, oracle):
+    import torch
+    q, k, v = make_inputs(oracle, 13, 1, 2, 2, 6, 128, BF16)
+    with pytest.raises(td.InvalidArgument):
+        td.attention_chunk_partial(dev(q, BF16), dev(k, BF16)[..., :64], dev(v, BF16))
+    with pytest.raises(td.InvalidArgument):
+        td.attention_chunk_partial(dev(q, BF16), dev(k, BF16), dev(v, F32))
+    with pytest.raises(td.InvalidArgument):  # 3 q heads over 2 kv heads
+        td.attention_chunk_partial(dev(q, BF16)[:, :1].expand(1, 3, 128).contiguous(), dev(k, BF16), dev(v, BF16))
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- combine primitives
+def test_combine_partials_partition_invariant(td, oracle):
+    """attention.cpp test: {4,4}, {1,7}, {2,2,2,2} partitions combine to the kernel."""
+    import torch
+    q, k, v = make_inputs(oracle, 10, 1, 2, 2, 8 * 512, 128, BF16)
+    ref = oracle.attention_naive(q, k, v)
+    qd, kd, vd = dev(q, BF16), dev(k, BF16), dev(v, BF16)
+    for sizes in ([4, 4], [1, 7], [2, 2, 2, 2]):
+        parts, begin = [], 0
+        for s in sizes:
+            ext = s * 512
+            parts.append(td.attention_chunk_partial(qd, kd[:, :, begin:begin + ext].contiguous(),
+                                                    vd[:, :, begin:begin + ext].contiguous()))
+            begin += ext
+        assert rel_err(host(td.combine_partials(parts)), ref) <= 1e-3
+    # pairwise fold, left to right
+    fold = parts[0]
+    for p_ in parts[1:]:
+        fold = td.combine_pair(fold, p_)
+    assert rel_err(host(fold.out), ref) <= 1e-3
+    # all-empty rows are rejected like the reference (invalid_argument)
+    empty = td.SoftmaxPartial(torch.full_like(parts[0].lse, -math.inf), torch.full_like(parts[0].lse, -math.inf),
+                              torch.zeros_like(parts[0].out))
+    with pytest.raises(td.InvalidArgument):
+        td.combine_partials([empty])
+    # identity absorbs exactly
+    right = td.combine_pair(parts[0], empty)
+    assert torch.equal(right.out, parts[0].out) and torch.equal(right.lse, parts[0].lse)
+
+
+def test_numerator_and_finalize(td, oracle):
+    import torch
+    q, k, v = make_inputs(oracle, 11, 1, 4, 4, 2000, 128, F32)
+    qd, kd, vd = dev(q, F32), dev(k, F32), dev(v, F32)
+    parts = [td.attention_chunk_partial(qd, kd[:, :, a:a + 500].contiguous(), vd[:, :, a:a + 500].contiguous())
+             for a in range(0, 2000, 500)]
+    shift = torch.stack([p_.lse for p_ in parts]).amax(0)
+    nds = [td.partial_to_numerator(p_, shift) for p_ in parts]
+    num = sum(n for n, _ in nds)
+    den = sum(d_ for _, d_ in nds)
+    out = td.finalize(num, den)
+    assert rel_err(host(out), oracle.attention_naive(q, k, v)) <= 1e-5
+
+
+# ---------------------------------------------------------------- single-process tree / ring
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_tree_decode_grid(td, oracle, dtype):
+    """test_decode.cpp:44-58 / acceptance criterion 3 grid at GPU shapes."""
+    for n in (17, 64, 1024, 5000):
+        q, k, v = make_inputs(oracle, 2 + n, 1, 8, 2, n, 128, dtype)
+        qd, kd, vd = dev(q, dtype), dev(k, dtype), dev(v, dtype)
+        for p in (1, 2, 3, 4, 7, 8, 16):
+            if p > n:
+                continue
+            want = oracle.tree_decode(q, k, v, p, HIER, 1.0, F64)
+            cache = td.shard_kv(kd, vd, p)
+            topo = td.topology_for_workers(p)
+            tree = td.tree_decode(qd, cache, topo).output
+            ring = td.ring_decode(qd, cache, topo).output
+            assert rel_err(host(tree), want) <= TOL[dtype], (n, p)
+            assert rel_err(host(ring), want) <= TOL[dtype], (n, p)
+
+
+def test_tree_decode_validation(td, oracle):
+    q, k, v = make_inputs(oracle, 12, 1, 2, 2, 16, 128, BF16)
+    qd, kd, vd = dev(q, BF16), dev(k, BF16), dev(v, BF16)
+    cache = td.shard_kv(kd, vd, 4)
+    with pytest.raises(td.InvalidArgument):
+        td.tree_decode(qd, cache, td.topology_for_workers(8))
+    with pytest.raises(td.InvalidArgument):
+        td.ring_decode(qd, cache, td.topology_for_workers(2))
+    with pytest.raises(td.InvalidArgument):
+        td.shard_kv(kd, vd, 17)
+    with pytest.raises(td.InvalidArgument):
+        td.shard_kv(kd, vd, 0)
+    with pytest.raises(td.InvalidArgument):
+        td.tree_decode(qd, td.ShardedKVCache([], [], 0), td.topology_for_workers(1))
+
+
+def test_decode_is_deterministic(td, oracle):
+    import torch
+    q, k, v = make_inputs(oracle, 9, 1, 32, 8, 40000, 128, BF16)
+    qd, kd, vd = dev(q, BF16), dev(k, BF16), dev(v, BF16)
+    cache = td.shard_kv(kd, vd, 8)
+    a = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+    b = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+    assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------- the Worker (C-ABI context) path
+@pytest.mark.parametrize("dtype,n_q,n_kv,n", [(F32, 1, 1, 65536), (BF16, 32, 8, 262144), (BF16, 8, 8, 70001)])
+def test_worker_generate_and_decode(td, oracle, dtype, n_q, n_kv, n):
+    """cfg1 at full size; GQA / MHA at reduced length. Inputs generated on the
+    device with the bit-exact generator, oracle on the same seeds."""
+    import torch
+    seed = oracle.mix64(0, n)  # data_seed = mix64(seed, N), bench.cpp:73
+    w = td.Worker(0)
+    w.generate_kv(td.DType(dtype), 1, n_kv, n, 128, oracle.mix64(seed, 2), oracle.mix64(seed, 3))
+    q = oracle.seeded(oracle.mix64(seed, 1), n_q * 128, dtype).reshape(1, n_q, 128)
+    out = w.tree_decode(dev(q, dtype))
+    # oracle on the first kv head's query group only (bounded CPU work)
+    g = n_q // n_kv
+    k0 = oracle.seeded(oracle.mix64(seed, 2), n * 128, dtype).reshape(1, 1, n, 128)
+    v0 = oracle.seeded(oracle.mix64(seed, 3), n * 128, dtype).reshape(1, 1, n, 128)
+    want = oracle.tree_decode(np.ascontiguousarray(q[:, :g]), k0, v0, 1, HIER, 1.0, F64, nthreads=8)
+    assert rel_err(host(out[:, :g]), want) <= TOL[dtype]
+    # host buffers through the same call (the e2e path)
+    out_h = w.tree_decode(torch.from_numpy(np.ascontiguousarray(q)).to(dev(q, dtype).dtype))
+    assert torch.equal(out_h, out.cpu())
+    kernels, kv_bytes, split = w.last_launch_stats()
+    assert kernels >= 2 and kv_bytes == 2 * n_kv * n * 128 * (2 if dtype == BF16 else 4)
+    w.close()
+
+
+def test_worker_place_matches_generate(td, oracle):
+    import torch
+    q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
+    w = td.Worker(0)
+    w.place_kv(dev(k, BF16), dev(v, BF16))
+    a = w.tree_decode(dev(q, BF16))
+    w.place_kv(torch.from_numpy(k).to(torch.bfloat16), torch.from_numpy(v).to(torch.bfloat16))  # from host
+    b = w.tree_decode(dev(q, BF16))
+    assert torch.equal(a, b)
+    assert rel_err(host(a), oracle.tree_decode(q, k, v, 1, HIER, 1.0, F64)) <= 1e-3
+    r = w.ring_decode(dev(q, BF16))  # p = 1: ring is the local partial
+    assert torch.equal(r, a)
+    w.close()
