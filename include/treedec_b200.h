@@ -151,6 +151,13 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
 int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
                    int flags);
 
+/* local_partials (decode.cpp:28-46) for this rank alone: the
+ * attention_chunk_partial of q against the placed shard, fp32 row_max /
+ * lse [b, n_q] and out [b, n_q, d]. TD_HOST_IO: q and the outputs are host
+ * pointers. */
+int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, float* row_max,
+                     float* lse, float* out, int flags);
+
 /* bf16 copy of the last output (TD_BF16_OUT), device pointer. */
 int td_output_bf16(td_context* ctx, const void** out_bf16);
 

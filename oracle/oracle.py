@@ -44,6 +44,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         targets.append("ref")
+        product = os.path.join(os.path.dirname(HERE), "paper_2408_04093_b200", "libtreedec_b200.so")
+        if os.path.exists(product):
+            targets.append("shim")  # the C++ drop-in check (tests/cpp/shim_parity.cpp)
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 

@@ -591,6 +591,34 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     return deliver_out(ctx, result, rows, out, flags);
 }
 
+int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, float* row_max,
+                     float* lse, float* out, int flags) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "local_partial: no KV shard placed");
+    if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "local_partial: q/kv head mismatch");
+    ctx->last_kernels = 0;
+    ctx->last_kv_bytes = 0.0;
+    const int64_t rows = ctx->b * n_q, d = ctx->d;
+    if (int rc = ensure_rows(ctx, rows, d)) return rc;
+    SplitPlan plan;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan)) return rc;
+    int rc = TD_OK;
+    const void* qd = stage_q(ctx, q, n_q, flags, &rc);
+    if (rc) return rc;
+    const bool host = (flags & TD_HOST_IO) != 0;
+    if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
+                          host ? ctx->r_max : row_max, host ? ctx->r_lse : lse,
+                          host ? ctx->r_out : out, (flags & TD_TIME_KERNELS) != 0)))
+        return rc;
+    if (host) {
+        TD_CUDA(cudaMemcpyAsync(row_max, ctx->r_max, rows * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        TD_CUDA(cudaMemcpyAsync(lse, ctx->r_lse, rows * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        TD_CUDA(cudaMemcpyAsync(out, ctx->r_out, rows * d * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return TD_OK;
+}
+
 int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
                    int flags) {
     if (int rc = require_ctx(ctx)) return rc;

@@ -1,0 +1,74 @@
+#!/usr/bin/env python3
+"""Multi-GPU parity check, one process per GPU (launched by torchrun; used by
+tests/test_gpu_multi.py). Every rank generates its own shard of the seeded
+cache on its GPU, runs the NCCL tree decode and the ring pass-KV decode, and
+rank 0 compares both against the CPU oracle (reference algorithm in Float64
+on the same bf16 / f32 values) over the first kv group's query heads.
+
+Prints one JSON line per rank-0 case; exits non-zero on any parity failure.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_04093_b200 as td
+    from oracle.oracle import BF16, F32, F64, HIER, Oracle
+
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    orc = Oracle()
+    w = td.Worker.from_torch_distributed(local)
+    cases = [  # dtype, b, n_q, n_kv, n, d, scale
+        (BF16, 1, 32, 8, 262144 + 3, 128, 1.0),
+        (BF16, 2, 8, 8, 20001, 128, 0.0883883476),
+        (F32, 1, 2, 2, 65536, 128, 1.0),
+        (BF16, 1, 4, 2, 3 * world + 1, 64, 1.0),   # tiny shards, ragged extents
+    ]
+    ok = True
+    for dt, b, n_q, n_kv, n, d, scale in cases:
+        seed = orc.mix64(0, n)
+        w.generate_kv(td.DType(dt), b, n_kv, n, d, orc.mix64(seed, 2), orc.mix64(seed, 3))
+        q = td.seeded_tensor([b, n_q, d], orc.mix64(seed, 1), 1.0, td.DType(dt))
+        tree = w.tree_decode(q, scale)
+        ring = w.ring_decode(q, scale)
+        # every rank must hold the same output
+        t_all = [torch.empty_like(tree) for _ in range(world)]
+        dist.all_gather(t_all, tree)
+        if rank == 0:
+            g = n_q // n_kv
+            qh = orc.seeded(orc.mix64(seed, 1), b * n_q * d, dt).reshape(b, n_q, d)
+            k0 = np.stack([orc.seeded(orc.mix64(seed, 2), n * d, dt, offset=bi * n_kv * n * d) for bi in range(b)]
+                          ).reshape(b, 1, n, d)
+            v0 = np.stack([orc.seeded(orc.mix64(seed, 3), n * d, dt, offset=bi * n_kv * n * d) for bi in range(b)]
+                          ).reshape(b, 1, n, d)
+            want = orc.tree_decode(np.ascontiguousarray(qh[:, :g]), k0, v0, world, HIER, scale, F64, nthreads=8)
+            tol = 1e-3 if dt == BF16 else 1e-5
+            mx = np.max(np.abs(want))
+            e_tree = float(np.max(np.abs(tree[:, :g].double().cpu().numpy() - want)) / mx)
+            e_ring = float(np.max(np.abs(ring[:, :g].double().cpu().numpy() - want)) / mx)
+            same = all(torch.equal(t_all[0], x) for x in t_all)
+            good = e_tree <= tol and e_ring <= tol and same
+            ok &= good
+            print(json.dumps({"world": world, "dtype": "bf16" if dt == BF16 else "f32", "n": n, "b": b, "n_q": n_q,
+                              "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring,
+                              "ranks_agree": same, "ok": good}), flush=True)
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0)
+    w.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
