@@ -54,9 +54,12 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
     ap.add_argument("--seq-len", type=int, default=None)
     ap.add_argument("--algo", choices=["tree", "ring"], default="tree")
+    ap.add_argument("--combine", choices=["nccl", "p2p"], default="nccl",
+                    help="tree exchange: two NCCL allreduces (paper-literal) or one-shot NVLink push")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=None)
+    ap.add_argument("--phases", action="store_true", help="add a per-phase breakdown (phases_us)")
     return ap.parse_args()
 
 
@@ -157,13 +160,13 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------- CPU reference (oracle/_ref)
-def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1):
+def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
     """Times the reference's own tree_decode (compiled from /root/reference by
-    oracle/Makefile) on a bounded sample: `sample_heads` q-heads of one kv
-    group at the full sequence length, p = n_gpus workers, rows spread over
-    nthreads host threads; scaled to the full head count."""
-    import numpy as np
-
+    oracle/Makefile into oracle/_ref) on a bounded sample: `sample_heads`
+    q-heads of kv head 0 at the full sequence length, p = n_gpus workers
+    (parallel_workers when p > 1), the sampled rows spread over `nthreads` host
+    threads; scaled linearly to all b * n_q rows. Inputs are built once (not
+    timed, like shard_kv in BASELINE.md section 3); returns the per-step values."""
     from oracle.oracle import BF16, F32, HIER, Oracle, Reference
     _, b, n_q, n_kv, n, d, dt = wl
     n = args.seq_len or n
@@ -172,38 +175,37 @@ def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1):
     seed = orc.mix64(0, n)
     g = n_q // n_kv
     sample_heads = max(1, min(sample_heads, g))
+    nthreads = max(1, min(nthreads, sample_heads))
     qh = orc.seeded(orc.mix64(seed, 1), sample_heads * d, dtc).reshape(1, sample_heads, d)
     k0 = orc.seeded(orc.mix64(seed, 2), n * d, dtc).reshape(1, 1, n, d)
     v0 = orc.seeded(orc.mix64(seed, 3), n * d, dtc).reshape(1, 1, n, d)
-    times = []
-    with ref.prepare(qh, k0, v0, n_gpus, dtc) as pr:
-        for _ in range(steps):
-            _, secs, _ = pr.decode(0, HIER, args.scale, parallel=n_gpus > 1, nthreads=nthreads)
-            times.append(secs)
-    per_row = min(times) / sample_heads
     rows = b * n_q
-    us_per_token = per_row * rows * 1e6 / b  # one decoded token per sequence per step
-    return us_per_token, times, {
-        "sample": f"{sample_heads} q-head(s) of kv head 0 at N={n}, p={n_gpus} workers, "
-                  f"scaled x{rows / sample_heads:g} to b*n_q={rows} rows; best of {steps}",
-        "cores": nthreads * (n_gpus if n_gpus > 1 else 1),
+    vals = []
+    with ref.prepare(qh, k0, v0, n_gpus, dtc) as pr:
+        del k0, v0
+        for i in range(warmup + steps):
+            _, secs, _ = pr.decode(0, HIER, args.scale, parallel=n_gpus > 1, nthreads=nthreads)
+            if i >= warmup:
+                vals.append(secs / sample_heads * rows * 1e6 / b)  # us per decoded token
+    cores = nthreads * (n_gpus if n_gpus > 1 else 1)
+    return vals, {
+        "sample": f"{sample_heads} q-head(s) of kv head 0 at N={n}, p={n_gpus} worker(s), {nthreads} row "
+                  f"thread(s); scaled x{rows / sample_heads:g} to b*n_q={rows} rows; inputs built once (untimed)",
+        "cores": cores,
     }
 
 
 def run_reference_arm(args, wl, world, rank):
     if rank != 0:
         return
-    nthreads = os.cpu_count() or 1
+    nproc = os.cpu_count() or 1
     _, b, n_q, n_kv, n, d, dt = wl
     g = n_q // n_kv
-    # all host threads: rows (q-heads) in parallel, p workers each; bounded sample
-    heads = min(g, max(1, nthreads // max(1, args.gpus)))
-    vals = []
+    # every host thread: p = N workers per call (threads), sampled rows in parallel
+    row_threads = max(1, nproc // max(1, args.gpus))
+    heads = min(g, row_threads)
     t0 = time.time()
-    for i in range(args.warmup + args.steps):
-        v, _, info = reference_cpu(args, wl, args.gpus, heads, max(1, nthreads // max(1, args.gpus)), steps=1)
-        if i >= args.warmup:
-            vals.append(v)
+    vals, info = reference_cpu(args, wl, args.gpus, heads, row_threads, steps=args.steps, warmup=args.warmup)
     value = sum(vals) / len(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "µs/token", "n_gpus": args.gpus,
@@ -212,7 +214,7 @@ def run_reference_arm(args, wl, world, rank):
         "config": {"workload": args.workload, "seq_len": args.seq_len or n, "batch": b, "q_heads": n_q,
                    "kv_heads": n_kv, "head_dim": d, "shards": args.gpus, "algo": "tree"},
         "cpu_baseline": {"value": value, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
-                         "sample": info["sample"] + f"; host nproc={os.cpu_count()}"},
+                         "sample": info["sample"] + f"; host nproc={nproc}"},
         "e2e": {"value": value, "unit": "µs/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(time.time() - t0, 1),
     }
@@ -261,9 +263,13 @@ def main():
     scratch = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if flush else None
     decode = w.tree_decode_async if args.algo == "tree" else w.ring_decode_async
     flags_timed = _capi.TD_TIME_KERNELS
+    base_flags = 0
+    if args.combine == "p2p" and world > 1 and args.algo == "tree":
+        w.enable_p2p(b * n_q, d)
+        base_flags = _capi.TD_P2P
 
     def step(flags):
-        decode(q.data_ptr(), n_q, out.data_ptr(), args.scale, flags)
+        decode(q.data_ptr(), n_q, out.data_ptr(), args.scale, flags | base_flags)
 
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 3)):
@@ -302,18 +308,28 @@ def main():
                 scratch.fill_(i & 0xFF)
             stream.synchronize()
         t0 = time.perf_counter()
-        decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO)
+        decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO | base_flags)
         e2e_times.append(time.perf_counter() - t0)
     e2e_ms = max_over_ranks(1000.0 * sum(e2e_times) / len(e2e_times), world)
     ok = torch.allclose(out_host, out.cpu())
+
+    # ---- per-phase breakdown (separate pass, not part of the timed number)
+    phases = None
+    if args.phases:
+        barrier(world)
+        w.reset_kernel_timer()
+        for _ in range(max(3, min(args.steps, 20))):
+            step(_capi.TD_TIME_PHASES)
+        barrier(world)
+        phases = [round(max_over_ranks(x, world) * 1000.0, 2) for x in w.phase_times()]
 
     # ---- CPU reference baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             heads = args.cpu_sample_heads or (n_q // n_kv)
-            v, _, info = reference_cpu(args, wl, 1, heads, min(os.cpu_count() or 1, heads), steps=2)
-            cpu = {"value": v, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
+            vals, info = reference_cpu(args, wl, 1, heads, os.cpu_count() or 1, steps=3)
+            cpu = {"value": min(vals), "unit": "µs/token", "cores": info["cores"], "kind": "reference",
                    "sample": info["sample"] + f"; host nproc={os.cpu_count()}"}
         except Exception as e:  # the reference library may be absent on a foreign box
             cpu = {"value": None, "unit": "µs/token", "cores": 0, "kind": "reference",
@@ -330,7 +346,7 @@ def main():
             "data": "synthetic (reference SplitMix64 generator, generated on device)",
             "config": {"workload": args.workload, "desc": desc, "seq_len": n, "batch": b, "q_heads": n_q,
                        "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": shard_len,
-                       "algo": args.algo, "scale": args.scale,
+                       "algo": args.algo, "combine": args.combine if world > 1 else "none", "scale": args.scale,
                        "l2": "flushed between steps" if flush else "inputs larger than L2 (KV shard > 4x126 MB)",
                        "parallelism": f"sp{world} (sequence-sharded KV)"},
             "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
@@ -345,11 +361,15 @@ def main():
             "e2e": {"value": e2e_ms * 1000.0 / b, "unit": "µs/token",
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
                     "matches_device_output": bool(ok)},
+            "phases_us": phases,
             "gpu_launches": kernels_per_step * args.steps,
             "kernels_per_step": kernels_per_step,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if base_flags and w.p2p_status():
+        print("p2p exchange reported a timeout", file=sys.stderr)
+        sys.exit(3)
     w.close()
     if world > 1:
         import torch.distributed as dist

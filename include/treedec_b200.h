@@ -52,7 +52,11 @@ typedef enum { TD_TREE_BINARY = 0, TD_RING_ALLREDUCE = 1, TD_HIERARCHICAL = 2 } 
 enum {
     TD_HOST_IO = 1,      /* q and out are host pointers (copies inside the call) */
     TD_TIME_KERNELS = 2, /* record CUDA events around the split-KV kernel (K1) */
-    TD_BF16_OUT = 4      /* also write a bf16 copy of out (td_output_bf16)      */
+    TD_BF16_OUT = 4,     /* also write a bf16 copy of out (td_output_bf16)      */
+    TD_TIME_PHASES = 8,  /* record CUDA events between the phases of the step   */
+    TD_P2P = 16,         /* tree decode: one-shot NVLink exchange instead of the
+                            two NCCL allreduces (needs td_p2p_open)              */
+    TD_DEBUG_TS = 32     /* kernels record %globaltimer stamps (td_debug_stamps) */
 };
 
 typedef struct td_context td_context;
@@ -118,6 +122,17 @@ int td_comm_unique_id(unsigned char id[128]);
 int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[128]);
 int td_comm_info(td_context* ctx, int* nranks, int* rank);
 
+/* One-shot NVLink exchange (the single-collective exact combine, SURVEY.md
+ * 8(f)1): each rank exports a CUDA-IPC handle of its exchange buffer sized
+ * for max_rows = b * n_q rows of head_dim d, the handles are all-gathered by
+ * the caller (rank order, nranks * 64 bytes) and every rank opens its peers'.
+ * td_tree_decode with TD_P2P then pushes each rank's partial into every
+ * peer's HBM and combines the p partials locally (one exchange, no NCCL).
+ * td_p2p_status reports a peer that never arrived (1) since the last call. */
+int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char handle[64]);
+int td_p2p_open(td_context* ctx, const unsigned char* handles);
+int td_p2p_status(td_context* ctx, int* error);
+
 /* shard_kv (decode.hpp:24, decode.cpp:68-85) for this rank: places rows
  * [start, start+len) of every (batch, kv-head) of a cache of seq_len tokens.
  * k/v are [b, n_kv, len, d] on the host (from_host = 1) or device. */
@@ -165,6 +180,17 @@ int td_output_bf16(td_context* ctx, const void** out_bf16);
  * the last td_reset_kernel_timer, and the number of timed calls. */
 int td_kernel_time(td_context* ctx, double* mean_ms, int* calls);
 int td_reset_kernel_timer(td_context* ctx);
+
+/* Mean duration (ms) of each phase of the decode steps made with
+ * TD_TIME_PHASES since the last td_reset_kernel_timer: phases[i] is the time
+ * between mark i and mark i+1 (tree: K1, K2, allreduce(max), K3,
+ * allreduce(sum), K4); *n = number of phases recorded. */
+int td_phase_times(td_context* ctx, double* phases, int max_phases, int* n, int* calls);
+
+/* Stamps of the last TD_DEBUG_TS call (ns, %globaltimer): [0] first K1 CTA
+ * start, [1] last K1 CTA end, [8 + 8*blk + k] stages of K2 block blk
+ * (0 entry, 1 merged + pushed, 2 fenced + flagged, 3 peers seen, 4 done). */
+int td_debug_stamps(td_context* ctx, unsigned long long* out, int n);
 
 /* Kernels of this library launched by the last decode call, and the
  * algorithmic HBM bytes of its K1 launch(es) (K + V of the shard). */

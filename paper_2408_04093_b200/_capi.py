@@ -15,16 +15,16 @@ LIB_PATH = os.path.join(HERE, "libtreedec_b200.so")
 TD_OK, TD_EINVAL, TD_EDOMAIN, TD_ECUDA, TD_ENCCL, TD_ESTATE = range(6)
 TD_F64, TD_F32, TD_BF16 = 0, 1, 2
 TD_TREE_BINARY, TD_RING_ALLREDUCE, TD_HIERARCHICAL = 0, 1, 2
-TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT = 1, 2, 4
+TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT, TD_TIME_PHASES, TD_P2P, TD_DEBUG_TS = 1, 2, 4, 8, 16, 32
 
 # Every symbol include/treedec_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = [
     "td_version", "td_last_error", "td_seeded_fill", "td_decode_workspace_bytes",
     "td_decode_partial", "td_combine_partials", "td_partial_to_numerator", "td_combine_pair",
     "td_finalize", "td_create", "td_destroy", "td_stream", "td_comm_unique_id", "td_comm_init",
-    "td_comm_info", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
+    "td_comm_info", "td_p2p_handle", "td_p2p_open", "td_p2p_status", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
     "td_tree_decode", "td_ring_decode", "td_local_partial", "td_output_bf16", "td_kernel_time",
-    "td_reset_kernel_timer", "td_last_launch_stats", "td_memory_bytes",
+    "td_reset_kernel_timer", "td_phase_times", "td_debug_stamps", "td_last_launch_stats", "td_memory_bytes",
 ]
 
 
@@ -79,6 +79,9 @@ def lib() -> ctypes.CDLL:
     L.td_comm_unique_id.argtypes = [ctypes.c_char_p]
     L.td_comm_init.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     L.td_comm_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    L.td_p2p_handle.argtypes = [_vp, _i64, _i64, ctypes.c_char_p]
+    L.td_p2p_open.argtypes = [_vp, ctypes.c_char_p]
+    L.td_p2p_status.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
     L.td_kv_place.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, ctypes.c_int]
     L.td_kv_generate.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_uint64,
                                  ctypes.c_double]
@@ -90,6 +93,9 @@ def lib() -> ctypes.CDLL:
     L.td_output_bf16.argtypes = [_vp, ctypes.POINTER(_vp)]
     L.td_kernel_time.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
     L.td_reset_kernel_timer.argtypes = [_vp]
+    L.td_debug_stamps.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    L.td_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                 ctypes.POINTER(ctypes.c_int)]
     L.td_last_launch_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int)]
     L.td_memory_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_size_t)]

@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -157,10 +158,27 @@ struct td_context {
 
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
     size_t timers_used = 0;
+    // TD_TIME_PHASES: per call, up to 8 marks
+    std::vector<std::vector<cudaEvent_t>> phase_sets;
+    size_t phase_used = 0;
+    std::vector<cudaEvent_t>* cur_phase = nullptr;
+    size_t cur_mark = 0;
 
     int last_kernels = 0;
     double last_kv_bytes = 0.0;
     int last_split_kernel = -1;
+
+    // one-shot NVLink exchange (td_p2p_*)
+    DevBuf xbuf;                      // [2][p][max_rows*(d+1)] floats + flags [2][p][kXchgBlocks]
+    size_t x_data_bytes = 0;
+    int64_t x_max_rows = 0, x_d = 0;
+    std::vector<void*> x_opened;      // IPC mappings to close
+    DevBuf x_ptrs;                    // device arrays: peers[p], peer_flags[p]
+    DevBuf x_err;
+    unsigned x_epoch = 0;
+    bool x_ready = false;
+
+    DevBuf dbg;  // TD_DEBUG_TS stamps
 };
 
 namespace {
@@ -174,8 +192,9 @@ int require_ctx(td_context* ctx) {
 // per-row buffers for rows = b * n_q (max) and d
 int ensure_rows(td_context* ctx, int64_t rows, int64_t d) {
     const size_t rd = size_t(rows) * size_t(d), r = size_t(rows);
+    auto pad = [](size_t n) { return (n + 15) / 16 * 16; };
     // row_max, lse, shift, r_max, r_lse: r each; out_local, out, r_out: rd; nd: rd + r
-    const size_t floats = 5 * r + 3 * rd + (rd + r) + 64;
+    const size_t floats = 5 * pad(r) + 3 * pad(rd) + pad(rd + r);
     TD_CUDA(ctx->rows.ensure(floats * sizeof(float)));
     float* f = ctx->rows.as<float>();
     auto take = [&](size_t n) {
@@ -205,6 +224,23 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan) {
     return TD_OK;
 }
 
+void phase_begin(td_context* ctx, int flags) {
+    ctx->cur_phase = nullptr;
+    if (!(flags & TD_TIME_PHASES)) return;
+    if (ctx->phase_used == ctx->phase_sets.size()) {
+        std::vector<cudaEvent_t> evs(8);
+        for (auto& e : evs) cudaEventCreate(&e);
+        ctx->phase_sets.push_back(evs);
+    }
+    ctx->cur_phase = &ctx->phase_sets[ctx->phase_used++];
+    ctx->cur_mark = 0;
+}
+
+void phase_mark(td_context* ctx) {
+    if (!ctx->cur_phase || ctx->cur_mark >= ctx->cur_phase->size()) return;
+    cudaEventRecord((*ctx->cur_phase)[ctx->cur_mark++], ctx->stream);
+}
+
 cudaEvent_t* next_timer(td_context* ctx) {
     if (ctx->timers_used == ctx->timers.size()) {
         cudaEvent_t a, b;
@@ -218,7 +254,7 @@ cudaEvent_t* next_timer(td_context* ctx) {
 // K1 + K2 over a [b][n_kv][t][d] buffer.
 int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const void* kb,
                 const void* vb, int64_t t, double scale, bool own_maps, float* rmax, float* lse,
-                float* out, bool timed) {
+                float* out, bool timed, td_context* phases = nullptr) {
     CUtensorMap mk, mv;
     const CUtensorMap *pk = nullptr, *pv = nullptr;
     if (plan.kernel == 1) {
@@ -240,6 +276,8 @@ int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const voi
         cudaEvent_t* pr = next_timer(ctx);
         e0 = pr[0];
         e1 = pr[1];
+    } else if (phases && phases->cur_phase && phases->cur_mark < phases->cur_phase->size()) {
+        e1 = (*phases->cur_phase)[phases->cur_mark++];  // mark between K1 and K2
     }
     TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
                                       ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
@@ -415,6 +453,10 @@ int td_destroy(td_context* ctx) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
     }
+    for (void* ptr : ctx->x_opened) cudaIpcCloseMemHandle(ptr);
+    ctx->xbuf.release();
+    ctx->x_ptrs.release();
+    ctx->x_err.release();
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->xfer);
     delete ctx;
@@ -456,6 +498,68 @@ int td_comm_info(td_context* ctx, int* nranks, int* rank) {
     if (int rc = require_ctx(ctx)) return rc;
     *nranks = ctx->nranks;
     *rank = ctx->rank;
+    return TD_OK;
+}
+
+int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char handle[64]) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (max_rows < 1 || d < 1 || d > 256) return set_err(TD_EINVAL, "p2p: bad max_rows / head_dim");
+    for (void* ptr : ctx->x_opened) cudaIpcCloseMemHandle(ptr);
+    ctx->x_opened.clear();
+    ctx->x_ready = false;
+    const size_t data = 2 * size_t(ctx->nranks) * size_t(max_rows) * size_t(d + 1) * sizeof(float);
+    const size_t flags = 2 * size_t(ctx->nranks) * td::kXchgBlocks * sizeof(unsigned);
+    ctx->xbuf.release();
+    TD_CUDA(ctx->xbuf.ensure(data + flags));
+    TD_CUDA(cudaMemset(ctx->xbuf.p, 0, data + flags));
+    TD_CUDA(ctx->x_err.ensure(sizeof(int)));
+    TD_CUDA(cudaMemset(ctx->x_err.p, 0, sizeof(int)));
+    ctx->x_data_bytes = data;
+    ctx->x_max_rows = max_rows;
+    ctx->x_d = d;
+    ctx->x_epoch = 0;
+    cudaIpcMemHandle_t h;
+    TD_CUDA(cudaIpcGetMemHandle(&h, ctx->xbuf.p));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+    std::memcpy(handle, &h, 64);
+    return TD_OK;
+}
+
+int td_p2p_open(td_context* ctx, const unsigned char* handles) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->xbuf.p) return set_err(TD_ESTATE, "p2p: call td_p2p_handle first");
+    const int p = ctx->nranks;
+    std::vector<void*> base(size_t(p), nullptr);
+    for (int q = 0; q < p; ++q) {
+        if (q == ctx->rank) {
+            base[size_t(q)] = ctx->xbuf.p;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + 64 * q, 64);
+        void* ptr = nullptr;
+        TD_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->x_opened.push_back(ptr);
+        base[size_t(q)] = ptr;
+    }
+    std::vector<void*> arr(2 * size_t(p));
+    for (int q = 0; q < p; ++q) {
+        arr[size_t(q)] = base[size_t(q)];
+        arr[size_t(p + q)] = static_cast<char*>(base[size_t(q)]) + ctx->x_data_bytes;
+    }
+    TD_CUDA(ctx->x_ptrs.ensure(arr.size() * sizeof(void*)));
+    TD_CUDA(cudaMemcpy(ctx->x_ptrs.p, arr.data(), arr.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    ctx->x_ready = true;
+    return TD_OK;
+}
+
+int td_p2p_status(td_context* ctx, int* error) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *error = 0;
+    if (!ctx->x_err.p) return TD_OK;
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    TD_CUDA(cudaMemcpy(error, ctx->x_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+    TD_CUDA(cudaMemset(ctx->x_err.p, 0, sizeof(int)));
     return TD_OK;
 }
 
@@ -550,9 +654,31 @@ int td_kv_pointers(td_context* ctx, void** k, void** v) {
     return TD_OK;
 }
 
+static int debug_begin(td_context* ctx, int flags) {
+    if (!(flags & TD_DEBUG_TS)) {
+        td::set_debug_stamps(nullptr);
+        return TD_OK;
+    }
+    TD_CUDA(ctx->dbg.ensure(4200 * sizeof(unsigned long long)));
+    TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 4200 * sizeof(unsigned long long), ctx->stream));
+    TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xff, sizeof(unsigned long long), ctx->stream));
+    td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
+    return TD_OK;
+}
+
+int td_debug_stamps(td_context* ctx, unsigned long long* out, int n) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->dbg.p) return set_err(TD_ESTATE, "no TD_DEBUG_TS call made");
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    TD_CUDA(cudaMemcpy(out, ctx->dbg.p, sizeof(unsigned long long) * size_t(std::min(n, 4200)),
+                       cudaMemcpyDeviceToHost));
+    return TD_OK;
+}
+
 int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
                    float* out, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
+    if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "tree_decode: no KV shard placed");
     if (strategy < 0 || strategy > 2) return set_err(TD_EINVAL, "tree_decode: unknown strategy");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "tree_decode: more workers than keys");
@@ -567,24 +693,66 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     int rc = TD_OK;
     const void* qd = stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
+    phase_begin(ctx, flags);
+    phase_mark(ctx);
+    if ((flags & TD_P2P) && ctx->nranks > 1) {
+        // K1 + K2x: split-KV partial, then one exchange + exact combine
+        if (!ctx->x_ready) return set_err(TD_ESTATE, "tree_decode: TD_P2P without td_p2p_open");
+        if (rows > ctx->x_max_rows || d != ctx->x_d)
+            return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
+        td::XchgArgs xa;
+        xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
+        xa.peer_flags = reinterpret_cast<unsigned* const*>(static_cast<void**>(ctx->x_ptrs.p) + ctx->nranks);
+        xa.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ctx->xbuf.p) + ctx->x_data_bytes);
+        xa.p = ctx->nranks;
+        xa.rank = ctx->rank;
+        xa.epoch = ++ctx->x_epoch;
+        xa.max_rows = ctx->x_max_rows;
+        xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 2 * int64_t(ctx->sm_count));
+        xa.error = static_cast<int*>(ctx->x_err.p);
+        const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
+        const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (flags & TD_TIME_KERNELS) {
+            cudaEvent_t* pr = next_timer(ctx);
+            e0 = pr[0];
+            e1 = pr[1];
+        } else if (ctx->cur_phase) {
+            e1 = (*ctx->cur_phase)[ctx->cur_mark++];
+        }
+        TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
+                                           ctx->ws.p, xa, ctx->out, ctx->stream, e0, e1));
+        phase_mark(ctx);
+        ctx->last_kernels = 2;
+        ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
+                             td::dtype_bytes(ctx->dtype);
+        ctx->last_split_kernel = plan.kernel;
+        return deliver_out(ctx, ctx->out, rows, out, flags);
+    }
     // 1. local partial (out, lse) of this shard
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
-                          ctx->row_max, ctx->lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0)))
+                          ctx->row_max, ctx->lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0,
+                          ctx->cur_phase ? ctx : nullptr)))
         return rc;
+    phase_mark(ctx);
     const float* result = ctx->out_local;
     if (ctx->nranks > 1) {
         // 2. allreduce(max) over lse -> common shift (decode.cpp:129-139)
         TD_NCCL(nccl().AllReduce(ctx->lse, ctx->shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm,
                               ctx->stream));
+        phase_mark(ctx);
         // 3. n = o e^(lse-m), d = e^(lse-m) (decode.cpp:150-153)
         TD_CUDA(td::launch_to_numerator(ctx->lse, ctx->out_local, ctx->shift, rows,
                                         static_cast<int>(d), ctx->nd, ctx->stream));
+        phase_mark(ctx);
         // 4. one fused sum-allreduce over [n|d] (decode.cpp:154-160); fp32 wire
         TD_NCCL(nccl().AllReduce(ctx->nd, ctx->nd, size_t(rows * d + rows), ncclFloat32, ncclSum,
                               ctx->comm, ctx->stream));
+        phase_mark(ctx);
         // 5. out = n / d (decode.cpp:165-173)
         TD_CUDA(td::launch_finalize(ctx->nd, rows, static_cast<int>(d), ctx->out, nullptr,
                                     ctx->stream));
+        phase_mark(ctx);
         ctx->last_kernels += 2;
         result = ctx->out;
     }
@@ -723,6 +891,35 @@ int td_kernel_time(td_context* ctx, double* mean_ms, int* calls) {
 int td_reset_kernel_timer(td_context* ctx) {
     if (int rc = require_ctx(ctx)) return rc;
     ctx->timers_used = 0;
+    ctx->phase_used = 0;
+    return TD_OK;
+}
+
+int td_phase_times(td_context* ctx, double* phases, int max_phases, int* n, int* calls) {
+    if (int rc = require_ctx(ctx)) return rc;
+    int np = 0;
+    for (int i = 0; i < max_phases; ++i) phases[i] = 0.0;
+    // marks recorded per call are counted by querying each event's status
+    for (size_t c = 0; c < ctx->phase_used; ++c) {
+        auto& evs = ctx->phase_sets[c];
+        int marks = 0;
+        for (auto& e : evs) {
+            if (cudaEventQuery(e) == cudaErrorNotReady) cudaEventSynchronize(e);
+            float dummy;
+            if (cudaEventElapsedTime(&dummy, evs[0], e) != cudaSuccess) break;
+            ++marks;
+        }
+        cudaGetLastError();
+        for (int i = 0; i + 1 < marks && i < max_phases; ++i) {
+            float ms = 0.f;
+            TD_CUDA(cudaEventElapsedTime(&ms, evs[size_t(i)], evs[size_t(i) + 1]));
+            phases[i] += ms;
+        }
+        np = std::max(np, marks - 1);
+    }
+    for (int i = 0; i < max_phases; ++i) phases[i] /= ctx->phase_used ? double(ctx->phase_used) : 1.0;
+    *n = np;
+    *calls = static_cast<int>(ctx->phase_used);
     return TD_OK;
 }
 

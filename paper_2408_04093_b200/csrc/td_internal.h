@@ -27,11 +27,16 @@ struct SplitPlan {
     int kernel = 0;  // 0 generic, 1 bf16 mma (TMA), 2 f32 (bulk)
     int dtype = kBF16;
     int64_t slots() const { return int64_t(ctas) * warps * maxseg; }
-    // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32)
+    // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32),
+    // then the per-CTA merged states [ctas * maxseg][group] (+ [..][d])
     size_t workspace_bytes() const {
-        return sizeof(float) * size_t(slots()) * size_t(group) * size_t(2 + d);
+        return sizeof(float) * (size_t(slots()) + size_t(ctas) * maxseg) * size_t(group) * size_t(2 + d);
     }
 };
+
+// TD_DEBUG_TS: kernels write %globaltimer stamps into buf (nullptr = off):
+// [0] min K1 CTA start, [1] max K1 CTA end, [8 + 8*blk + k] K2 block stages.
+void set_debug_stamps(unsigned long long* buf);
 
 // Chooses the kernel and grid for a shard. Returns false (with msg) when the
 // shape is unsupported.
@@ -46,6 +51,33 @@ cudaError_t launch_decode_partial(const SplitPlan& plan, const void* q, const vo
                                   const CUtensorMap* tmv, void* workspace, float* row_max,
                                   float* lse, float* out, cudaStream_t stream,
                                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+
+// K1 alone (events around it when given).
+cudaError_t launch_split(const SplitPlan& plan, const void* q, const void* k, const void* v,
+                         float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
+                         void* workspace, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1);
+
+// One-shot NVLink exchange buffers (td_p2p_*): every rank's exchange buffer
+// holds [2 parities][p sources][max_rows lse | max_rows*d out] floats; flags
+// are [2][p][kXchgMaxBlocks] u32 per rank.
+struct XchgArgs {
+    float* const* peers;       // device array [p]
+    unsigned* flags;           // own flags
+    unsigned* const* peer_flags;  // device array [p]
+    int p = 1, rank = 0;
+    unsigned epoch = 0;
+    int64_t max_rows = 0;
+    int64_t max_blocks = 0;
+    int* error = nullptr;
+};
+constexpr int kXchgBlocks = 1024;
+
+// K1 + K2x: split-KV partial, merge, one-shot exchange and exact combine;
+// out [b, n_q, d] fp32 final (identical on every rank).
+cudaError_t launch_decode_exchange(const SplitPlan& plan, const void* q, const void* k, const void* v,
+                                   float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
+                                   void* workspace, const XchgArgs& xa, float* out, cudaStream_t stream,
+                                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // Builds the 2-D tensor map used by the bf16 kernel over rows x d elements.
 bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,

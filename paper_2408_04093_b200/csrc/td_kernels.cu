@@ -39,10 +39,69 @@ struct K1Args {
     float* slot_m;  // [slots][group]
     float* slot_l;
     float* slot_o;  // [slots][group][d]
+    float* cslot_m; // per-CTA merged states [ctas * maxseg][group]
+    float* cslot_l;
+    float* cslot_o; // [ctas * maxseg][group][d]
+    unsigned long long* dbg;  // optional globaltimer stamps (TD_DEBUG_TS)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ int64_t cta_begin(int64_t total, int c, int ctas) {
     return total * c / ctas;
+}
+
+// End of K1: merges the W warp states of each of CTA c's segments into one
+// CTA state (cslot_*), so K2 merges ctas, not ctas * W, states per row. All
+// loads of a phase are independent (one L2 round trip each). sm must hold
+// 3 * W * maxseg * group floats; every thread of the CTA calls this after a
+// __syncthreads() that follows the warps' final flushes.
+template <int W>
+__device__ void cta_merge(const K1Args& a, int c, float* sm) {
+    const int g = a.group, D = a.d, ms = a.maxseg;
+    const int nsh = ms * g;
+    const int nml = W * nsh;
+    float* sm_m = sm;
+    float* sm_l = sm + nml;
+    float* sm_e = sm + 2 * nml;
+    const int64_t base = int64_t(c) * nml;
+    for (int i = threadIdx.x; i < nml; i += blockDim.x) {
+        sm_m[i] = a.slot_m[base + i];
+        sm_l[i] = a.slot_l[base + i];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nsh; i += blockDim.x) {
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < W; ++w) M = fmaxf(M, sm_m[w * nsh + i]);
+        float L = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const float m = sm_m[w * nsh + i];
+            const float e = (m == -CUDART_INF_F) ? 0.f : exp2f(m - M);
+            sm_e[w * nsh + i] = e;
+            L += e * sm_l[w * nsh + i];
+        }
+        a.cslot_m[int64_t(c) * nsh + i] = M;
+        a.cslot_l[int64_t(c) * nsh + i] = L;
+    }
+    __syncthreads();
+    const int64_t n = int64_t(nsh) * D;
+#pragma unroll 4
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+        const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
+        float O = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const float ew = sm_e[w * nsh + i];
+            if (ew != 0.f) O += ew * a.slot_o[(base + int64_t(w) * nsh + i) * D + j];
+        }
+        a.cslot_o[(int64_t(c) * nsh + i) * D + j] = O;
+    }
 }
 
 // =========================================================================
@@ -68,6 +127,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     __shared__ uint64_t bars[W][S];
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
+    const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -294,6 +354,12 @@ __global__ void __launch_bounds__(W * 32, 1)
             a.slot_l[slot * a.group + h] = 0.f;
         }
     }
+    __syncthreads();
+    cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    if (a.dbg && threadIdx.x == 0) {
+        atomicMin(a.dbg + 0, t_start);
+        atomicMax(a.dbg + 1, gtimer());
+    }
 }
 
 // =========================================================================
@@ -311,6 +377,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     __shared__ uint64_t bars[W][S];
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
 
+    const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -466,6 +533,12 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
             a.slot_l[slot * G + lane] = 0.f;
         }
     }
+    __syncthreads();
+    cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    if (a.dbg && threadIdx.x == 0) {
+        atomicMin(a.dbg + 0, t_start);
+        atomicMax(a.dbg + 1, gtimer());
+    }
 }
 
 // =========================================================================
@@ -480,8 +553,11 @@ template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
 
 template <typename TIn>
-__global__ void __launch_bounds__(128) k1_generic(const K1Args a, int W) {
+__global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
     constexpr int T = 32;
+    constexpr int W = 4;
+    extern __shared__ float gen_smem[];
+    const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -567,6 +643,8 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a, int W) {
             }
         }
     }
+    __syncthreads();
+    cta_merge<W>(a, c, gen_smem);
 }
 
 // =========================================================================
@@ -578,78 +656,216 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a, int W) {
 // =========================================================================
 constexpr int K2_THREADS = 512;
 
-__global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a, int W, float* row_max,
-                                                         float* lse, float* out) {
-    __shared__ float red[K2_THREADS / 32];
-    __shared__ float acc_l[K2_THREADS / 32];
-    __shared__ float acc_o[K2_THREADS / 32][256];
-    const int r = blockIdx.x;  // over bh_count * group
+constexpr int kK2MaxCand = 1024;
+
+struct K2Smem {
+    float m[kK2MaxCand];
+    float l[kK2MaxCand];
+    float e[kK2MaxCand];
+    int64_t cs[kK2MaxCand];
+    float red[K2_THREADS / 32];
+    float acc[K2_THREADS];
+};
+
+// Merges the CTA states of row r (over bh_count * group) into out_row (D
+// floats, any address space) and returns (lse, row_max) in natural log
+// units: two bulk rounds of independent loads (the (m, l) of every covering
+// CTA, then their o rows spread over all threads). All threads call it.
+__device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row, float& lse_o,
+                          float& rmax_o) {
     const int64_t bh = r / a.group;
-    const int h = r % a.group;
-    const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
-    const int64_t orow = b * a.n_q + kvh * a.group + h;
-    const int D = a.d;
+    const int h = static_cast<int>(r % a.group);
+    const int D = a.d, g = a.group;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
-
     int64_t c_lo = 0, c_hi = -1;
     if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
         const int64_t X = bh * a.tiles_per_bh, Xe = X + a.tiles_per_bh - 1;
         c_lo = ((X + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
         c_hi = ((Xe + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
     }
-    const int64_t ncand = (c_hi - c_lo + 1) * W;
-    auto slot_of = [&](int64_t i) {
-        const int64_t cc = c_lo + i / W;
-        const int ww = static_cast<int>(i % W);
-        const int64_t seg = bh - cta_begin(a.total_tiles, static_cast<int>(cc), a.ctas) / a.tiles_per_bh;
-        return (cc * W + ww) * a.maxseg + seg;
-    };
-    // pass 1: M
+    const int S = static_cast<int>(c_hi - c_lo + 1);
     float mloc = -CUDART_INF_F;
-    for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x)
-        mloc = fmaxf(mloc, a.slot_m[slot_of(i) * a.group + h]);
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const int c = static_cast<int>(c_lo + i);
+        const int64_t cs = int64_t(c) * a.maxseg + (bh - cta_begin(a.total_tiles, c, a.ctas) / a.tiles_per_bh);
+        const float m = a.cslot_m[cs * g + h];
+        sm.m[i] = m;
+        sm.l[i] = a.cslot_l[cs * g + h];
+        sm.cs[i] = cs;
+        mloc = fmaxf(mloc, m);
+    }
     for (int off = 16; off >= 1; off >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
-    if (lane == 0) red[warp] = mloc;
+    if (lane == 0) sm.red[warp] = mloc;
     __syncthreads();
     float M = -CUDART_INF_F;
-    for (int i = 0; i < nw; ++i) M = fmaxf(M, red[i]);
-    // pass 2: weighted sums, warp per candidate slot, lanes over d
-    float lsum = 0.f, osum[8];
-    for (int i = 0; i < 8; ++i) osum[i] = 0.f;
-    if (M != -CUDART_INF_F) {
-        for (int64_t i = warp; i < ncand; i += nw) {
-            const int64_t slot = slot_of(i);
-            const float mm = a.slot_m[slot * a.group + h];
-            if (mm == -CUDART_INF_F) continue;
-            const float e = exp2f(mm - M);
-            lsum += e * a.slot_l[slot * a.group + h];
-            const float* so = a.slot_o + (slot * a.group + h) * int64_t(D);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int j = lane + 32 * k;
-                if (j < D) osum[k] += e * so[j];
-            }
-        }
+    for (int i = 0; i < nw; ++i) M = fmaxf(M, sm.red[i]);
+    __syncthreads();
+    float lpart = 0.f;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const float e = (sm.m[i] == -CUDART_INF_F) ? 0.f : exp2f(sm.m[i] - M);
+        sm.e[i] = e;
+        lpart += e * sm.l[i];
     }
-    if (lane == 0) acc_l[warp] = lsum;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int j = lane + 32 * k;
-        if (j < D) acc_o[warp][j] = osum[k];
-    }
+    for (int off = 16; off >= 1; off >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, off);
+    if (lane == 0) sm.red[warp] = lpart;
     __syncthreads();
     float L = 0.f;
-    for (int i = 0; i < nw; ++i) L += acc_l[i];
-    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    for (int i = 0; i < nw; ++i) L += sm.red[i];
+    // o rows: thread (grp, j) sums candidates grp, grp + NG, ...
+    const int NG = blockDim.x / D;
+    const int grp = threadIdx.x / D, j = threadIdx.x % D;
+    if (grp < NG) {
+        float acc = 0.f;
+#pragma unroll 8
+        for (int i = grp; i < S; i += NG) {
+            const float e = sm.e[i];
+            if (e != 0.f) acc += e * a.cslot_o[(sm.cs[i] * g + h) * D + j];
+        }
+        sm.acc[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < D; jj += blockDim.x) {
         float O = 0.f;
-        for (int i = 0; i < nw; ++i) O += acc_o[i][j];
-        out[orow * D + j] = (M == -CUDART_INF_F) ? 0.f : O / L;
+        for (int q = 0; q < NG; ++q) O += sm.acc[q * D + jj];
+        out_row[jj] = (M == -CUDART_INF_F) ? 0.f : O / L;
     }
+    lse_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
+    rmax_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : M * kLn2;
+    __syncthreads();  // sm is reused by the next row
+}
+
+__device__ __forceinline__ int64_t out_row_of(const K1Args& a, int64_t r) {
+    const int64_t bh = r / a.group, h = r % a.group;
+    return (bh / a.n_kv) * a.n_q + (bh % a.n_kv) * a.group + h;
+}
+
+// K2: merge the split states of each (b, q-head) row into the shard's
+// partial: out = O/L, lse = (M + log2 L) ln 2, row_max = M ln 2. Empty rows
+// give the identity (-inf, -inf, 0), like attention_chunk_partial on an
+// empty chunk (attention.cpp:56-61).
+__global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a, float* row_max,
+                                                         float* lse, float* out) {
+    __shared__ K2Smem sm;
+    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
+    const int64_t rows = a.bh_count * a.group;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t orow = out_row_of(a, r);
+        float l, m;
+        merge_row(a, r, sm, out + orow * a.d, l, m);
+        if (threadIdx.x == 0) {
+            lse[orow] = l;
+            row_max[orow] = m;
+        }
+    }
+    if (ts && threadIdx.x == 0) ts[4] = gtimer();
+}
+
+// =========================================================================
+// K2x: K2 fused with a one-shot NVLink exchange (the single-collective exact
+// combine of SURVEY.md 8(f)1). Each block merges its rows' split states,
+// stores [lse | out] of those rows into slot `rank` of every peer's exchange
+// buffer (CUDA-IPC mapped HBM, plain stores over NVLink), raises one flag
+// per (peer, block), waits for the p flags of its own rows, and combines the
+// p partials locally: shift = max lse, w = e^(lse - shift), out = sum w o /
+// sum w -- the max-allreduce / rescale / sum-allreduce / divide of
+// decode.cpp:129-173 in one exchange. Slots alternate by epoch parity, so a
+// rank can never overwrite a slot a peer is still reading. The grid never
+// exceeds the co-resident capacity, so every block pushes before any waits.
+// =========================================================================
+struct Xchg {
+    float* const* peers;  // [p] exchange buffers (own included), device array
+    unsigned* flags;      // own flags [2][p][kXchgMaxBlocks]
+    unsigned* const* peer_flags;
+    int p, rank;
+    unsigned epoch;
+    int64_t max_rows;
+    int* error;           // set on timeout
+};
+constexpr int kXchgMaxBlocks = kXchgBlocks;
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a, Xchg x,
+                                                          float* out) {
+    __shared__ K2Smem sm;
+    __shared__ float lse_s;
+    const int64_t rows = a.bh_count * a.group;
+    const int D = a.d;
+    const unsigned par = x.epoch & 1u;
+    const int64_t stride = x.max_rows * int64_t(D + 1);  // floats per (parity, src) slot
+    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
+    // 1. merge + push my rows
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t orow = out_row_of(a, r);
+        float* own = x.peers[x.rank] + (int64_t(par) * x.p + x.rank) * stride;
+        float l, m;
+        merge_row(a, r, sm, own + x.max_rows + orow * D, l, m);
+        if (threadIdx.x == 0) {
+            own[orow] = l;
+            lse_s = l;
+        }
+        __syncthreads();
+        const float* src = own + x.max_rows + orow * D;
+        for (int q = 0; q < x.p; ++q) {
+            if (q == x.rank) continue;
+            float* dst = x.peers[q] + (int64_t(par) * x.p + x.rank) * stride;
+            for (int j = threadIdx.x; j < D; j += blockDim.x) dst[x.max_rows + orow * D + j] = src[j];
+            if (threadIdx.x == 0) dst[orow] = lse_s;
+        }
+    }
+    __syncthreads();
+    if (ts && threadIdx.x == 0) ts[1] = gtimer();
+    // 2. publish: one flag per (peer, block)
     if (threadIdx.x == 0) {
-        lse[orow] = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
-        row_max[orow] = (M == -CUDART_INF_F) ? -CUDART_INF_F : M * kLn2;
+        __threadfence_system();
+        if (ts) ts[2] = gtimer();
+        for (int q = 0; q < x.p; ++q)
+            st_release_sys(x.peer_flags[q] + (par * x.p + x.rank) * kXchgMaxBlocks + blockIdx.x, x.epoch);
     }
+    // 3. wait for every source's flag of this block
+    if (threadIdx.x < x.p) {
+        const unsigned* f = x.flags + (par * x.p + threadIdx.x) * kXchgMaxBlocks + blockIdx.x;
+        const long long t0 = clock64();
+        while (ld_acquire_sys(f) != x.epoch) {
+            if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
+                atomicExch(x.error, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    if (ts && threadIdx.x == 0) ts[3] = gtimer();
+    // 4. exact combine of the p partials of my rows
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t orow = out_row_of(a, r);
+        float shift = -CUDART_INF_F;
+        for (int q = 0; q < x.p; ++q)
+            shift = fmaxf(shift, __ldcg(x.peers[x.rank] + (int64_t(par) * x.p + q) * stride + orow));
+        for (int j = threadIdx.x; j < D; j += blockDim.x) {
+            float num = 0.f, den = 0.f;
+            for (int q = 0; q < x.p; ++q) {
+                const float* slot = x.peers[x.rank] + (int64_t(par) * x.p + q) * stride;
+                const float l = __ldcg(slot + orow);
+                if (l == -CUDART_INF_F) continue;
+                const float w = expf(l - shift);
+                den += w;
+                num += w * __ldcg(slot + x.max_rows + orow * D + j);
+            }
+            out[orow * D + j] = num / den;
+        }
+    }
+    if (ts && threadIdx.x == 0) ts[4] = gtimer();
 }
 
 // =========================================================================
@@ -763,9 +979,12 @@ size_t bf16_smem() {
 }
 size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 * 4 + 128; }
 
+unsigned long long* g_dbg = nullptr;  // set by set_debug_stamps
+
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
     K1Args a{};
+    a.dbg = g_dbg;
     a.q = q;
     a.k = k;
     a.v = v;
@@ -785,6 +1004,11 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.slot_m = f;
     a.slot_l = f + ns;
     a.slot_o = f + 2 * ns;
+    float* cf = f + ns * (2 + int64_t(p.d));
+    const int64_t nc = int64_t(p.ctas) * p.maxseg * p.group;
+    a.cslot_m = cf;
+    a.cslot_l = cf + nc;
+    a.cslot_o = cf + 2 * nc;
     return a;
 }
 
@@ -795,6 +1019,8 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 }
 
 }  // namespace
+
+void set_debug_stamps(unsigned long long* buf) { g_dbg = buf; }
 
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
                 SplitPlan& p, std::string& msg) {
@@ -888,11 +1114,9 @@ bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, in
     return true;
 }
 
-cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void* k,
-                                  const void* v, float scale, const CUtensorMap* tmk,
-                                  const CUtensorMap* tmv, void* ws, float* row_max, float* lse,
-                                  float* out, cudaStream_t st, cudaEvent_t ev0,
-                                  cudaEvent_t ev1) {
+cudaError_t launch_split(const SplitPlan& p, const void* q, const void* k, const void* v,
+                         float scale, const CUtensorMap* tmk, const CUtensorMap* tmv, void* ws,
+                         cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
     const K1Args a = make_args(p, q, k, v, scale, ws);
     cudaError_t e = cudaSuccess;
     if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
@@ -929,13 +1153,57 @@ cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void*
         default: return cudaErrorInvalidValue;
         }
     } else {
-        if (p.dtype == kBF16) k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, 0, st>>>(a, kGenWarps);
-        else k1_generic<float><<<p.ctas, kGenWarps * 32, 0, st>>>(a, kGenWarps);
+        const size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
+        if (p.dtype == kBF16) {
+            if ((e = set_smem(k1_generic<__nv_bfloat16>, sm)) != cudaSuccess) return e;
+            k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
+        } else {
+            if ((e = set_smem(k1_generic<float>, sm)) != cudaSuccess) return e;
+            k1_generic<float><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
+        }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev1 && (e = cudaEventRecord(ev1, st)) != cudaSuccess) return e;
-    k2_combine<<<static_cast<unsigned>(p.bh_count * p.group), K2_THREADS, 0, st>>>(a, p.warps, row_max,
-                                                                                   lse, out);
+    return cudaSuccess;
+}
+
+cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void* k,
+                                  const void* v, float scale, const CUtensorMap* tmk,
+                                  const CUtensorMap* tmv, void* ws, float* row_max, float* lse,
+                                  float* out, cudaStream_t st, cudaEvent_t ev0,
+                                  cudaEvent_t ev1) {
+    cudaError_t e = launch_split(p, q, k, v, scale, tmk, tmv, ws, st, ev0, ev1);
+    if (e != cudaSuccess) return e;
+    const K1Args a = make_args(p, q, k, v, scale, ws);
+    int64_t rows = p.bh_count * p.group;
+    k2_combine<<<static_cast<unsigned>(rows < 4096 ? rows : 4096), K2_THREADS, 0, st>>>(a, row_max,
+                                                                                        lse, out);
+    return cudaGetLastError();
+}
+
+
+
+cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void* k, const void* v,
+                                   float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
+                                   void* ws, const XchgArgs& xa, float* out, cudaStream_t st,
+                                   cudaEvent_t ev0, cudaEvent_t ev1) {
+    // K1 (+ events) through the partial launcher with K2 suppressed
+    cudaError_t e = launch_split(p, q, k, v, scale, tmk, tmv, ws, st, ev0, ev1);
+    if (e != cudaSuccess) return e;
+    const K1Args a = make_args(p, q, k, v, scale, ws);
+    Xchg x{};
+    x.peers = xa.peers;
+    x.flags = xa.flags;
+    x.peer_flags = xa.peer_flags;
+    x.p = xa.p;
+    x.rank = xa.rank;
+    x.epoch = xa.epoch;
+    x.max_rows = xa.max_rows;
+    x.error = xa.error;
+    const int64_t rows = p.bh_count * p.group;
+    int64_t grid = rows < xa.max_blocks ? rows : xa.max_blocks;
+    if (grid < 1) grid = 1;
+    k2_exchange<<<static_cast<unsigned>(grid), K2_THREADS, 0, st>>>(a, x, out);
     return cudaGetLastError();
 }
 

@@ -403,6 +403,22 @@ class Worker:
         dist.broadcast_object_list(obj, src=0)
         return cls(device, (nranks, rank, obj[0]))
 
+    def enable_p2p(self, max_rows: int, d: int):
+        """Set up the one-shot NVLink exchange (TD_P2P): export this rank's
+        exchange-buffer IPC handle, all-gather the handles with
+        torch.distributed (plumbing) and map the peers' buffers."""
+        import torch.distributed as dist
+        h = self._ct.create_string_buffer(64)
+        check(lib().td_p2p_handle(self.h, max_rows, d, h))
+        handles = [None] * self.nranks
+        dist.all_gather_object(handles, h.raw)
+        check(lib().td_p2p_open(self.h, b"".join(handles)))
+
+    def p2p_status(self) -> int:
+        e = self._ct.c_int()
+        check(lib().td_p2p_status(self.h, self._ct.byref(e)))
+        return e.value
+
     def close(self):
         if getattr(self, "h", None):
             lib().td_destroy(self.h)
@@ -495,6 +511,17 @@ class Worker:
         ms, n = self._ct.c_double(), self._ct.c_int()
         check(lib().td_kernel_time(self.h, self._ct.byref(ms), self._ct.byref(n)))
         return ms.value, n.value
+
+    def phase_times(self) -> list[float]:
+        arr = (self._ct.c_double * 8)()
+        n, calls = self._ct.c_int(), self._ct.c_int()
+        check(lib().td_phase_times(self.h, arr, 8, self._ct.byref(n), self._ct.byref(calls)))
+        return [arr[i] for i in range(n.value)]
+
+    def debug_stamps(self, n: int = 8 + 8 * 64) -> list[int]:
+        arr = (self._ct.c_uint64 * n)()
+        check(lib().td_debug_stamps(self.h, arr, n))
+        return list(arr)
 
     def reset_kernel_timer(self):
         check(lib().td_reset_kernel_timer(self.h))

@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python bench.py --steps 20 --warmup 3 --phases --no-cpu-baseline > gpurun_out/b1.log 2>&1
+for n in 2 4; do
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2960$n bench.py --gpus $n --steps 20 --warmup 3 --phases > gpurun_out/b$n.log 2>&1
+done
+NCCL_DEBUG=INFO timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29617 bench.py --gpus 4 --steps 5 --warmup 3 > gpurun_out/b4_ncclinfo.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_multi.py tests/test_gpu_shim.py -q -p timeout --timeout 800 > gpurun_out/multi.log 2>&1
+timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu.log 2>&1
+echo done

@@ -1,0 +1,65 @@
+#!/usr/bin/env python3
+"""Per-stage device timestamps of one decode step (TD_DEBUG_TS), per rank.
+torchrun --nproc-per-node N scripts/ts_probe.py [--combine p2p|nccl] [--seq-len N]
+Prints, per rank, microseconds relative to the first K1 CTA start:
+K1 end, and for the K2 blocks the max over blocks of each stage."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--combine", default="p2p")
+    ap.add_argument("--seq-len", type=int, default=1 << 20)
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_04093_b200 as td
+    from paper_2408_04093_b200 import _capi
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = td.Worker.from_torch_distributed(local) if world > 1 else td.Worker(local)
+    b, n_q, n_kv, d = 1, 32, 8, 128
+    w.generate_kv(td.DType.Bf16, b, n_kv, args.seq_len, d, 11, 12)
+    q = td.seeded_tensor([b, n_q, d], 13, 1.0, td.DType.Bf16)
+    out = torch.empty(b, n_q, d, device="cuda")
+    flags = 0
+    if args.combine == "p2p" and world > 1:
+        w.enable_p2p(b * n_q, d)
+        flags = _capi.TD_P2P
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags)
+    res = []
+    for _ in range(5):
+        w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags | _capi.TD_DEBUG_TS)
+        st = w.debug_stamps(8 + 8 * 64)
+        t0 = st[0]
+        blocks = [st[8 + 8 * i: 8 + 8 * i + 5] for i in range(64) if st[8 + 8 * i] != 0]
+        rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
+        summary = {"k1_end": rel(st[1])}
+        for k, name in enumerate(["k2_entry", "merged_pushed", "fenced_flagged", "peers_seen", "done"]):
+            vals = [bl[k] for bl in blocks if bl[k]]
+            if vals:
+                summary[name + "_min"] = rel(min(vals))
+                summary[name + "_max"] = rel(max(vals))
+        res.append(summary)
+    print(json.dumps({"rank": local, "world": world, "combine": args.combine, "steps": res[1:]}), flush=True)
+    w.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

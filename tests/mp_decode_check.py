@@ -29,6 +29,7 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     orc = Oracle()
     w = td.Worker.from_torch_distributed(local)
+    w.enable_p2p(2 * 32, 128)
     cases = [  # dtype, b, n_q, n_kv, n, d, scale
         (BF16, 1, 32, 8, 262144 + 3, 128, 1.0),
         (BF16, 2, 8, 8, 20001, 128, 0.0883883476),
@@ -42,6 +43,8 @@ def main():
         q = td.seeded_tensor([b, n_q, d], orc.mix64(seed, 1), 1.0, td.DType(dt))
         tree = w.tree_decode(q, scale)
         ring = w.ring_decode(q, scale)
+        fits = b * n_q <= 64 and d == 128
+        p2p = w.tree_decode(q, scale, flags=td._capi.TD_P2P) if fits else tree
         # every rank must hold the same output
         t_all = [torch.empty_like(tree) for _ in range(world)]
         dist.all_gather(t_all, tree)
@@ -57,11 +60,12 @@ def main():
             mx = np.max(np.abs(want))
             e_tree = float(np.max(np.abs(tree[:, :g].double().cpu().numpy() - want)) / mx)
             e_ring = float(np.max(np.abs(ring[:, :g].double().cpu().numpy() - want)) / mx)
+            e_p2p = float(np.max(np.abs(p2p[:, :g].double().cpu().numpy() - want)) / mx)
             same = all(torch.equal(t_all[0], x) for x in t_all)
-            good = e_tree <= tol and e_ring <= tol and same
+            good = e_tree <= tol and e_ring <= tol and e_p2p <= tol and same and w.p2p_status() == 0
             ok &= good
             print(json.dumps({"world": world, "dtype": "bf16" if dt == BF16 else "f32", "n": n, "b": b, "n_q": n_q,
-                              "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring,
+                              "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring, "p2p_rel_err": e_p2p,
                               "ranks_agree": same, "ok": good}), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
