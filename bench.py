@@ -159,6 +159,23 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
+def align_streams(world, stream):
+    """After a host barrier the ranks' GPUs start their queues up to hundreds of
+    us apart, and the first exchange of the timed loop would absorb that skew.
+    A one-element NCCL allreduce, followed on the library stream by a
+    device-side wait (no host sync), releases every rank's first step within
+    microseconds of each other."""
+    if world == 1:
+        return
+    import torch
+    import torch.distributed as dist
+    t = torch.ones(1, device="cuda")
+    dist.all_reduce(t)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream())
+    stream.wait_event(ev)
+
+
 # ---------------------------------------------------------------- CPU reference (oracle/_ref)
 def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
     """Times the reference's own tree_decode (compiled from /root/reference by
@@ -280,14 +297,26 @@ def main():
     w.reset_kernel_timer()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # pass A: the step as a user runs it (per-step events around the call only)
         barrier(world)
+        align_streams(world, stream)
         for i in range(args.steps):
             if flush:
                 with torch.cuda.stream(stream):
                     scratch.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            step(flags_timed)
+            step(0)
             evs[i][1].record(stream)
+        barrier(world)
+        # pass B: the same steps with CUDA events around the split-KV kernel (K1)
+        # for the roofline (an event between K1 and K2 would serialise the PDL
+        # launch, so it is kept out of pass A)
+        align_streams(world, stream)
+        for i in range(args.steps):
+            if flush:
+                with torch.cuda.stream(stream):
+                    scratch.fill_(i & 0xFF)
+            step(flags_timed)
         barrier(world)
     step_ms = [a.elapsed_time(bb) for a, bb in evs]
     ms_local = sum(step_ms) / len(step_ms)
@@ -318,6 +347,7 @@ def main():
     if args.phases:
         barrier(world)
         w.reset_kernel_timer()
+        align_streams(world, stream)
         for _ in range(max(3, min(args.steps, 20))):
             step(_capi.TD_TIME_PHASES)
         barrier(world)

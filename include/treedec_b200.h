@@ -189,7 +189,8 @@ int td_phase_times(td_context* ctx, double* phases, int max_phases, int* n, int*
 
 /* Stamps of the last TD_DEBUG_TS call (ns, %globaltimer): [0] first K1 CTA
  * start, [1] last K1 CTA end, [8 + 8*blk + k] stages of K2 block blk
- * (0 entry, 1 merged + pushed, 2 fenced + flagged, 3 peers seen, 4 done). */
+ * (0 entry, 1 merged + pushed, 2 fenced + flagged, 3 peers seen, 4 done),
+ * [4096 + 2c], [4097 + 2c] start / end of K1 CTA c (n up to 6144). */
 int td_debug_stamps(td_context* ctx, unsigned long long* out, int n);
 
 /* Kernels of this library launched by the last decode call, and the

@@ -281,7 +281,7 @@ int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const voi
     }
     TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
                                       ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
-    ctx->last_kernels += 2;
+    ctx->last_kernels += 2;  // K1 + K2
     ctx->last_kv_bytes += 2.0 * double(ctx->b) * double(ctx->n_kv) * double(t) * double(ctx->d) *
                           td::dtype_bytes(ctx->dtype);
     ctx->last_split_kernel = plan.kernel;
@@ -659,8 +659,8 @@ static int debug_begin(td_context* ctx, int flags) {
         td::set_debug_stamps(nullptr);
         return TD_OK;
     }
-    TD_CUDA(ctx->dbg.ensure(4200 * sizeof(unsigned long long)));
-    TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 4200 * sizeof(unsigned long long), ctx->stream));
+    TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
+    TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream));
     TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xff, sizeof(unsigned long long), ctx->stream));
     td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
     return TD_OK;
@@ -670,7 +670,7 @@ int td_debug_stamps(td_context* ctx, unsigned long long* out, int n) {
     if (int rc = require_ctx(ctx)) return rc;
     if (!ctx->dbg.p) return set_err(TD_ESTATE, "no TD_DEBUG_TS call made");
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
-    TD_CUDA(cudaMemcpy(out, ctx->dbg.p, sizeof(unsigned long long) * size_t(std::min(n, 4200)),
+    TD_CUDA(cudaMemcpy(out, ctx->dbg.p, sizeof(unsigned long long) * size_t(std::min(n, 6144)),
                        cudaMemcpyDeviceToHost));
     return TD_OK;
 }
@@ -720,14 +720,38 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         } else if (ctx->cur_phase) {
             e1 = (*ctx->cur_phase)[ctx->cur_mark++];
         }
+        float* xdst = (flags & TD_HOST_IO) ? ctx->out : out;
+        if (ctx->b * ctx->n_kv > td::kXchgBlocks)
+            return set_err(TD_EINVAL, "tree_decode: TD_P2P supports at most 1024 (batch, kv-head) rows");
         TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
-                                           ctx->ws.p, xa, ctx->out, ctx->stream, e0, e1));
+                                           ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
         phase_mark(ctx);
-        ctx->last_kernels = 2;
+        ctx->last_kernels = 2;  // K1 + K2x
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
                              td::dtype_bytes(ctx->dtype);
         ctx->last_split_kernel = plan.kernel;
-        return deliver_out(ctx, ctx->out, rows, out, flags);
+        return deliver_out(ctx, xdst, rows, out, flags);
+    }
+    if (ctx->nranks == 1) {
+        // p = 1: the shard partial is the result (shift = lse, w = 1): one kernel,
+        // written straight into the caller's buffer when it is on the device
+        float* dst = (flags & TD_HOST_IO) ? ctx->out : out;
+        const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
+        const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (flags & TD_TIME_KERNELS) {
+            cudaEvent_t* pr = next_timer(ctx);
+            e0 = pr[0];
+            e1 = pr[1];
+        }
+        TD_CUDA(td::launch_decode_final(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
+                                        ctx->ws.p, dst, ctx->stream, e0, e1));
+        phase_mark(ctx);
+        ctx->last_kernels = 2;  // K1 + K2
+        ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
+                             td::dtype_bytes(ctx->dtype);
+        ctx->last_split_kernel = plan.kernel;
+        return deliver_out(ctx, dst, rows, out, flags);
     }
     // 1. local partial (out, lse) of this shard
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,

@@ -43,7 +43,7 @@ void set_debug_stamps(unsigned long long* buf);
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
                 SplitPlan& plan, std::string& msg);
 
-// K1 + K2: attention_chunk_partial of q against one shard, written as fp32
+// K1 (+ merge tail): attention_chunk_partial of q against one shard, written as fp32
 // (row_max, lse, out) rows [b][n_q] / [b][n_q][d]. tmk/tmv are the shard's
 // tensor maps (bf16 mma kernel only; may be null otherwise).
 cudaError_t launch_decode_partial(const SplitPlan& plan, const void* q, const void* k,
@@ -52,10 +52,11 @@ cudaError_t launch_decode_partial(const SplitPlan& plan, const void* q, const vo
                                   float* lse, float* out, cudaStream_t stream,
                                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
-// K1 alone (events around it when given).
-cudaError_t launch_split(const SplitPlan& plan, const void* q, const void* k, const void* v,
-                         float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
-                         void* workspace, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1);
+// K1 with the final-output tail (p = 1: the local partial is the answer).
+cudaError_t launch_decode_final(const SplitPlan& plan, const void* q, const void* k, const void* v,
+                                float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
+                                void* workspace, float* out, cudaStream_t stream,
+                                cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // One-shot NVLink exchange buffers (td_p2p_*): every rank's exchange buffer
 // holds [2 parities][p sources][max_rows lse | max_rows*d out] floats; flags
@@ -72,7 +73,7 @@ struct XchgArgs {
 };
 constexpr int kXchgBlocks = 1024;
 
-// K1 + K2x: split-KV partial, merge, one-shot exchange and exact combine;
+// K1 + exchange tail: split-KV partial, merge, one-shot exchange and exact combine;
 // out [b, n_q, d] fp32 final (identical on every rank).
 cudaError_t launch_decode_exchange(const SplitPlan& plan, const void* q, const void* k, const void* v,
                                    float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,

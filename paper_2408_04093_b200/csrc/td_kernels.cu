@@ -29,6 +29,30 @@
 
 namespace td {
 
+// One-shot NVLink exchange (the single-collective exact combine, SURVEY.md
+// 8(f)1): every rank's exchange buffer holds [2 parities][p sources]
+// [max_rows lse | max_rows * d out] floats; flags are [2][p][kXchgBlocks]
+// u32, one per (parity, source, bh).
+struct Xchg {
+    float* const* peers;  // [p] exchange buffers (own included), device array
+    unsigned* flags;      // own flags
+    unsigned* const* peer_flags;
+    int p, rank;
+    unsigned epoch;
+    int64_t max_rows;
+    int* error;           // set on timeout
+};
+
+// What K2 does with the merged rows.
+enum TailMode { kTailPartial = 0, kTailFinal = 1, kTailExchange = 2 };
+struct Tail {
+    int mode;
+    float* row_max;      // [b][n_q]      (partial)
+    float* lse;          // [b][n_q]      (partial)
+    float* out;          // [b][n_q][d]   (partial / final)
+    Xchg x;              // (exchange)
+};
+
 struct K1Args {
     const void* q;  // [b][n_q][d], kv dtype
     const void* k;  // [bh][t][d]
@@ -43,6 +67,7 @@ struct K1Args {
     float* cslot_l;
     float* cslot_o; // [ctas * maxseg][group][d]
     unsigned long long* dbg;  // optional globaltimer stamps (TD_DEBUG_TS)
+    Tail tail;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -50,6 +75,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+
 
 __device__ __forceinline__ int64_t cta_begin(int64_t total, int c, int ctas) {
     return total * c / ctas;
@@ -128,6 +154,9 @@ __global__ void __launch_bounds__(W * 32, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
     const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
+    // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
+    // (griddepcontrol.wait) for this grid's completion before reading.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -357,8 +386,13 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncthreads();
     cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
     if (a.dbg && threadIdx.x == 0) {
+        const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
-        atomicMax(a.dbg + 1, gtimer());
+        atomicMax(a.dbg + 1, t_end);
+        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c]
+            a.dbg[4096 + 2 * c] = t_start;
+            a.dbg[4096 + 2 * c + 1] = t_end;
+        }
     }
 }
 
@@ -378,6 +412,9 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
 
     const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
+    // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
+    // (griddepcontrol.wait) for this grid's completion before reading.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -536,8 +573,13 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     __syncthreads();
     cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
     if (a.dbg && threadIdx.x == 0) {
+        const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
-        atomicMax(a.dbg + 1, gtimer());
+        atomicMax(a.dbg + 1, t_end);
+        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c]
+            a.dbg[4096 + 2 * c] = t_start;
+            a.dbg[4096 + 2 * c + 1] = t_end;
+        }
     }
 }
 
@@ -557,7 +599,11 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
     constexpr int T = 32;
     constexpr int W = 4;
     extern __shared__ float gen_smem[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
+    // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
+    // (griddepcontrol.wait) for this grid's completion before reading.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
@@ -689,9 +735,9 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
         const int c = static_cast<int>(c_lo + i);
         const int64_t cs = int64_t(c) * a.maxseg + (bh - cta_begin(a.total_tiles, c, a.ctas) / a.tiles_per_bh);
-        const float m = a.cslot_m[cs * g + h];
+        const float m = __ldcg(a.cslot_m + cs * g + h);
         sm.m[i] = m;
-        sm.l[i] = a.cslot_l[cs * g + h];
+        sm.l[i] = __ldcg(a.cslot_l + cs * g + h);
         sm.cs[i] = cs;
         mloc = fmaxf(mloc, m);
     }
@@ -712,17 +758,31 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
     __syncthreads();
     float L = 0.f;
     for (int i = 0; i < nw; ++i) L += sm.red[i];
-    // o rows: thread (grp, j) sums candidates grp, grp + NG, ...
-    const int NG = blockDim.x / D;
-    const int grp = threadIdx.x / D, j = threadIdx.x % D;
+    // o rows: thread (grp, j) sums candidates grp, grp + NG, ... (with
+    // blockDim < D, one group and each thread takes several j)
+    const int NG = blockDim.x >= static_cast<unsigned>(D) ? static_cast<int>(blockDim.x) / D : 1;
+    const int grp = blockDim.x >= static_cast<unsigned>(D) ? static_cast<int>(threadIdx.x) / D : 0;
+    const int jstep = blockDim.x >= static_cast<unsigned>(D) ? D : static_cast<int>(blockDim.x);
     if (grp < NG) {
-        float acc = 0.f;
-#pragma unroll 8
-        for (int i = grp; i < S; i += NG) {
-            const float e = sm.e[i];
-            if (e != 0.f) acc += e * a.cslot_o[(sm.cs[i] * g + h) * D + j];
+        for (int j = blockDim.x >= static_cast<unsigned>(D) ? threadIdx.x % D : threadIdx.x; j < D; j += jstep) {
+            // cta_merge writes every cslot_o (0 for empty segments), so the loads are
+            // unconditional and independent: issue them in batches of 8
+            float acc = 0.f;
+            for (int i = grp; i < S; i += 8 * NG) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int iu = i + u * NG;
+                    v[u] = iu < S ? __ldcg(a.cslot_o + (sm.cs[iu] * g + h) * D + j) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int iu = i + u * NG;
+                    acc += (iu < S ? sm.e[iu] : 0.f) * v[u];
+                }
+            }
+            sm.acc[grp * D + j] = acc;
         }
-        sm.acc[threadIdx.x] = acc;
     }
     __syncthreads();
     for (int jj = threadIdx.x; jj < D; jj += blockDim.x) {
@@ -740,49 +800,6 @@ __device__ __forceinline__ int64_t out_row_of(const K1Args& a, int64_t r) {
     return (bh / a.n_kv) * a.n_q + (bh % a.n_kv) * a.group + h;
 }
 
-// K2: merge the split states of each (b, q-head) row into the shard's
-// partial: out = O/L, lse = (M + log2 L) ln 2, row_max = M ln 2. Empty rows
-// give the identity (-inf, -inf, 0), like attention_chunk_partial on an
-// empty chunk (attention.cpp:56-61).
-__global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a, float* row_max,
-                                                         float* lse, float* out) {
-    __shared__ K2Smem sm;
-    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
-    if (ts && threadIdx.x == 0) ts[0] = gtimer();
-    const int64_t rows = a.bh_count * a.group;
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const int64_t orow = out_row_of(a, r);
-        float l, m;
-        merge_row(a, r, sm, out + orow * a.d, l, m);
-        if (threadIdx.x == 0) {
-            lse[orow] = l;
-            row_max[orow] = m;
-        }
-    }
-    if (ts && threadIdx.x == 0) ts[4] = gtimer();
-}
-
-// =========================================================================
-// K2x: K2 fused with a one-shot NVLink exchange (the single-collective exact
-// combine of SURVEY.md 8(f)1). Each block merges its rows' split states,
-// stores [lse | out] of those rows into slot `rank` of every peer's exchange
-// buffer (CUDA-IPC mapped HBM, plain stores over NVLink), raises one flag
-// per (peer, block), waits for the p flags of its own rows, and combines the
-// p partials locally: shift = max lse, w = e^(lse - shift), out = sum w o /
-// sum w -- the max-allreduce / rescale / sum-allreduce / divide of
-// decode.cpp:129-173 in one exchange. Slots alternate by epoch parity, so a
-// rank can never overwrite a slot a peer is still reading. The grid never
-// exceeds the co-resident capacity, so every block pushes before any waits.
-// =========================================================================
-struct Xchg {
-    float* const* peers;  // [p] exchange buffers (own included), device array
-    unsigned* flags;      // own flags [2][p][kXchgMaxBlocks]
-    unsigned* const* peer_flags;
-    int p, rank;
-    unsigned epoch;
-    int64_t max_rows;
-    int* error;           // set on timeout
-};
 constexpr int kXchgMaxBlocks = kXchgBlocks;
 
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
@@ -794,46 +811,81 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a, Xchg x,
-                                                          float* out) {
+// =========================================================================
+// K2 (launched with programmatic dependent launch: its blocks are scheduled
+// as K1's CTAs retire and wait in griddepcontrol.wait, so the kernel
+// boundary costs no launch latency). Each block merges rows r = blockIdx,
+// blockIdx + grid, ... of the shard (merge_row over the CTA states) and, per
+// a.tail.mode:
+//   kTailPartial  row_max / lse / out of the shard -- attention_chunk_partial
+//                 (attention.cpp:146-168), combine_partials across CTAs
+//                 (attention.cpp:207-241)
+//   kTailFinal    out only (p = 1: the partial is the decode result)
+// =========================================================================
+__global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     __shared__ K2Smem sm;
-    __shared__ float lse_s;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
+    const Tail& t = a.tail;
+    const int64_t rows = a.bh_count * a.group;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t orow = out_row_of(a, r);
+        float l, m;
+        merge_row(a, r, sm, t.out + orow * a.d, l, m);
+        if (t.mode == kTailPartial && threadIdx.x == 0) {
+            t.lse[orow] = l;
+            t.row_max[orow] = m;
+        }
+    }
+    if (ts && threadIdx.x == 0) ts[4] = gtimer();
+}
+
+// =========================================================================
+// K2x: K2 fused with the one-shot NVLink exchange (kTailExchange). Each
+// block merges its rows, stores [lse | out] of them into slot `rank` of every
+// peer's exchange buffer (CUDA-IPC mapped HBM, plain stores over NVLink),
+// fence.sys, raises flag (rank, block) on every peer, waits for the p
+// sources' flags of its block and combines its rows: shift = max lse,
+// w = e^(lse - shift), out = sum w o / sum w -- allreduce(max),
+// partial_to_numerator, allreduce(sum) and n/d of decode.cpp:129-173 in one
+// exchange. Slots alternate by epoch parity (a rank cannot overwrite a slot a
+// peer still reads: it would first need the peer's next-step flag). The grid
+// never exceeds the co-resident capacity and every block pushes before it
+// waits, so the exchange cannot deadlock; the spin is bounded (~2 s).
+// =========================================================================
+__global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
+    __shared__ K2Smem sm;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const Xchg& x = a.tail.x;
     const int64_t rows = a.bh_count * a.group;
     const int D = a.d;
     const unsigned par = x.epoch & 1u;
-    const int64_t stride = x.max_rows * int64_t(D + 1);  // floats per (parity, src) slot
+    const int64_t stride = x.max_rows * int64_t(D + 1);  // floats per (parity, source)
     unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
     if (ts && threadIdx.x == 0) ts[0] = gtimer();
-    // 1. merge + push my rows
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float* own = x.peers[x.rank] + (int64_t(par) * x.p + x.rank) * stride;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // merge + push
         const int64_t orow = out_row_of(a, r);
-        float* own = x.peers[x.rank] + (int64_t(par) * x.p + x.rank) * stride;
         float l, m;
-        merge_row(a, r, sm, own + x.max_rows + orow * D, l, m);
-        if (threadIdx.x == 0) {
-            own[orow] = l;
-            lse_s = l;
-        }
-        __syncthreads();
-        const float* src = own + x.max_rows + orow * D;
+        merge_row(a, r, sm, own + x.max_rows + orow * D, l, m);  // ends with a barrier
         for (int q = 0; q < x.p; ++q) {
-            if (q == x.rank) continue;
-            float* dst = x.peers[q] + (int64_t(par) * x.p + x.rank) * stride;
-            for (int j = threadIdx.x; j < D; j += blockDim.x) dst[x.max_rows + orow * D + j] = src[j];
-            if (threadIdx.x == 0) dst[orow] = lse_s;
+            float* dst = q == x.rank ? own : x.peers[q] + (int64_t(par) * x.p + x.rank) * stride;
+            if (q != x.rank)
+                for (int j = threadIdx.x; j < D; j += blockDim.x)
+                    dst[x.max_rows + orow * D + j] = own[x.max_rows + orow * D + j];
+            if (threadIdx.x == 0) dst[orow] = l;
         }
     }
     __syncthreads();
     if (ts && threadIdx.x == 0) ts[1] = gtimer();
-    // 2. publish: one flag per (peer, block)
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // publish
         __threadfence_system();
         if (ts) ts[2] = gtimer();
         for (int q = 0; q < x.p; ++q)
             st_release_sys(x.peer_flags[q] + (par * x.p + x.rank) * kXchgMaxBlocks + blockIdx.x, x.epoch);
     }
-    // 3. wait for every source's flag of this block
-    if (threadIdx.x < x.p) {
+    if (threadIdx.x < static_cast<unsigned>(x.p)) {  // wait for the p sources of this block
         const unsigned* f = x.flags + (par * x.p + threadIdx.x) * kXchgMaxBlocks + blockIdx.x;
         const long long t0 = clock64();
         while (ld_acquire_sys(f) != x.epoch) {
@@ -841,13 +893,12 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a, Xchg x
                 atomicExch(x.error, 1);
                 break;
             }
-            __nanosleep(64);
+            __nanosleep(32);
         }
     }
     __syncthreads();
     if (ts && threadIdx.x == 0) ts[3] = gtimer();
-    // 4. exact combine of the p partials of my rows
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // exact combine of the p partials
         const int64_t orow = out_row_of(a, r);
         float shift = -CUDART_INF_F;
         for (int q = 0; q < x.p; ++q)
@@ -857,12 +908,11 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a, Xchg x
             for (int q = 0; q < x.p; ++q) {
                 const float* slot = x.peers[x.rank] + (int64_t(par) * x.p + q) * stride;
                 const float l = __ldcg(slot + orow);
-                if (l == -CUDART_INF_F) continue;
-                const float w = expf(l - shift);
+                const float w = l == -CUDART_INF_F ? 0.f : expf(l - shift);
                 den += w;
                 num += w * __ldcg(slot + x.max_rows + orow * D + j);
             }
-            out[orow * D + j] = num / den;
+            a.tail.out[orow * D + j] = num / den;
         }
     }
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
@@ -1114,10 +1164,11 @@ bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, in
     return true;
 }
 
-cudaError_t launch_split(const SplitPlan& p, const void* q, const void* k, const void* v,
-                         float scale, const CUtensorMap* tmk, const CUtensorMap* tmv, void* ws,
-                         cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
-    const K1Args a = make_args(p, q, k, v, scale, ws);
+namespace {
+
+// One K1 launch (any variant) with the tail configured in a.
+cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tmk,
+                      const CUtensorMap* tmv, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
     cudaError_t e = cudaSuccess;
     if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
     if (p.kernel == 1) {
@@ -1153,7 +1204,8 @@ cudaError_t launch_split(const SplitPlan& p, const void* q, const void* k, const
         default: return cudaErrorInvalidValue;
         }
     } else {
-        const size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
+        size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
+        if (sm < sizeof(K2Smem)) sm = sizeof(K2Smem);
         if (p.dtype == kBF16) {
             if ((e = set_smem(k1_generic<__nv_bfloat16>, sm)) != cudaSuccess) return e;
             k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
@@ -1167,44 +1219,75 @@ cudaError_t launch_split(const SplitPlan& p, const void* q, const void* k, const
     return cudaSuccess;
 }
 
+}  // namespace
+
+namespace {
+
+// K2 right behind K1 with programmatic stream serialization (PDL).
+cudaError_t launch_k2(const K1Args& a, int64_t grid, bool exchange, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid < 1 ? 1 : grid));
+    cfg.blockDim = dim3(K2_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange, a) : cudaLaunchKernelEx(&cfg, k2_combine, a);
+}
+
+}  // namespace
+
 cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void* k,
                                   const void* v, float scale, const CUtensorMap* tmk,
                                   const CUtensorMap* tmv, void* ws, float* row_max, float* lse,
                                   float* out, cudaStream_t st, cudaEvent_t ev0,
                                   cudaEvent_t ev1) {
-    cudaError_t e = launch_split(p, q, k, v, scale, tmk, tmv, ws, st, ev0, ev1);
+    K1Args a = make_args(p, q, k, v, scale, ws);
+    a.tail.mode = kTailPartial;
+    a.tail.row_max = row_max;
+    a.tail.lse = lse;
+    a.tail.out = out;
+    cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
-    const K1Args a = make_args(p, q, k, v, scale, ws);
-    int64_t rows = p.bh_count * p.group;
-    k2_combine<<<static_cast<unsigned>(rows < 4096 ? rows : 4096), K2_THREADS, 0, st>>>(a, row_max,
-                                                                                        lse, out);
-    return cudaGetLastError();
+    const int64_t rows = p.bh_count * p.group;
+    return launch_k2(a, rows < 4096 ? rows : 4096, false, st);
 }
 
-
+cudaError_t launch_decode_final(const SplitPlan& p, const void* q, const void* k, const void* v,
+                                float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
+                                void* ws, float* out, cudaStream_t st, cudaEvent_t ev0,
+                                cudaEvent_t ev1) {
+    K1Args a = make_args(p, q, k, v, scale, ws);
+    a.tail.mode = kTailFinal;
+    a.tail.out = out;
+    cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
+    if (e != cudaSuccess) return e;
+    const int64_t rows = p.bh_count * p.group;
+    return launch_k2(a, rows < 4096 ? rows : 4096, false, st);
+}
 
 cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void* k, const void* v,
                                    float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
                                    void* ws, const XchgArgs& xa, float* out, cudaStream_t st,
                                    cudaEvent_t ev0, cudaEvent_t ev1) {
-    // K1 (+ events) through the partial launcher with K2 suppressed
-    cudaError_t e = launch_split(p, q, k, v, scale, tmk, tmv, ws, st, ev0, ev1);
+    K1Args a = make_args(p, q, k, v, scale, ws);
+    a.tail.mode = kTailExchange;
+    a.tail.out = out;
+    a.tail.x.peers = xa.peers;
+    a.tail.x.flags = xa.flags;
+    a.tail.x.peer_flags = xa.peer_flags;
+    a.tail.x.p = xa.p;
+    a.tail.x.rank = xa.rank;
+    a.tail.x.epoch = xa.epoch;
+    a.tail.x.max_rows = xa.max_rows;
+    a.tail.x.error = xa.error;
+    cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
-    const K1Args a = make_args(p, q, k, v, scale, ws);
-    Xchg x{};
-    x.peers = xa.peers;
-    x.flags = xa.flags;
-    x.peer_flags = xa.peer_flags;
-    x.p = xa.p;
-    x.rank = xa.rank;
-    x.epoch = xa.epoch;
-    x.max_rows = xa.max_rows;
-    x.error = xa.error;
     const int64_t rows = p.bh_count * p.group;
-    int64_t grid = rows < xa.max_blocks ? rows : xa.max_blocks;
-    if (grid < 1) grid = 1;
-    k2_exchange<<<static_cast<unsigned>(grid), K2_THREADS, 0, st>>>(a, x, out);
-    return cudaGetLastError();
+    return launch_k2(a, rows < xa.max_blocks ? rows : xa.max_blocks, true, st);
 }
 
 namespace {

@@ -43,11 +43,17 @@ def main():
     res = []
     for _ in range(5):
         w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags | _capi.TD_DEBUG_TS)
-        st = w.debug_stamps(8 + 8 * 64)
+        st = w.debug_stamps(6144)
         t0 = st[0]
+        ends = sorted((st[4097 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4097 + 2 * c])
+        starts = sorted((st[4096 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4096 + 2 * c])
         blocks = [st[8 + 8 * i: 8 + 8 * i + 5] for i in range(64) if st[8 + 8 * i] != 0]
         rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
         summary = {"k1_end": rel(st[1])}
+        if ends:
+            q = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
+            summary["cta_start_q"] = [q(starts, f) for f in (0.0, 0.5, 1.0)]
+            summary["cta_end_q"] = [q(ends, f) for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
         for k, name in enumerate(["k2_entry", "merged_pushed", "fenced_flagged", "peers_seen", "done"]):
             vals = [bl[k] for bl in blocks if bl[k]]
             if vals:
