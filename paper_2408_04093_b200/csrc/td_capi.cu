@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -710,6 +711,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         xa.max_rows = ctx->x_max_rows;
         xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 2 * int64_t(ctx->sm_count));
         xa.error = static_cast<int*>(ctx->x_err.p);
+        if (const char* v = std::getenv("TD_XCHG_VARIANT")) xa.variant = std::atoi(v);
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
         const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;

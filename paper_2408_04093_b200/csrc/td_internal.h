@@ -70,6 +70,7 @@ struct XchgArgs {
     int64_t max_rows = 0;
     int64_t max_blocks = 0;
     int* error = nullptr;
+    int variant = 0;
 };
 constexpr int kXchgBlocks = 1024;
 

@@ -41,6 +41,7 @@ struct Xchg {
     unsigned epoch;
     int64_t max_rows;
     int* error;           // set on timeout
+    int variant;          // flag protocol (TD_XCHG_VARIANT, experiments)
 };
 
 // What K2 does with the merged rows.
@@ -877,24 +878,41 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
             if (threadIdx.x == 0) dst[orow] = l;
         }
     }
+    if (x.variant == 4) __threadfence_system();  // every writer fences its own stores
     __syncthreads();
     if (ts && threadIdx.x == 0) ts[1] = gtimer();
     if (threadIdx.x == 0) {  // publish
-        __threadfence_system();
+        if (x.variant != 4) __threadfence_system();
         if (ts) ts[2] = gtimer();
-        for (int q = 0; q < x.p; ++q)
-            st_release_sys(x.peer_flags[q] + (par * x.p + x.rank) * kXchgMaxBlocks + blockIdx.x, x.epoch);
+        for (int q = 0; q < x.p; ++q) {
+            unsigned* f = x.peer_flags[q] + (par * x.p + x.rank) * kXchgMaxBlocks + blockIdx.x;
+            if (x.variant == 1 || x.variant == 4)
+                asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(f), "r"(x.epoch) : "memory");
+            else if (x.variant == 2)
+                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(x.epoch) : "memory");
+            else
+                st_release_sys(f, x.epoch);
+        }
     }
     if (threadIdx.x < static_cast<unsigned>(x.p)) {  // wait for the p sources of this block
         const unsigned* f = x.flags + (par * x.p + threadIdx.x) * kXchgMaxBlocks + blockIdx.x;
         const long long t0 = clock64();
-        while (ld_acquire_sys(f) != x.epoch) {
+        for (;;) {
+            unsigned v;
+            if (x.variant == 1 || x.variant == 4)
+                asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            else if (x.variant == 2)
+                asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            else
+                v = ld_acquire_sys(f);
+            if (v == x.epoch) break;
             if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
                 atomicExch(x.error, 1);
                 break;
             }
-            __nanosleep(32);
+            if (x.variant == 0) __nanosleep(32);
         }
+        if (x.variant == 1 || x.variant == 2 || x.variant == 4) __threadfence_system();  // acquire side
     }
     __syncthreads();
     if (ts && threadIdx.x == 0) ts[3] = gtimer();
@@ -1284,6 +1302,7 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.x.epoch = xa.epoch;
     a.tail.x.max_rows = xa.max_rows;
     a.tail.x.error = xa.error;
+    a.tail.x.variant = xa.variant;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
     const int64_t rows = p.bh_count * p.group;
