@@ -508,7 +508,8 @@ int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char ha
     for (void* ptr : ctx->x_opened) cudaIpcCloseMemHandle(ptr);
     ctx->x_opened.clear();
     ctx->x_ready = false;
-    const size_t data = 2 * size_t(ctx->nranks) * size_t(max_rows) * size_t(d + 1) * sizeof(float);
+    // LL words (value, epoch): [2 parities][p sources][max_rows][d + 1] x 8 bytes
+    const size_t data = 2 * size_t(ctx->nranks) * size_t(max_rows) * size_t(d + 1) * 2 * sizeof(float);
     const size_t flags = 2 * size_t(ctx->nranks) * td::kXchgBlocks * sizeof(unsigned);
     ctx->xbuf.release();
     TD_CUDA(ctx->xbuf.ensure(data + flags));
@@ -711,7 +712,6 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         xa.max_rows = ctx->x_max_rows;
         xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 2 * int64_t(ctx->sm_count));
         xa.error = static_cast<int*>(ctx->x_err.p);
-        if (const char* v = std::getenv("TD_XCHG_VARIANT")) xa.variant = std::atoi(v);
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
         const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -59,7 +59,7 @@ cudaError_t launch_decode_final(const SplitPlan& plan, const void* q, const void
                                 cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // One-shot NVLink exchange buffers (td_p2p_*): every rank's exchange buffer
-// holds [2 parities][p sources][max_rows lse | max_rows*d out] floats; flags
+// holds [2 parities][p sources][max_rows][d out | lse] LL words (value, epoch); flags
 // are [2][p][kXchgMaxBlocks] u32 per rank.
 struct XchgArgs {
     float* const* peers;       // device array [p]
@@ -70,7 +70,6 @@ struct XchgArgs {
     int64_t max_rows = 0;
     int64_t max_blocks = 0;
     int* error = nullptr;
-    int variant = 0;
 };
 constexpr int kXchgBlocks = 1024;
 

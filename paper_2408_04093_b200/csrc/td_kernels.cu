@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "td_device.cuh"
 #include "td_internal.h"
@@ -31,8 +34,7 @@ namespace td {
 
 // One-shot NVLink exchange (the single-collective exact combine, SURVEY.md
 // 8(f)1): every rank's exchange buffer holds [2 parities][p sources]
-// [max_rows lse | max_rows * d out] floats; flags are [2][p][kXchgBlocks]
-// u32, one per (parity, source, bh).
+// [max_rows][d out | lse] LL words (value bits, epoch) -- see k2_exchange.
 struct Xchg {
     float* const* peers;  // [p] exchange buffers (own included), device array
     unsigned* flags;      // own flags
@@ -41,7 +43,6 @@ struct Xchg {
     unsigned epoch;
     int64_t max_rows;
     int* error;           // set on timeout
-    int variant;          // flag protocol (TD_XCHG_VARIANT, experiments)
 };
 
 // What K2 does with the merged rows.
@@ -703,92 +704,85 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
 // =========================================================================
 constexpr int K2_THREADS = 512;
 
-constexpr int kK2MaxCand = 1024;
-
 struct K2Smem {
-    float m[kK2MaxCand];
-    float l[kK2MaxCand];
-    float e[kK2MaxCand];
-    int64_t cs[kK2MaxCand];
-    float red[K2_THREADS / 32];
-    float acc[K2_THREADS];
+    float m[K2_THREADS];    // per-group running max (log2 units)
+    float l[K2_THREADS];    // per-group running sum
+    float acc[K2_THREADS];  // per-group running o, [grp][j]
 };
 
 // Merges the CTA states of row r (over bh_count * group) into out_row (D
-// floats, any address space) and returns (lse, row_max) in natural log
-// units: two bulk rounds of independent loads (the (m, l) of every covering
-// CTA, then their o rows spread over all threads). All threads call it.
+// floats, any address space) and returns (lse, row_max) in natural log units.
+// One round of independent loads: thread (grp, j) streams the candidates
+// grp, grp + NG, ... of its d-column with an online rescale, then the NG
+// group states are merged through shared memory (one barrier). Only the
+// first covering CTA can start in an earlier bh, so no per-candidate
+// division is needed. All threads of the block call it.
 __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row, float& lse_o,
                           float& rmax_o) {
     const int64_t bh = r / a.group;
     const int h = static_cast<int>(r % a.group);
     const int D = a.d, g = a.group;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    int64_t c_lo = 0, c_hi = -1;
+    int64_t c_lo = 0, c_hi = -1, seg_lo = 0;
     if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
         const int64_t X = bh * a.tiles_per_bh, Xe = X + a.tiles_per_bh - 1;
         c_lo = ((X + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
         c_hi = ((Xe + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
+        seg_lo = bh - cta_begin(a.total_tiles, static_cast<int>(c_lo), a.ctas) / a.tiles_per_bh;
     }
     const int S = static_cast<int>(c_hi - c_lo + 1);
-    float mloc = -CUDART_INF_F;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const int c = static_cast<int>(c_lo + i);
-        const int64_t cs = int64_t(c) * a.maxseg + (bh - cta_begin(a.total_tiles, c, a.ctas) / a.tiles_per_bh);
-        const float m = __ldcg(a.cslot_m + cs * g + h);
-        sm.m[i] = m;
-        sm.l[i] = __ldcg(a.cslot_l + cs * g + h);
-        sm.cs[i] = cs;
-        mloc = fmaxf(mloc, m);
-    }
-    for (int off = 16; off >= 1; off >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
-    if (lane == 0) sm.red[warp] = mloc;
-    __syncthreads();
-    float M = -CUDART_INF_F;
-    for (int i = 0; i < nw; ++i) M = fmaxf(M, sm.red[i]);
-    __syncthreads();
-    float lpart = 0.f;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const float e = (sm.m[i] == -CUDART_INF_F) ? 0.f : exp2f(sm.m[i] - M);
-        sm.e[i] = e;
-        lpart += e * sm.l[i];
-    }
-    for (int off = 16; off >= 1; off >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, off);
-    if (lane == 0) sm.red[warp] = lpart;
-    __syncthreads();
-    float L = 0.f;
-    for (int i = 0; i < nw; ++i) L += sm.red[i];
-    // o rows: thread (grp, j) sums candidates grp, grp + NG, ... (with
-    // blockDim < D, one group and each thread takes several j)
-    const int NG = blockDim.x >= static_cast<unsigned>(D) ? static_cast<int>(blockDim.x) / D : 1;
-    const int grp = blockDim.x >= static_cast<unsigned>(D) ? static_cast<int>(threadIdx.x) / D : 0;
-    const int jstep = blockDim.x >= static_cast<unsigned>(D) ? D : static_cast<int>(blockDim.x);
+    const bool wide = blockDim.x >= static_cast<unsigned>(D);
+    const int NG = wide ? static_cast<int>(blockDim.x) / D : 1;
+    const int grp = wide ? static_cast<int>(threadIdx.x) / D : 0;
+    const int jstep = wide ? D : static_cast<int>(blockDim.x);
     if (grp < NG) {
-        for (int j = blockDim.x >= static_cast<unsigned>(D) ? threadIdx.x % D : threadIdx.x; j < D; j += jstep) {
-            // cta_merge writes every cslot_o (0 for empty segments), so the loads are
-            // unconditional and independent: issue them in batches of 8
-            float acc = 0.f;
-            for (int i = grp; i < S; i += 8 * NG) {
-                float v[8];
+        for (int j = wide ? threadIdx.x % D : threadIdx.x; j < D; j += jstep) {
+            float mt = -CUDART_INF_F, lt = 0.f, at = 0.f;
+            for (int i0 = grp; i0 < S; i0 += 8 * NG) {
+                float mv[8], lv[8], ov[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int iu = i + u * NG;
-                    v[u] = iu < S ? __ldcg(a.cslot_o + (sm.cs[iu] * g + h) * D + j) : 0.f;
+                    const int i = i0 + u * NG;
+                    if (i < S) {
+                        const int64_t cs = (c_lo + i) * a.maxseg + (i == 0 ? seg_lo : 0);
+                        mv[u] = __ldcg(a.cslot_m + cs * g + h);
+                        lv[u] = __ldcg(a.cslot_l + cs * g + h);
+                        ov[u] = __ldcg(a.cslot_o + (cs * g + h) * D + j);
+                    } else {
+                        mv[u] = -CUDART_INF_F;
+                        lv[u] = ov[u] = 0.f;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int iu = i + u * NG;
-                    acc += (iu < S ? sm.e[iu] : 0.f) * v[u];
+                    if (mv[u] == -CUDART_INF_F) continue;
+                    if (mv[u] > mt) {
+                        const float sc = exp2f(mt - mv[u]);  // 0 when mt = -inf
+                        at *= sc;
+                        lt *= sc;
+                        mt = mv[u];
+                    }
+                    const float e = exp2f(mv[u] - mt);
+                    at += e * ov[u];
+                    lt += e * lv[u];
                 }
             }
-            sm.acc[grp * D + j] = acc;
+            sm.acc[grp * D + j] = at;
+            if (j == (wide ? 0 : static_cast<int>(threadIdx.x)) && (wide || threadIdx.x == 0)) {
+                sm.m[grp] = mt;
+                sm.l[grp] = lt;
+            }
         }
     }
     __syncthreads();
+    float M = -CUDART_INF_F;
+    for (int q = 0; q < NG; ++q) M = fmaxf(M, sm.m[q]);
+    float L = 0.f;
+    for (int q = 0; q < NG; ++q)
+        if (sm.m[q] != -CUDART_INF_F) L += exp2f(sm.m[q] - M) * sm.l[q];
     for (int jj = threadIdx.x; jj < D; jj += blockDim.x) {
         float O = 0.f;
-        for (int q = 0; q < NG; ++q) O += sm.acc[q * D + jj];
+        for (int q = 0; q < NG; ++q)
+            if (sm.m[q] != -CUDART_INF_F) O += exp2f(sm.m[q] - M) * sm.acc[q * D + jj];
         out_row[jj] = (M == -CUDART_INF_F) ? 0.f : O / L;
     }
     lse_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
@@ -843,96 +837,84 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
 }
 
 // =========================================================================
-// K2x: K2 fused with the one-shot NVLink exchange (kTailExchange). Each
-// block merges its rows, stores [lse | out] of them into slot `rank` of every
-// peer's exchange buffer (CUDA-IPC mapped HBM, plain stores over NVLink),
-// fence.sys, raises flag (rank, block) on every peer, waits for the p
-// sources' flags of its block and combines its rows: shift = max lse,
-// w = e^(lse - shift), out = sum w o / sum w -- allreduce(max),
-// partial_to_numerator, allreduce(sum) and n/d of decode.cpp:129-173 in one
-// exchange. Slots alternate by epoch parity (a rank cannot overwrite a slot a
-// peer still reads: it would first need the peer's next-step flag). The grid
-// never exceeds the co-resident capacity and every block pushes before it
-// waits, so the exchange cannot deadlock; the spin is bounded (~2 s).
+// K2x: K2 fused with the one-shot NVLink exchange (kTailExchange), LL
+// protocol: every 8-byte word of the exchange buffer is (value, epoch), so a
+// word's data and its readiness travel in one single-copy-atomic store over
+// NVLink -- no system fence, no separate flag. Each block merges its rows
+// (merge_row) and stores [out | lse] of them into slot `rank` of every peer's
+// buffer (CUDA-IPC mapped HBM); then it reads, word by word, the p sources of
+// its rows (spinning until a word carries this step's epoch) and combines:
+// shift = max lse, w = e^(lse - shift), out = sum w o / sum w -- the
+// allreduce(max), partial_to_numerator, allreduce(sum) and n/d of
+// decode.cpp:129-173 in one exchange. Slots alternate by epoch parity (a rank
+// cannot overwrite a slot a peer still reads: it would first need the peer's
+// next-step words). The grid never exceeds the co-resident capacity and every
+// block pushes before it reads, so the exchange cannot deadlock; each spin is
+// bounded (~2 s) and reports through x.error.
 // =========================================================================
+__device__ __forceinline__ void st_ll(uint2* p, float v, unsigned e) {
+    asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(e)
+                 : "memory");
+}
+__device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
+    unsigned v, f;
+    const long long t0 = clock64();
+    for (;;) {
+        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(f) : "l"(p) : "memory");
+        if (f == e) break;
+        if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
+            atomicExch(err, 1);
+            break;
+        }
+    }
+    return __uint_as_float(v);
+}
+
 __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     __shared__ K2Smem sm;
+    __shared__ float row[256];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const Xchg& x = a.tail.x;
     const int64_t rows = a.bh_count * a.group;
     const int D = a.d;
     const unsigned par = x.epoch & 1u;
-    const int64_t stride = x.max_rows * int64_t(D + 1);  // floats per (parity, source)
+    const int64_t stride = x.max_rows * int64_t(D + 1);  // words per (parity, source)
+    uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
     unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
     if (ts && threadIdx.x == 0) ts[0] = gtimer();
-    float* own = x.peers[x.rank] + (int64_t(par) * x.p + x.rank) * stride;
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // merge + push
         const int64_t orow = out_row_of(a, r);
         float l, m;
-        merge_row(a, r, sm, own + x.max_rows + orow * D, l, m);  // ends with a barrier
-        for (int q = 0; q < x.p; ++q) {
-            float* dst = q == x.rank ? own : x.peers[q] + (int64_t(par) * x.p + x.rank) * stride;
-            if (q != x.rank)
-                for (int j = threadIdx.x; j < D; j += blockDim.x)
-                    dst[x.max_rows + orow * D + j] = own[x.max_rows + orow * D + j];
-            if (threadIdx.x == 0) dst[orow] = l;
+        merge_row(a, r, sm, row, l, m);  // ends with a barrier
+        const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
+        for (int j = threadIdx.x; j <= D; j += blockDim.x) {
+            const float v = j < D ? row[j] : l;
+            for (int q = 0; q < x.p; ++q) st_ll(peers[q] + off + j, v, x.epoch);
         }
     }
-    if (x.variant == 4) __threadfence_system();  // every writer fences its own stores
-    __syncthreads();
     if (ts && threadIdx.x == 0) ts[1] = gtimer();
-    if (threadIdx.x == 0) {  // publish
-        if (x.variant != 4) __threadfence_system();
-        if (ts) ts[2] = gtimer();
-        for (int q = 0; q < x.p; ++q) {
-            unsigned* f = x.peer_flags[q] + (par * x.p + x.rank) * kXchgMaxBlocks + blockIdx.x;
-            if (x.variant == 1 || x.variant == 4)
-                asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(f), "r"(x.epoch) : "memory");
-            else if (x.variant == 2)
-                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(x.epoch) : "memory");
-            else
-                st_release_sys(f, x.epoch);
-        }
-    }
-    if (threadIdx.x < static_cast<unsigned>(x.p)) {  // wait for the p sources of this block
-        const unsigned* f = x.flags + (par * x.p + threadIdx.x) * kXchgMaxBlocks + blockIdx.x;
-        const long long t0 = clock64();
-        for (;;) {
-            unsigned v;
-            if (x.variant == 1 || x.variant == 4)
-                asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            else if (x.variant == 2)
-                asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            else
-                v = ld_acquire_sys(f);
-            if (v == x.epoch) break;
-            if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
-                atomicExch(x.error, 1);
-                break;
-            }
-            if (x.variant == 0) __nanosleep(32);
-        }
-        if (x.variant == 1 || x.variant == 2 || x.variant == 4) __threadfence_system();  // acquire side
-    }
-    __syncthreads();
-    if (ts && threadIdx.x == 0) ts[3] = gtimer();
+    const uint2* own = peers[x.rank];
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // exact combine of the p partials
         const int64_t orow = out_row_of(a, r);
-        float shift = -CUDART_INF_F;
-        for (int q = 0; q < x.p; ++q)
-            shift = fmaxf(shift, __ldcg(x.peers[x.rank] + (int64_t(par) * x.p + q) * stride + orow));
         for (int j = threadIdx.x; j < D; j += blockDim.x) {
+            float lq[8], shift = -CUDART_INF_F;
+            for (int q = 0; q < x.p; ++q) {
+                const float l = ld_ll(own + (int64_t(par) * x.p + q) * stride + orow * (D + 1) + D, x.epoch, x.error);
+                if (q < 8) lq[q] = l;
+                shift = fmaxf(shift, l);
+            }
             float num = 0.f, den = 0.f;
             for (int q = 0; q < x.p; ++q) {
-                const float* slot = x.peers[x.rank] + (int64_t(par) * x.p + q) * stride;
-                const float l = __ldcg(slot + orow);
+                const uint2* slot = own + (int64_t(par) * x.p + q) * stride + orow * (D + 1);
+                const float l = q < 8 ? lq[q] : ld_ll(slot + D, x.epoch, x.error);
                 const float w = l == -CUDART_INF_F ? 0.f : expf(l - shift);
                 den += w;
-                num += w * __ldcg(slot + x.max_rows + orow * D + j);
+                num += w * ld_ll(slot + j, x.epoch, x.error);
             }
             a.tail.out[orow * D + j] = num / den;
         }
     }
+    if (ts && threadIdx.x == 0) ts[3] = gtimer();
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
 }
 
@@ -1082,8 +1064,19 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
 
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes));
+    // the attribute is per kernel and per device; set it once (a driver call per
+    // launch would sit on the host side of every decode step)
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[{reinterpret_cast<const void*>(kernel), dev}];
+    if (cur >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(bytes));
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 }  // namespace
@@ -1302,7 +1295,6 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.x.epoch = xa.epoch;
     a.tail.x.max_rows = xa.max_rows;
     a.tail.x.error = xa.error;
-    a.tail.x.variant = xa.variant;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
     const int64_t rows = p.bh_count * p.group;
