@@ -828,6 +828,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
         const int64_t orow = out_row_of(a, r);
         float l, m;
         merge_row(a, r, sm, t.out + orow * a.d, l, m);
+        if (ts && threadIdx.x == 0 && r == blockIdx.x) ts[2] = gtimer();
         if (t.mode == kTailPartial && threadIdx.x == 0) {
             t.lse[orow] = l;
             t.row_max[orow] = m;
@@ -886,6 +887,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
         const int64_t orow = out_row_of(a, r);
         float l, m;
         merge_row(a, r, sm, row, l, m);  // ends with a barrier
+        if (ts && threadIdx.x == 0 && r == blockIdx.x) ts[2] = gtimer();
         const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
         for (int j = threadIdx.x; j <= D; j += blockDim.x) {
             const float v = j < D ? row[j] : l;

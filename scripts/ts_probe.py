@@ -51,10 +51,10 @@ def main():
         rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
         summary = {"k1_end": rel(st[1])}
         if ends:
-            q = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
-            summary["cta_start_q"] = [q(starts, f) for f in (0.0, 0.5, 1.0)]
-            summary["cta_end_q"] = [q(ends, f) for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
-        for k, name in enumerate(["k2_entry", "merged_pushed", "fenced_flagged", "peers_seen", "done"]):
+            qt = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
+            summary["cta_start_q"] = [qt(starts, f) for f in (0.0, 0.5, 1.0)]
+            summary["cta_end_q"] = [qt(ends, f) for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
+        for k, name in enumerate(["k2_entry", "pushed", "merged", "seen", "done"]):
             vals = [bl[k] for bl in blocks if bl[k]]
             if vals:
                 summary[name + "_min"] = rel(min(vals))

@@ -59,7 +59,7 @@ def main():
                 blocks = [st[8 + 8 * i: 8 + 8 * i + 5] for i in range(64) if st[8 + 8 * i]]
                 t0 = min(bl[0] for bl in blocks)
                 stamps.append([round((max(bl[k] for bl in blocks) - t0) / 1000.0, 2) for k in range(5)])
-            res["p2p_stage_max_us(entry,pushed,fenced,seen,done)"] = stamps[1:]
+            res["p2p_stage_max_us(entry,pushed,merged_row0,seen,done)"] = stamps[1:]
     print(json.dumps(res), flush=True)
     w.close()
     dist.barrier()
