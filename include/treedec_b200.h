@@ -56,7 +56,11 @@ enum {
     TD_TIME_PHASES = 8,  /* record CUDA events between the phases of the step   */
     TD_P2P = 16,         /* tree decode: one-shot NVLink exchange instead of the
                             two NCCL allreduces (needs td_p2p_open)              */
-    TD_DEBUG_TS = 32     /* kernels record %globaltimer stamps (td_debug_stamps) */
+    TD_DEBUG_TS = 32,    /* kernels record %globaltimer stamps (td_debug_stamps) */
+    TD_DETERMINISTIC = 64 /* static split only: bitwise-reproducible results (the
+                             default also hands the last ~15% of each (batch,
+                             kv-head) row out dynamically; results then agree to
+                             ~1e-7 between calls, the grouping of tiles varies) */
 };
 
 typedef struct td_context td_context;
@@ -74,6 +78,11 @@ const char* td_last_error(void);
  * directly). Replaces: seeded_random_tensor + slice_seq. */
 int td_seeded_fill(int dtype, void* dst, uint64_t seed, double scale, int64_t bh_count,
                    int64_t seq, int64_t start, int64_t len, int64_t d, void* stream);
+
+/* Process-wide TD_DETERMINISTIC for every call (including the stateless
+ * td_decode_partial): bitwise-reproducible results, the reference's
+ * determinism property (test_decode.cpp:185-202). */
+int td_set_deterministic(int on);
 
 /* Workspace bytes td_decode_partial needs for this shard shape. */
 int td_decode_workspace_bytes(int dtype, int64_t b, int64_t n_q, int64_t n_kv, int64_t t,

@@ -15,11 +15,11 @@ LIB_PATH = os.path.join(HERE, "libtreedec_b200.so")
 TD_OK, TD_EINVAL, TD_EDOMAIN, TD_ECUDA, TD_ENCCL, TD_ESTATE = range(6)
 TD_F64, TD_F32, TD_BF16 = 0, 1, 2
 TD_TREE_BINARY, TD_RING_ALLREDUCE, TD_HIERARCHICAL = 0, 1, 2
-TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT, TD_TIME_PHASES, TD_P2P, TD_DEBUG_TS = 1, 2, 4, 8, 16, 32
+TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT, TD_TIME_PHASES, TD_P2P, TD_DEBUG_TS, TD_DETERMINISTIC = 1, 2, 4, 8, 16, 32, 64
 
 # Every symbol include/treedec_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = [
-    "td_version", "td_last_error", "td_seeded_fill", "td_decode_workspace_bytes",
+    "td_version", "td_last_error", "td_seeded_fill", "td_set_deterministic", "td_decode_workspace_bytes",
     "td_decode_partial", "td_combine_partials", "td_partial_to_numerator", "td_combine_pair",
     "td_finalize", "td_create", "td_destroy", "td_stream", "td_comm_unique_id", "td_comm_init",
     "td_comm_info", "td_p2p_handle", "td_p2p_open", "td_p2p_status", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
     L.td_version.restype = ctypes.c_int
     L.td_last_error.restype = ctypes.c_char_p
     L.td_seeded_fill.argtypes = [ctypes.c_int, _vp, ctypes.c_uint64, ctypes.c_double, _i64, _i64, _i64, _i64, _i64, _vp]
+    L.td_set_deterministic.argtypes = [ctypes.c_int]
     L.td_decode_workspace_bytes.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_size_t)]
     L.td_decode_partial.argtypes = [ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_double,
                                     _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]

@@ -25,6 +25,7 @@ using td::SplitPlan;
 namespace {
 
 thread_local std::string g_err;
+int g_deterministic = 0;  // td_set_deterministic
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -180,6 +181,24 @@ struct td_context {
     bool x_ready = false;
 
     DevBuf dbg;  // TD_DEBUG_TS stamps
+
+    // calibrated static partition: per-CTA streaming speed of this GPU's SMs
+    // (blocks land on the same SMs launch after launch), measured once
+    std::vector<float> cal_w;
+    bool cal_failed = false;
+    DevBuf cal_q;
+    struct PartTab {
+        int64_t total = -1, per_bh = 0, bh = 0;
+        int ctas = 0, maxseg = 0;
+        DevBuf buf;  // int64 x[ctas + 1] then int bh[3 * bh_count]
+    };
+    PartTab tabs[4];
+    int tab_next = 0;
+
+    bool det = false;  // this call: static split only (TD_DETERMINISTIC)
+    DevBuf ctr;        // K1 dynamic-pool counters (SplitPlan::counters)
+    int64_t ctr_bh = -1;
+    int kpar = 0;      // parity of the next launch
 };
 
 namespace {
@@ -215,13 +234,147 @@ int ensure_rows(td_context* ctx, int64_t rows, int64_t d) {
     return TD_OK;
 }
 
+bool calibration_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TD_CALIBRATE");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+// Device tables of the speed-weighted static partition of `plan` (cached).
+int apply_partition(td_context* ctx, SplitPlan& plan) {
+    for (auto& tb : ctx->tabs)
+        if (tb.total == plan.total_tiles && tb.per_bh == plan.tiles_per_bh && tb.bh == plan.bh_count &&
+            tb.ctas == plan.ctas) {
+            plan.maxseg = std::max(plan.maxseg, tb.maxseg);
+            plan.x_table = static_cast<const int64_t*>(tb.buf.p);
+            plan.bh_table = reinterpret_cast<const int*>(static_cast<const int64_t*>(tb.buf.p) + plan.ctas + 1);
+            return TD_OK;
+        }
+    auto& tb = ctx->tabs[ctx->tab_next];
+    ctx->tab_next = (ctx->tab_next + 1) % 4;
+    std::vector<int64_t> x(size_t(plan.ctas) + 1);
+    std::vector<int> bh(3 * size_t(plan.bh_count));
+    td::build_partition(plan, ctx->cal_w.data(), x.data(), bh.data());
+    const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));  // the buffer may still be read by a launch
+    TD_CUDA(tb.buf.ensure(xb + bb));
+    TD_CUDA(cudaMemcpy(tb.buf.p, x.data(), xb, cudaMemcpyHostToDevice));
+    TD_CUDA(cudaMemcpy(static_cast<char*>(tb.buf.p) + xb, bh.data(), bb, cudaMemcpyHostToDevice));
+    tb.total = plan.total_tiles;
+    tb.per_bh = plan.tiles_per_bh;
+    tb.bh = plan.bh_count;
+    tb.ctas = plan.ctas;
+    tb.maxseg = plan.maxseg;
+    plan.x_table = static_cast<const int64_t*>(tb.buf.p);
+    plan.bh_table = reinterpret_cast<const int*>(static_cast<const int64_t*>(tb.buf.p) + plan.ctas + 1);
+    return TD_OK;
+}
+
+int ensure_rows(td_context* ctx, int64_t rows, int64_t d);
+
+// Measures how fast each CTA of the split kernel streams on this GPU (per-CTA
+// globaltimer stamps, static split, two rounds: equal ranges, then ranges
+// weighted by the first round's speeds) and keeps speed weights per block
+// index. Block b lands on the same SM in every launch of this grid, so the
+// weights carry over; they only move work, never change what is computed.
+int calibrate(td_context* ctx, int64_t n_q) {
+    SplitPlan p;
+    std::string msg;
+    if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), ctx->len,
+                        static_cast<int>(ctx->d), ctx->sm_count, p, msg, false) ||
+        p.kernel != 1 || !ctx->tm_ok)
+        return set_err(TD_EINVAL, "calibration not applicable");
+    const int G = p.ctas;
+    const int64_t rows = ctx->b * n_q;
+    if (int rc = ensure_rows(ctx, rows, ctx->d)) return rc;
+    TD_CUDA(ctx->cal_q.ensure(size_t(rows) * size_t(ctx->d) * 2));
+    TD_CUDA(cudaMemsetAsync(ctx->cal_q.p, 0, size_t(rows) * size_t(ctx->d) * 2, ctx->stream));
+    TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
+    std::vector<float> w(size_t(G), 1.f);
+    std::vector<unsigned long long> st(6144);
+    for (int round = 0; round < 2; ++round) {
+        SplitPlan pr = p;
+        std::vector<int64_t> x(size_t(G) + 1);
+        std::vector<int> bh(3 * size_t(pr.bh_count));
+        td::build_partition(pr, w.data(), x.data(), bh.data());
+        DevBuf tab;
+        const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
+        TD_CUDA(tab.ensure(xb + bb));
+        TD_CUDA(cudaMemcpy(tab.p, x.data(), xb, cudaMemcpyHostToDevice));
+        TD_CUDA(cudaMemcpy(static_cast<char*>(tab.p) + xb, bh.data(), bb, cudaMemcpyHostToDevice));
+        pr.x_table = static_cast<const int64_t*>(tab.p);
+        pr.bh_table = reinterpret_cast<const int*>(static_cast<const int64_t*>(tab.p) + G + 1);
+        TD_CUDA(ctx->ws.ensure(pr.workspace_bytes()));
+        std::vector<double> dur(size_t(G), 0.0);
+        cudaError_t e = cudaSuccess;
+        for (int rep = 0; rep < 3 && e == cudaSuccess; ++rep) {
+            e = cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream);
+            td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
+            if (e == cudaSuccess)
+                e = td::launch_decode_partial(pr, ctx->cal_q.p, ctx->k.p, ctx->v.p, 1.0f, &ctx->tmk, &ctx->tmv,
+                                              ctx->ws.p, ctx->r_max, ctx->r_lse, ctx->r_out, ctx->stream);
+            td::set_debug_stamps(nullptr);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(st.data(), ctx->dbg.p, st.size() * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+            if (rep == 0) continue;  // the first launch pays cold-start effects
+            for (int c = 0; c < G && c < 1024; ++c)
+                if (st[4097 + 2 * c] > st[4096 + 2 * c]) dur[size_t(c)] += double(st[4097 + 2 * c] - st[4096 + 2 * c]);
+        }
+        tab.release();
+        TD_CUDA(e);
+        double mean = 0.0;
+        int n = 0;
+        std::vector<double> speed(size_t(G), 0.0);
+        for (int c = 0; c < G; ++c) {
+            const int64_t tiles = x[size_t(c) + 1] - x[size_t(c)];
+            if (tiles > 0 && dur[size_t(c)] > 0) {
+                speed[size_t(c)] = double(tiles) / dur[size_t(c)];
+                mean += speed[size_t(c)];
+                ++n;
+            }
+        }
+        if (n == 0) return set_err(TD_ECUDA, "calibration: no stamps");
+        mean /= n;
+        for (int c = 0; c < G; ++c)
+            w[size_t(c)] = speed[size_t(c)] > 0 ? static_cast<float>(std::min(1.5, std::max(0.5, speed[size_t(c)] / mean)))
+                                                 : w[size_t(c)];
+    }
+    ctx->cal_w = w;
+    return TD_OK;
+}
+
 int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan) {
     std::string msg;
     if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
     if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), t,
-                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg))
+                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det))
         return set_err(TD_EINVAL, msg);
+    if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
+        if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
+            if (calibrate(ctx, n_q) != TD_OK) ctx->cal_failed = true;  // keep the equal split
+        }
+        if (ctx->cal_w.size() == size_t(plan.ctas))
+            if (int rc = apply_partition(ctx, plan)) return rc;
+    }
     TD_CUDA(ctx->ws.ensure(plan.workspace_bytes()));
+    if (plan.pool_tiles > 0) {
+        // pool counters: zero at rest except the last launch's parity; a new
+        // layout (bh_count) starts from a zeroed buffer
+        const size_t cap = ctx->ctr.cap;
+        TD_CUDA(ctx->ctr.ensure(plan.counters_bytes()));
+        if (ctx->ctr.cap != cap || ctx->ctr_bh != plan.bh_count) {
+            TD_CUDA(cudaMemsetAsync(ctx->ctr.p, 0, ctx->ctr.cap, ctx->stream));
+            ctx->ctr_bh = plan.bh_count;
+            ctx->kpar = 0;
+        }
+        plan.counters = static_cast<unsigned*>(ctx->ctr.p);
+        plan.parity = ctx->kpar;
+        ctx->kpar ^= 1;
+    }
     return TD_OK;
 }
 
@@ -345,9 +498,15 @@ int td_decode_workspace_bytes(int dtype, int64_t b, int64_t n_q, int64_t n_kv, i
     int dev = 0;
     cudaGetDevice(&dev);
     if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
-                        static_cast<int>(d), sm_count_of(dev), plan, msg))
+                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0))
         return set_err(TD_EINVAL, msg);
-    *bytes = plan.workspace_bytes();
+    // + the pool counters, carved from the end of the caller's workspace
+    *bytes = (plan.workspace_bytes() + 255) / 256 * 256 + plan.counters_bytes();
+    return TD_OK;
+}
+
+int td_set_deterministic(int on) {
+    g_deterministic = on != 0;
     return TD_OK;
 }
 
@@ -360,9 +519,10 @@ int td_decode_partial(int dtype, const void* q, const void* k, const void* v, in
     int dev = 0;
     cudaGetDevice(&dev);
     if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
-                        static_cast<int>(d), sm_count_of(dev), plan, msg))
+                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0))
         return set_err(TD_EINVAL, msg);
-    if (workspace_bytes < plan.workspace_bytes())
+    const size_t ctr_off = (plan.workspace_bytes() + 255) / 256 * 256;
+    if (workspace_bytes < ctr_off + plan.counters_bytes())
         return set_err(TD_EINVAL, "td_decode_partial: workspace too small");
     CUtensorMap mk, mv;
     if (plan.kernel == 1) {
@@ -370,6 +530,11 @@ int td_decode_partial(int dtype, const void* q, const void* k, const void* v, in
         if (!td::make_tensor_map(&mk, k, rows, static_cast<int>(d), plan.tile, msg) ||
             !td::make_tensor_map(&mv, v, rows, static_cast<int>(d), plan.tile, msg))
             return set_err(TD_ECUDA, msg);
+    }
+    if (plan.pool_tiles > 0) {  // stateless: counters zeroed on every call
+        plan.counters = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + ctr_off);
+        plan.parity = 0;
+        TD_CUDA(cudaMemsetAsync(plan.counters, 0, plan.counters_bytes(), static_cast<cudaStream_t>(stream)));
     }
     TD_CUDA(td::launch_decode_partial(plan, q, k, v, static_cast<float>(scale), &mk, &mv, workspace,
                                       row_max, lse, out, static_cast<cudaStream_t>(stream)));
@@ -458,6 +623,10 @@ int td_destroy(td_context* ctx) {
     ctx->xbuf.release();
     ctx->x_ptrs.release();
     ctx->x_err.release();
+    ctx->ctr.release();
+    ctx->dbg.release();
+    ctx->cal_q.release();
+    for (auto& tb : ctx->tabs) tb.buf.release();
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->xfer);
     delete ctx;
@@ -680,6 +849,7 @@ int td_debug_stamps(td_context* ctx, unsigned long long* out, int n) {
 int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
                    float* out, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
+    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
     if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "tree_decode: no KV shard placed");
     if (strategy < 0 || strategy > 2) return set_err(TD_EINVAL, "tree_decode: unknown strategy");
@@ -788,6 +958,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
 int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, float* row_max,
                      float* lse, float* out, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
+    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "local_partial: no KV shard placed");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "local_partial: q/kv head mismatch");
     ctx->last_kernels = 0;
@@ -816,6 +987,7 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
 int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
                    int flags) {
     if (int rc = require_ctx(ctx)) return rc;
+    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "ring_decode: no KV shard placed");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "ring_decode: more workers than keys");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "ring_decode: q/kv head mismatch");

@@ -21,17 +21,32 @@ inline int dtype_bytes(int dt) { return dt == kBF16 ? 2 : (dt == kF32 ? 4 : 8); 
 // range [c*total/ctas, (c+1)*total/ctas), so every SM gets the same number
 // of tiles (+-1) whatever b, n_kv and t are.
 struct SplitPlan {
+    // tiles_per_bh / total_tiles describe the STATIC tile space (the first
+    // tiles_per_bh tiles of every bh, bh-major); the remaining pool_tiles of
+    // each bh (from tile pool_first on) form the dynamic pool.
     int64_t bh_count = 0, t = 0, tiles_per_bh = 0, total_tiles = 0;
+    int64_t full_tiles_per_bh = 0, pool_first = 0, pool_tiles = 0;
+    int pool_chunk = 0, slot_warps = 0;
     int d = 0, n_q = 0, n_kv = 0, group = 0;
     int tile = 0, warps = 0, ctas = 0, maxseg = 0;
     int kernel = 0;  // 0 generic, 1 bf16 mma (TMA), 2 f32 (bulk)
     int dtype = kBF16;
-    int64_t slots() const { return int64_t(ctas) * warps * maxseg; }
+    // run-time state of a launch (set by the caller): pool counters
+    // [2 parities][bh_count] u32, zero at rest except the last launch's
+    // parity, and the parity of this launch (alternate between launches)
+    unsigned* counters = nullptr;
+    int parity = 0;
+    // calibrated static partition (device tables, optional; see
+    // build_partition): CTA c owns static tiles [x_table[c], x_table[c+1])
+    const int64_t* x_table = nullptr;
+    const int* bh_table = nullptr;
+    int64_t slots() const { return int64_t(ctas) * slot_warps * maxseg; }
     // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32),
     // then the per-CTA merged states [ctas * maxseg][group] (+ [..][d])
     size_t workspace_bytes() const {
         return sizeof(float) * (size_t(slots()) + size_t(ctas) * maxseg) * size_t(group) * size_t(2 + d);
     }
+    size_t counters_bytes() const { return sizeof(unsigned) * 2 * size_t(bh_count > 0 ? bh_count : 1); }
 };
 
 // TD_DEBUG_TS: kernels write %globaltimer stamps into buf (nullptr = off):
@@ -40,8 +55,15 @@ void set_debug_stamps(unsigned long long* buf);
 
 // Chooses the kernel and grid for a shard. Returns false (with msg) when the
 // shape is unsupported.
+// allow_pool = false gives a static split: bitwise-reproducible results.
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& plan, std::string& msg);
+                SplitPlan& plan, std::string& msg, bool allow_pool = true);
+
+// Static partition proportional to per-CTA speeds (weights[c] > 0, size
+// plan.ctas): x[c] = first static tile of CTA c (x has ctas + 1 entries),
+// bh[3 bh + {0, 1, 2}] = (first covering CTA, last covering CTA, segment of
+// bh in the first). Raises plan.maxseg when the uneven ranges need it.
+void build_partition(SplitPlan& plan, const float* weights, int64_t* x, int* bh);
 
 // K1 (+ merge tail): attention_chunk_partial of q against one shard, written as fp32
 // (row_max, lse, out) rows [b][n_q] / [b][n_q][d]. tmk/tmv are the shard's

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -69,6 +70,21 @@ struct K1Args {
     float* cslot_l;
     float* cslot_o; // [ctas * maxseg][group][d]
     unsigned long long* dbg;  // optional globaltimer stamps (TD_DEBUG_TS)
+    int reverse;              // debug: CTA c takes range ctas-1-c (TD_DEBUG_REVERSE)
+    // dynamic "home" pool (k1_bf16): tiles [pool_first, pool_first + pool_tiles)
+    // of every bh are handed out at run time in chunks of pool_chunk tiles to
+    // the CTAs whose static range covers that bh; a warp folds them into its
+    // own slot (phase 1) of that segment, so K2 merges the same states.
+    int64_t pool_first, pool_tiles;
+    int pool_chunk;
+    int slot_warps;           // state slots per CTA and segment (warps * 2 with a pool)
+    unsigned* pool_ctr;       // [bh_count] chunks taken (this launch's parity)
+    unsigned* pool_next;      // [bh_count] the other parity's counters (zeroed by K2)
+    // calibrated static partition (optional): CTA c owns static tiles
+    // [x_table[c], x_table[c+1]); bh_table[3 bh + {0,1,2}] = the first and last
+    // CTA covering bh and bh's segment index in the first one
+    const int64_t* x_table;
+    const int* bh_table;
     Tail tail;
 };
 
@@ -79,8 +95,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 
+// n / d for non-negative operands; 32-bit division (a short sequence) when both
+// fit, the 64-bit software division (~100 dependent instructions) otherwise.
+__device__ __forceinline__ int64_t div_nn(int64_t n, int64_t d) {
+    if (((n | d) >> 32) == 0) return static_cast<int64_t>(static_cast<uint32_t>(n) / static_cast<uint32_t>(d));
+    return n / d;
+}
+
 __device__ __forceinline__ int64_t cta_begin(int64_t total, int c, int ctas) {
-    return total * c / ctas;
+    return div_nn(total * c, ctas);
 }
 
 // End of K1: merges the W warp states of each of CTA c's segments into one
@@ -110,7 +133,7 @@ __device__ void cta_merge(const K1Args& a, int c, float* sm) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const float m = sm_m[w * nsh + i];
-            const float e = (m == -CUDART_INF_F) ? 0.f : exp2f(m - M);
+            const float e = (m == -CUDART_INF_F) ? 0.f : fast_exp2(m - M);
             sm_e[w * nsh + i] = e;
             L += e * sm_l[w * nsh + i];
         }
@@ -153,6 +176,8 @@ __global__ void __launch_bounds__(W * 32, 1)
 
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[W][S];
+    __shared__ int64_t st_bh[W][S], st_tb[W][S];  // tile of each stage (bh, tile-in-bh)
+    __shared__ int st_rec[W][S];                   // -1: static tile, else pool record
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
     const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
@@ -160,12 +185,11 @@ __global__ void __launch_bounds__(W * 32, 1)
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x;
-    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
-    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
-    const int64_t span = x1 - x0;
-    const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
-    const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
+    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int64_t A = a.tiles_per_bh;  // static tiles per bh (the pool holds the rest)
+    const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int64_t bh_first = x0 / (A > 0 ? A : 1);
     uint8_t* wsm = smem + size_t(warp) * S * STAGE_BYTES;
 
     if (lane == 0) {
@@ -179,11 +203,56 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncwarp();
     const uint64_t pol = policy_evict_first();
 
-    auto issue = [&](int64_t kk, int s) {
-        const int64_t x = x0 + warp + kk * W;
-        const int64_t bh = x / a.tiles_per_bh;
-        const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
-        const int row = static_cast<int>(bh * a.t + tok0);
+    // ---- tile stream (warp-uniform): this CTA's static tiles x0 + warp + kW,
+    // then chunks of the pools of the bhs its range covers (dynamic: CTAs on
+    // SMs that stream faster take more of them). rec = slot phase (0 static,
+    // 1 pool), so pool tiles land in this CTA's own segment slots.
+    int64_t s_next = x0 + warp;
+    const int64_t nch = a.pool_tiles > 0 ? (a.pool_tiles + a.pool_chunk - 1) / a.pool_chunk : 0;
+    const int64_t cb_lo = x1 > x0 ? x0 / A : 0, cb_hi = x1 > x0 ? (x1 - 1) / A : -1;
+    const int64_t ncb = cb_hi - cb_lo + 1;
+    const int64_t last_static = x1 > x0 + warp ? x0 + warp + ((x1 - 1 - x0 - warp) / W) * W : -1;
+    const int64_t cb_start = last_static >= 0 ? last_static / A : cb_hi;  // stay on the current bh first
+    int64_t p_bh = -1, p_pos = 0, p_end = 0, p_tries = 0;
+    bool p_done = nch == 0 || ncb <= 0;
+    auto next_tile = [&](int64_t& bh, int64_t& tb, int& rec) -> bool {
+        if (s_next < x1) {
+            bh = s_next / A;
+            tb = s_next - bh * A;
+            rec = 0;
+            s_next += W;
+            return true;
+        }
+        while (!p_done) {
+            if (p_pos < p_end) {
+                bh = p_bh;
+                tb = p_pos++;
+                rec = 1;
+                return true;
+            }
+            if (p_bh >= 0) {  // next chunk of the bh being helped
+                unsigned k = 0;
+                if (lane == 0) k = atomicAdd(a.pool_ctr + p_bh, 1u);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k < nch) {
+                    p_pos = a.pool_first + int64_t(k) * a.pool_chunk;
+                    p_end = min(p_pos + a.pool_chunk, a.pool_first + a.pool_tiles);
+                    continue;
+                }
+                p_bh = -1;  // exhausted
+            }
+            if (p_tries == ncb) {
+                p_done = true;
+                break;
+            }
+            p_bh = cb_lo + (cb_start - cb_lo + p_tries) % ncb;
+            ++p_tries;
+        }
+        return false;
+    };
+    auto issue = [&](int s, int64_t bh, int64_t tb) {
+        if (lane != 0) return;
+        const int row = static_cast<int>(bh * a.t + tb * T);
         uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
         uint8_t* vd = kd + TILE_BYTES;
         mbar_expect_tx(&bars[warp][s], STAGE_BYTES);
@@ -193,8 +262,22 @@ __global__ void __launch_bounds__(W * 32, 1)
             tma_load_2d(vd + bx * BOX_BYTES, &tmv, &bars[warp][s], bx * 64, row, pol);
         }
     };
-    if (lane == 0)
-        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
+    auto refill = [&](int s) {
+        int64_t bh, tb;
+        int rec;
+        if (next_tile(bh, tb, rec)) {
+            if (lane == 0) {
+                st_bh[warp][s] = bh;
+                st_tb[warp][s] = tb;
+                st_rec[warp][s] = rec;
+            }
+            issue(s, bh, tb);
+        } else if (lane == 0) {
+            st_bh[warp][s] = -1;
+        }
+        __syncwarp();
+    };
+    for (int s = 0; s < S; ++s) refill(s);
 
     const int hA = 2 * (lane & 3), hB = hA + 1;  // this lane's heads (N columns)
     const int eta = lane >> 2;                   // B-fragment head / C-fragment row
@@ -206,7 +289,8 @@ __global__ void __launch_bounds__(W * 32, 1)
     float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
     uint32_t qf[KS][2];
     int64_t cur_bh = -1;
-    uint32_t flushed = 0;
+    int cur_rec = -1;
+    uint64_t flushed = 0;
 
     auto load_q = [&](int64_t bh) {
         const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
@@ -226,7 +310,8 @@ __global__ void __launch_bounds__(W * 32, 1)
         m0 = m1 = -CUDART_INF_F;
         l0 = l1 = 0.f;
     };
-    auto flush = [&](int seg) {
+    // state -> this warp's slot (c, warp, phase, seg); phase 1 holds pool tiles
+    auto flush = [&](int64_t bh, int rec) {
         float la = l0, lb = l1;
         la += __shfl_xor_sync(0xffffffffu, la, 4);
         la += __shfl_xor_sync(0xffffffffu, la, 8);
@@ -234,10 +319,13 @@ __global__ void __launch_bounds__(W * 32, 1)
         lb += __shfl_xor_sync(0xffffffffu, lb, 4);
         lb += __shfl_xor_sync(0xffffffffu, lb, 8);
         lb += __shfl_xor_sync(0xffffffffu, lb, 16);
-        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
+        const int seg = static_cast<int>(bh - bh_first);
+        const int sub = a.slot_warps == W ? warp : 2 * warp + rec;
+        const int64_t slot = (int64_t(c) * a.slot_warps + sub) * a.maxseg + seg;
         float* sm = a.slot_m + slot * a.group;
         float* sl = a.slot_l + slot * a.group;
         float* so = a.slot_o + slot * a.group * int64_t(D);
+        flushed |= 1ull << (2 * seg + rec);
         if (lane < 4) {
             if (hA < a.group) { sm[hA] = m0; sl[hA] = la; }
             if (hB < a.group) { sm[hB] = m1; sl[hB] = lb; }
@@ -254,23 +342,24 @@ __global__ void __launch_bounds__(W * 32, 1)
                 so[hB * D + d0 + 8] = o[md][3];
             }
         }
-        flushed |= 1u << seg;
     };
 
     reset();
-    for (int64_t kk = 0; kk < nmine; ++kk) {
+    for (int64_t kk = 0;; ++kk) {
         const int s = static_cast<int>(kk % S);
         const uint32_t phase = static_cast<uint32_t>((kk / S) & 1);
-        const int64_t x = x0 + warp + kk * W;
-        const int64_t bh = x / a.tiles_per_bh;
-        const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
-        if (bh != cur_bh) {
+        const int64_t bh = st_bh[warp][s];
+        if (bh < 0) break;  // stream exhausted (tiles are consumed in issue order)
+        const int64_t tok0 = st_tb[warp][s] * T;
+        const int rec = st_rec[warp][s];
+        if (bh != cur_bh || rec != cur_rec) {
             if (cur_bh >= 0) {
-                flush(static_cast<int>(cur_bh - bh_first));
+                flush(cur_bh, cur_rec);
                 reset();
             }
+            if (bh != cur_bh) load_q(bh);
             cur_bh = bh;
-            load_q(bh);
+            cur_rec = rec;
         }
         const int64_t rem = a.t - tok0;
         const int nvalid = rem < T ? static_cast<int>(rem) : T;
@@ -373,27 +462,34 @@ __global__ void __launch_bounds__(W * 32, 1)
             }
         }
         __syncwarp();
-        if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+        refill(s);
     }
-    if (cur_bh >= 0) flush(static_cast<int>(cur_bh - bh_first));
-    // untouched segments are empty partials (m = -inf)
-    for (int seg = 0; seg < a.maxseg; ++seg) {
-        if (flushed & (1u << seg)) continue;
-        const int64_t slot = (int64_t(c) * W + warp) * a.maxseg + seg;
-        for (int h = lane; h < a.group; h += 32) {
-            a.slot_m[slot * a.group + h] = -CUDART_INF_F;
-            a.slot_l[slot * a.group + h] = 0.f;
+    if (cur_bh >= 0) flush(cur_bh, cur_rec);
+    // untouched slots are empty partials (m = -inf)
+    const int phases = a.slot_warps == W ? 1 : 2;
+    for (int seg = 0; seg < a.maxseg; ++seg)
+        for (int ph = 0; ph < phases; ++ph) {
+            if (flushed & (1ull << (2 * seg + ph))) continue;
+            const int sub = phases == 1 ? warp : 2 * warp + ph;
+            const int64_t slot = (int64_t(c) * a.slot_warps + sub) * a.maxseg + seg;
+            for (int h = lane; h < a.group; h += 32) {
+                a.slot_m[slot * a.group + h] = -CUDART_INF_F;
+                a.slot_l[slot * a.group + h] = 0.f;
+            }
         }
-    }
     __syncthreads();
-    cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    if (phases == 2) cta_merge<2 * W>(a, c, reinterpret_cast<float*>(smem));
+    else cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
     if (a.dbg && threadIdx.x == 0) {
         const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
         atomicMax(a.dbg + 1, t_end);
-        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c]
+        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c], SM id at dbg[2048 + c]
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             a.dbg[4096 + 2 * c] = t_start;
             a.dbg[4096 + 2 * c + 1] = t_end;
+            a.dbg[2048 + c] = smid;
         }
     }
 }
@@ -418,9 +514,9 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x;
-    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
-    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
     const int64_t span = x1 - x0;
     const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
     const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
@@ -578,9 +674,12 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
         atomicMax(a.dbg + 1, t_end);
-        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c]
+        if (c < 1024) {  // per-CTA [start, end] at dbg[4096 + 2c], SM id at dbg[2048 + c]
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             a.dbg[4096 + 2 * c] = t_start;
             a.dbg[4096 + 2 * c + 1] = t_end;
+            a.dbg[2048 + c] = smid;
         }
     }
 }
@@ -607,9 +706,9 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x;
-    const int64_t x0 = cta_begin(a.total_tiles, c, a.ctas);
-    const int64_t x1 = cta_begin(a.total_tiles, c + 1, a.ctas);
+    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
+    const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
     const int64_t span = x1 - x0;
     const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
     const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
@@ -723,13 +822,18 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
     const int h = static_cast<int>(r % a.group);
     const int D = a.d, g = a.group;
     int64_t c_lo = 0, c_hi = -1, seg_lo = 0;
-    if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
+    if (a.bh_table) {
+        c_lo = __ldg(a.bh_table + 3 * bh);
+        c_hi = __ldg(a.bh_table + 3 * bh + 1);
+        seg_lo = __ldg(a.bh_table + 3 * bh + 2);
+    } else if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
         const int64_t X = bh * a.tiles_per_bh, Xe = X + a.tiles_per_bh - 1;
-        c_lo = ((X + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
-        c_hi = ((Xe + 1) * a.ctas + a.total_tiles - 1) / a.total_tiles - 1;
-        seg_lo = bh - cta_begin(a.total_tiles, static_cast<int>(c_lo), a.ctas) / a.tiles_per_bh;
+        c_lo = div_nn((X + 1) * a.ctas + a.total_tiles - 1, a.total_tiles) - 1;
+        c_hi = div_nn((Xe + 1) * a.ctas + a.total_tiles - 1, a.total_tiles) - 1;
+        seg_lo = bh - div_nn(cta_begin(a.total_tiles, static_cast<int>(c_lo), a.ctas), a.tiles_per_bh);
     }
     const int S = static_cast<int>(c_hi - c_lo + 1);
+    const int SP = S;
     const bool wide = blockDim.x >= static_cast<unsigned>(D);
     const int NG = wide ? static_cast<int>(blockDim.x) / D : 1;
     const int grp = wide ? static_cast<int>(threadIdx.x) / D : 0;
@@ -737,12 +841,12 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
     if (grp < NG) {
         for (int j = wide ? threadIdx.x % D : threadIdx.x; j < D; j += jstep) {
             float mt = -CUDART_INF_F, lt = 0.f, at = 0.f;
-            for (int i0 = grp; i0 < S; i0 += 8 * NG) {
+            for (int i0 = grp; i0 < SP; i0 += 8 * NG) {
                 float mv[8], lv[8], ov[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int i = i0 + u * NG;
-                    if (i < S) {
+                    if (i < S) {  // static CTA state
                         const int64_t cs = (c_lo + i) * a.maxseg + (i == 0 ? seg_lo : 0);
                         mv[u] = __ldcg(a.cslot_m + cs * g + h);
                         lv[u] = __ldcg(a.cslot_l + cs * g + h);
@@ -756,12 +860,12 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
                 for (int u = 0; u < 8; ++u) {
                     if (mv[u] == -CUDART_INF_F) continue;
                     if (mv[u] > mt) {
-                        const float sc = exp2f(mt - mv[u]);  // 0 when mt = -inf
+                        const float sc = fast_exp2(mt - mv[u]);  // 0 when mt = -inf
                         at *= sc;
                         lt *= sc;
                         mt = mv[u];
                     }
-                    const float e = exp2f(mv[u] - mt);
+                    const float e = fast_exp2(mv[u] - mt);
                     at += e * ov[u];
                     lt += e * lv[u];
                 }
@@ -778,11 +882,11 @@ __device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row
     for (int q = 0; q < NG; ++q) M = fmaxf(M, sm.m[q]);
     float L = 0.f;
     for (int q = 0; q < NG; ++q)
-        if (sm.m[q] != -CUDART_INF_F) L += exp2f(sm.m[q] - M) * sm.l[q];
+        if (sm.m[q] != -CUDART_INF_F) L += fast_exp2(sm.m[q] - M) * sm.l[q];
     for (int jj = threadIdx.x; jj < D; jj += blockDim.x) {
         float O = 0.f;
         for (int q = 0; q < NG; ++q)
-            if (sm.m[q] != -CUDART_INF_F) O += exp2f(sm.m[q] - M) * sm.acc[q * D + jj];
+            if (sm.m[q] != -CUDART_INF_F) O += fast_exp2(sm.m[q] - M) * sm.acc[q * D + jj];
         out_row[jj] = (M == -CUDART_INF_F) ? 0.f : O / L;
     }
     lse_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
@@ -820,6 +924,11 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     __shared__ K2Smem sm;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the other parity's pool counters are the next launch's: zero them
+    if (a.pool_tiles > 0)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
+             i += int64_t(gridDim.x) * blockDim.x)
+            a.pool_next[i] = 0u;
     unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
     if (ts && threadIdx.x == 0) ts[0] = gtimer();
     const Tail& t = a.tail;
@@ -875,6 +984,11 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     __shared__ K2Smem sm;
     __shared__ float row[256];
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the other parity's pool counters are the next launch's: zero them
+    if (a.pool_tiles > 0)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
+             i += int64_t(gridDim.x) * blockDim.x)
+            a.pool_next[i] = 0u;
     const Xchg& x = a.tail.x;
     const int64_t rows = a.bh_count * a.group;
     const int D = a.d;
@@ -1037,6 +1151,8 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
                  void* ws) {
     K1Args a{};
     a.dbg = g_dbg;
+    static const int rev = [] { const char* e = std::getenv("TD_DEBUG_REVERSE"); return e ? std::atoi(e) : 0; }();
+    a.reverse = rev;
     a.q = q;
     a.k = k;
     a.v = v;
@@ -1061,6 +1177,17 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.cslot_m = cf;
     a.cslot_l = cf + nc;
     a.cslot_o = cf + 2 * nc;
+    a.pool_first = p.pool_first;
+    a.pool_tiles = p.pool_tiles;
+    a.pool_chunk = p.pool_chunk;
+    a.slot_warps = p.slot_warps;
+    a.x_table = p.x_table;
+    a.bh_table = p.bh_table;
+    if (p.pool_tiles > 0) {
+        unsigned* cnt = p.counters;  // [2 parities][bh_count]
+        a.pool_ctr = cnt + p.parity * p.bh_count;
+        a.pool_next = cnt + (1 - p.parity) * p.bh_count;
+    }
     return a;
 }
 
@@ -1086,7 +1213,7 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 void set_debug_stamps(unsigned long long* buf) { g_dbg = buf; }
 
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& p, std::string& msg) {
+                SplitPlan& p, std::string& msg, bool allow_pool) {
     if (b < 1 || n_q < 1 || n_kv < 1 || d < 1 || t < 0) {
         msg = "decode: dimensions must be positive";
         return false;
@@ -1127,13 +1254,32 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
         p.tile = kGenTile;
         p.warps = kGenWarps;
     }
-    p.tiles_per_bh = (t + p.tile - 1) / p.tile;
+    p.full_tiles_per_bh = (t + p.tile - 1) / p.tile;
+    // Dynamic pool (bf16 kernel): the last pool_frac of every bh's tiles are
+    // handed out at run time, so SMs that stream slower (their share of HBM
+    // bandwidth differs by up to ~20%) do less of them.
+    static const double pool_frac = [] {
+        const char* e = std::getenv("TD_POOL_FRAC");
+        return e ? std::atof(e) : 0.15;
+    }();
+    static const int pool_chunk = [] {
+        const char* e = std::getenv("TD_POOL_CHUNK");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    int64_t pool = 0;
+    if (allow_pool && p.kernel == 1 && p.full_tiles_per_bh >= 16 && pool_frac > 0.0)
+        pool = std::min<int64_t>(p.full_tiles_per_bh / 2, static_cast<int64_t>(p.full_tiles_per_bh * pool_frac));
+    p.pool_tiles = pool;
+    p.pool_first = p.full_tiles_per_bh - pool;
+    p.pool_chunk = pool_chunk;
+    p.tiles_per_bh = p.full_tiles_per_bh - pool;
     p.total_tiles = p.bh_count * p.tiles_per_bh;
-    // one CTA per SM (the per-warp pipelines fill shared memory); never more
-    // CTAs than tiles.
+    // one CTA per SM (the per-warp pipelines fill shared memory); without a
+    // pool never more CTAs than tiles.
     int64_t ctas = sm_count;
-    if (p.total_tiles < ctas) ctas = p.total_tiles > 0 ? p.total_tiles : 1;
+    if (pool == 0 && p.total_tiles < ctas) ctas = p.total_tiles > 0 ? p.total_tiles : 1;
     p.ctas = static_cast<int>(ctas);
+    p.slot_warps = p.warps * (pool > 0 ? 2 : 1);
     const int64_t per_cta = (p.total_tiles + p.ctas - 1) / p.ctas;
     const int64_t tpb = p.tiles_per_bh > 0 ? p.tiles_per_bh : 1;
     p.maxseg = static_cast<int>((per_cta + tpb - 1) / tpb + 1);
@@ -1142,6 +1288,33 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
         return false;
     }
     return true;
+}
+
+void build_partition(SplitPlan& p, const float* w, int64_t* x, int* bh) {
+    const int G = p.ctas;
+    const int64_t T = p.total_tiles, A = p.tiles_per_bh > 0 ? p.tiles_per_bh : 1;
+    double tot = 0.0;
+    for (int c = 0; c < G; ++c) tot += w[c] > 0.f ? w[c] : 0.f;
+    double acc = 0.0;
+    x[0] = 0;
+    for (int c = 0; c < G; ++c) {
+        acc += w[c] > 0.f ? w[c] : 0.f;
+        int64_t e = c + 1 == G ? T : static_cast<int64_t>(std::llround(double(T) * acc / (tot > 0 ? tot : 1.0)));
+        x[c + 1] = std::min(T, std::max(x[c], e));
+    }
+    int maxseg = 1;
+    for (int c = 0; c < G; ++c)
+        if (x[c + 1] > x[c]) maxseg = std::max<int>(maxseg, static_cast<int>((x[c + 1] - 1) / A - x[c] / A + 1));
+    for (int64_t b = 0; b < p.bh_count; ++b) {
+        const int64_t X = b * A, Xe = X + A - 1;
+        // the CTA c with x[c] <= X < x[c + 1] (never an empty range)
+        const int lo = static_cast<int>(std::upper_bound(x, x + G + 1, X) - x) - 1;
+        const int hi = static_cast<int>(std::upper_bound(x, x + G + 1, Xe) - x) - 1;
+        bh[3 * b] = lo;
+        bh[3 * b + 1] = hi;
+        bh[3 * b + 2] = static_cast<int>(b - x[lo] / A);
+    }
+    p.maxseg = std::max(p.maxseg, maxseg);
 }
 
 bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,

@@ -59,6 +59,9 @@ def main():
             if vals:
                 summary[name + "_min"] = rel(min(vals))
                 summary[name + "_max"] = rel(max(vals))
+        if os.environ.get("TS_DUMP_CTAS"):
+            summary["ctas"] = [(c, st[2048 + c], round((st[4097 + 2 * c] - t0) / 1000.0, 2))
+                               for c in range(1024) if st[4097 + 2 * c]]
         res.append(summary)
     print(json.dumps({"rank": local, "world": world, "combine": args.combine, "steps": res[1:]}), flush=True)
     w.close()

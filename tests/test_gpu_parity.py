@@ -217,13 +217,28 @@ def test_tree_decode_validation(td, oracle):
 
 
 def test_decode_is_deterministic(td, oracle):
+    """test_decode.cpp:185-202: bitwise-identical results in deterministic mode;
+    the default (dynamic tail) mode agrees to ~1e-7."""
     import torch
-    q, k, v = make_inputs(oracle, 9, 1, 32, 8, 40000, 128, BF16)
+    q, k, v = make_inputs(oracle, 9, 1, 32, 8, 400000, 128, BF16)
     qd, kd, vd = dev(q, BF16), dev(k, BF16), dev(v, BF16)
     cache = td.shard_kv(kd, vd, 8)
-    a = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
-    b = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
-    assert torch.equal(a, b)
+    try:
+        td.set_deterministic(True)
+        a = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+        b = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+        assert torch.equal(a, b)
+        w = td.Worker(0)
+        w.place_kv(kd, vd)
+        x = w.tree_decode(qd)
+        y = w.tree_decode(qd)
+        assert torch.equal(x, y)
+    finally:
+        td.set_deterministic(False)
+    c = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+    z = w.tree_decode(qd)
+    w.close()
+    assert rel_err(host(c), host(a)) <= 1e-6 and rel_err(host(z), host(x)) <= 1e-6
 
 
 # ---------------------------------------------------------------- the Worker (C-ABI context) path
@@ -245,7 +260,7 @@ def test_worker_generate_and_decode(td, oracle, dtype, n_q, n_kv, n):
     assert rel_err(host(out[:, :g]), want) <= TOL[dtype]
     # host buffers through the same call (the e2e path)
     out_h = w.tree_decode(torch.from_numpy(np.ascontiguousarray(q)).to(dev(q, dtype).dtype))
-    assert torch.equal(out_h, out.cpu())
+    assert rel_err(out_h.double().numpy(), host(out)) <= 1e-6  # default mode: ~1e-7 between calls
     kernels, kv_bytes, split = w.last_launch_stats()
     assert kernels >= 2 and kv_bytes == 2 * n_kv * n * 128 * (2 if dtype == BF16 else 4)
     w.close()
@@ -259,8 +274,13 @@ def test_worker_place_matches_generate(td, oracle):
     a = w.tree_decode(dev(q, BF16))
     w.place_kv(torch.from_numpy(k).to(torch.bfloat16), torch.from_numpy(v).to(torch.bfloat16))  # from host
     b = w.tree_decode(dev(q, BF16))
-    assert torch.equal(a, b)
+    assert rel_err(host(a), host(b)) <= 1e-6
     assert rel_err(host(a), oracle.tree_decode(q, k, v, 1, HIER, 1.0, F64)) <= 1e-3
     r = w.ring_decode(dev(q, BF16))  # p = 1: ring is the local partial
-    assert torch.equal(r, a)
+    assert rel_err(host(r), host(a)) <= 1e-6
+    # deterministic mode: bitwise-identical repeated calls through every entry point
+    x = w.tree_decode(dev(q, BF16), flags=td._capi.TD_DETERMINISTIC)
+    y = w.tree_decode(dev(q, BF16), flags=td._capi.TD_DETERMINISTIC)
+    z = w.ring_decode(dev(q, BF16), flags=td._capi.TD_DETERMINISTIC)
+    assert torch.equal(x, y) and torch.equal(x, z)
     w.close()
