@@ -155,6 +155,18 @@ int td_kv_place(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq
 int td_kv_generate(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t seq_len,
                    int64_t d, uint64_t seed_k, uint64_t seed_v, double scale);
 
+/* KV append, the caller side of tree_decode in a generation loop (SURVEY.md
+ * section 8(f)2): the cache grows by one token that lands at the end of the
+ * last shard (rank p-1). Every rank calls it (seq_len += 1 everywhere); only
+ * rank p-1 reads k/v, one [b, n_kv, 1, d] token in the cache dtype (host or
+ * device). Capacity grows geometrically (or to td_kv_reserve's size), so a
+ * step costs two strided copies of b*n_kv*d elements. tree_decode is exact
+ * under any partition (safe-softmax invariance), so the result equals the
+ * reference's decode over the grown cache. */
+int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host);
+/* Reserves room for `tokens` more appended tokens on rank p-1 (no-op elsewhere). */
+int td_kv_reserve(td_context* ctx, int64_t tokens);
+
 /* Shard geometry of the placed cache. */
 int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes);
 /* Device pointers of the placed shard (for tests). */

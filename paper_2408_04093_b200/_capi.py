@@ -23,6 +23,7 @@ EXPORTS = [
     "td_decode_partial", "td_combine_partials", "td_partial_to_numerator", "td_combine_pair",
     "td_finalize", "td_create", "td_destroy", "td_stream", "td_comm_unique_id", "td_comm_init",
     "td_comm_info", "td_p2p_handle", "td_p2p_open", "td_p2p_status", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
+    "td_kv_append", "td_kv_reserve",
     "td_tree_decode", "td_ring_decode", "td_local_partial", "td_output_bf16", "td_kernel_time",
     "td_reset_kernel_timer", "td_phase_times", "td_debug_stamps", "td_last_launch_stats", "td_memory_bytes",
 ]
@@ -88,6 +89,8 @@ def lib() -> ctypes.CDLL:
                                  ctypes.c_double]
     L.td_kv_info.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t)]
     L.td_kv_pointers.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+    L.td_kv_append.argtypes = [_vp, _vp, _vp, ctypes.c_int]
+    L.td_kv_reserve.argtypes = [_vp, _i64]
     L.td_tree_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_int, _vp, ctypes.c_int]
     L.td_ring_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, ctypes.c_int]
     L.td_local_partial.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, ctypes.c_int]

@@ -146,6 +146,8 @@ struct td_context {
     bool kv_ok = false;
     int dtype = td::kBF16;
     int64_t b = 0, n_kv = 0, seq_len = 0, d = 0, start = 0, len = 0;
+    int64_t cap = 0;  // tokens per bh row allocated (>= len: room for td_kv_append)
+    std::vector<int64_t> lens;  // every rank's shard length (chunk_extents, then appends on rank p-1)
     DevBuf k, v;
     CUtensorMap tmk{}, tmv{};
     bool tm_ok = false;
@@ -156,6 +158,7 @@ struct td_context {
           *nd = nullptr, *out = nullptr, *r_max = nullptr, *r_lse = nullptr, *r_out = nullptr;
     DevBuf q_dev, out_bf16;
     DevBuf ring[2][2];                           // [buffer][k|v]
+    DevBuf ring_own[2];                          // own shard packed contiguously (cap > len)
     std::vector<cudaEvent_t> ring_ev;            // compute-done / recv-done
 
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
@@ -286,6 +289,7 @@ int calibrate(td_context* ctx, int64_t n_q) {
                         static_cast<int>(ctx->d), ctx->sm_count, p, msg, false) ||
         p.kernel != 1 || !ctx->tm_ok)
         return set_err(TD_EINVAL, "calibration not applicable");
+    p.row_stride = ctx->cap;
     const int G = p.ctas;
     const int64_t rows = ctx->b * n_q;
     if (int rc = ensure_rows(ctx, rows, ctx->d)) return rc;
@@ -347,12 +351,15 @@ int calibrate(td_context* ctx, int64_t n_q) {
     return TD_OK;
 }
 
-int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan) {
+// stride: tokens per bh row in memory (the placed shard's capacity; 0 for a
+// contiguous [bh][t][d] buffer such as a ring chunk)
+int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t stride) {
     std::string msg;
     if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
     if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), t,
                         static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det))
         return set_err(TD_EINVAL, msg);
+    plan.row_stride = stride;
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
         if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
             if (calibrate(ctx, n_q) != TD_OK) ctx->cal_failed = true;  // keep the equal split
@@ -661,6 +668,7 @@ int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[1
     }
     ctx->nranks = nranks;
     ctx->rank = rank;
+    if (ctx->kv_ok) ctx->lens = chunk_extents(ctx->seq_len, nranks);
     return TD_OK;
 }
 
@@ -752,6 +760,8 @@ static int kv_alloc(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t
     ctx->d = d;
     ctx->start = start;
     ctx->len = len;
+    ctx->cap = len;
+    ctx->lens = chunk_extents(seq_len, ctx->nranks);
     ctx->kv_ok = false;
     ctx->tm_ok = false;
     return TD_OK;
@@ -761,7 +771,8 @@ static int kv_finish(td_context* ctx) {
     ctx->tm_ok = false;
     if (ctx->dtype == TD_BF16 && (ctx->d == 64 || ctx->d == 128 || ctx->d == 256) && ctx->len > 0) {
         std::string msg;
-        const int64_t rows = ctx->b * ctx->n_kv * ctx->len;
+        const int64_t rows = ctx->b * ctx->n_kv * ctx->cap;  // rows of the allocation (stride cap)
+        if (rows >= (int64_t(1) << 31)) return set_err(TD_EINVAL, "kv: shard too large for 32-bit TMA rows");
         SplitPlan plan;
         if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(ctx->n_kv), static_cast<int>(ctx->n_kv),
                             ctx->len, static_cast<int>(ctx->d), ctx->sm_count, plan, msg))
@@ -805,6 +816,62 @@ int td_kv_generate(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t 
                                 ctx->stream))
         return rc;
     return kv_finish(ctx);
+}
+
+// Grows the placed shard's per-row capacity to `cap` tokens (rows are
+// re-strided, the data kept).
+static int kv_grow(td_context* ctx, int64_t cap) {
+    const size_t esz = td::dtype_bytes(ctx->dtype);
+    const size_t row_old = size_t(ctx->cap) * size_t(ctx->d) * esz, row_new = size_t(cap) * size_t(ctx->d) * esz;
+    const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (DevBuf* buf : {&ctx->k, &ctx->v}) {
+        void* fresh = nullptr;
+        TD_CUDA(cudaMalloc(&fresh, rows * row_new));
+        const cudaError_t e = cudaMemcpy2DAsync(fresh, row_new, buf->p, row_old,
+                                                size_t(ctx->len) * size_t(ctx->d) * esz, rows,
+                                                cudaMemcpyDeviceToDevice, ctx->stream);
+        if (e != cudaSuccess) {
+            cudaFree(fresh);
+            TD_CUDA(e);
+        }
+        TD_CUDA(cudaStreamSynchronize(ctx->stream));
+        buf->release();
+        buf->p = fresh;
+        buf->cap = rows * row_new;
+    }
+    ctx->cap = cap;
+    for (auto& tb : ctx->tabs) tb.total = -1;  // partition tables follow the new shape
+    return kv_finish(ctx);
+}
+
+int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "kv_append: no KV shard placed");
+    ctx->seq_len += 1;  // every rank: the cache is one token longer, on rank p-1
+    ctx->lens.back() += 1;
+    if (ctx->rank != ctx->nranks - 1) return TD_OK;
+    if (ctx->len == ctx->cap)
+        if (int rc = kv_grow(ctx, ctx->cap + std::max<int64_t>(1024, ctx->cap / 8))) return rc;
+    const size_t esz = td::dtype_bytes(ctx->dtype);
+    const size_t tok = size_t(ctx->d) * esz, pitch = size_t(ctx->cap) * tok;
+    const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
+    const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->k.p) + size_t(ctx->len) * tok, pitch, k, tok, tok, rows,
+                              kind, ctx->stream));
+    TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->v.p) + size_t(ctx->len) * tok, pitch, v, tok, tok, rows,
+                              kind, ctx->stream));
+    ctx->len += 1;
+    if (from_host) TD_CUDA(cudaStreamSynchronize(ctx->stream));  // the caller may reuse its buffer
+    return TD_OK;
+}
+
+int td_kv_reserve(td_context* ctx, int64_t tokens) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "kv_reserve: no KV shard placed");
+    if (tokens < 0) return set_err(TD_EINVAL, "kv_reserve: negative count");
+    if (ctx->rank != ctx->nranks - 1 || ctx->len + tokens <= ctx->cap) return TD_OK;
+    return kv_grow(ctx, ctx->len + tokens);
 }
 
 int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes) {
@@ -861,7 +928,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     const int64_t d = ctx->d;
     if (int rc = ensure_rows(ctx, rows, d)) return rc;
     SplitPlan plan;
-    if (int rc = plan_for(ctx, n_q, ctx->len, plan)) return rc;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap)) return rc;
     int rc = TD_OK;
     const void* qd = stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
@@ -966,7 +1033,7 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
     const int64_t rows = ctx->b * n_q, d = ctx->d;
     if (int rc = ensure_rows(ctx, rows, d)) return rc;
     SplitPlan plan;
-    if (int rc = plan_for(ctx, n_q, ctx->len, plan)) return rc;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap)) return rc;
     int rc = TD_OK;
     const void* qd = stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
@@ -1000,14 +1067,17 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
     const void* qd = stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
     const bool timed = (flags & TD_TIME_KERNELS) != 0;
-    const std::vector<int64_t> ext = chunk_extents(ctx->seq_len, p);
-    const int64_t max_len = ext[0];
+    // shard lengths: chunk_extents at placement, grown by td_kv_append on rank p-1
+    const std::vector<int64_t>& ext = ctx->lens;
+    if (ext.size() != size_t(p) || ext[size_t(w)] != ctx->len)
+        return set_err(TD_ESTATE, "ring_decode: shards are not the chunk_extents placement");
+    const int64_t max_len = *std::max_element(ext.begin(), ext.end());
     const size_t esz = td::dtype_bytes(ctx->dtype);
     const size_t row_bytes = size_t(ctx->b) * size_t(ctx->n_kv) * size_t(d) * esz;
 
     // own chunk first: root = parts[w]
     SplitPlan plan;
-    if ((rc = plan_for(ctx, n_q, ctx->len, plan))) return rc;
+    if ((rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap))) return rc;
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
                           ctx->r_max, ctx->r_lse, ctx->r_out, timed)))
         return rc;
@@ -1023,6 +1093,17 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
         const void* cur_k = ctx->k.p;
         const void* cur_v = ctx->v.p;
         int64_t cur_len = ctx->len;
+        if (ctx->cap != ctx->len) {  // appended shard: rows are cap apart, send them packed
+            const size_t tok = size_t(d) * esz, nbh = size_t(ctx->b) * size_t(ctx->n_kv);
+            for (int i = 0; i < 2; ++i) {
+                TD_CUDA(ctx->ring_own[i].ensure(nbh * size_t(ctx->len) * tok + 16));
+                TD_CUDA(cudaMemcpy2DAsync(ctx->ring_own[i].p, size_t(ctx->len) * tok, i ? ctx->v.p : ctx->k.p,
+                                          size_t(ctx->cap) * tok, size_t(ctx->len) * tok, nbh,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+            }
+            cur_k = ctx->ring_own[0].p;
+            cur_v = ctx->ring_own[1].p;
+        }
         // the transfer stream may start only once q/kv are ready on the compute stream
         TD_CUDA(cudaEventRecord(ctx->ring_ev[0], ctx->stream));
         TD_CUDA(cudaStreamWaitEvent(ctx->xfer, ctx->ring_ev[0], 0));
@@ -1045,7 +1126,7 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
             // compute on the received chunk once it lands, fold into the root
             TD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ring_ev[1], 0));
             SplitPlan pl;
-            if ((rc = plan_for(ctx, n_q, in_len, pl))) return rc;
+            if ((rc = plan_for(ctx, n_q, in_len, pl, 0))) return rc;
             if ((rc = run_partial(ctx, pl, qd, dst[0].p, dst[1].p, in_len, scale, false, ctx->row_max,
                                   ctx->lse, ctx->out_local, timed)))
                 return rc;

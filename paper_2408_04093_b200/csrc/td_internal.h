@@ -25,6 +25,7 @@ struct SplitPlan {
     // tiles_per_bh tiles of every bh, bh-major); the remaining pool_tiles of
     // each bh (from tile pool_first on) form the dynamic pool.
     int64_t bh_count = 0, t = 0, tiles_per_bh = 0, total_tiles = 0;
+    int64_t row_stride = 0;  // tokens per bh row in memory (0: t; > t with append capacity)
     int64_t full_tiles_per_bh = 0, pool_first = 0, pool_tiles = 0;
     int pool_chunk = 0, slot_warps = 0;
     int d = 0, n_q = 0, n_kv = 0, group = 0;

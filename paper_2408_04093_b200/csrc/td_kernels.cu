@@ -61,6 +61,7 @@ struct K1Args {
     const void* k;  // [bh][t][d]
     const void* v;
     int64_t bh_count, t, tiles_per_bh, total_tiles;
+    int64_t row_stride;  // tokens between consecutive bh rows in memory (>= t: append capacity)
     int d, n_q, n_kv, group, ctas, maxseg;
     float scale_log2;
     float* slot_m;  // [slots][group]
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     };
     auto issue = [&](int s, int64_t bh, int64_t tb) {
         if (lane != 0) return;
-        const int row = static_cast<int>(bh * a.t + tb * T);
+        const int row = static_cast<int>(bh * a.row_stride + tb * T);
         uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
         uint8_t* vd = kd + TILE_BYTES;
         mbar_expect_tx(&bars[warp][s], STAGE_BYTES);
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     const int64_t span = x1 - x0;
     const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
     const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
-    const int64_t rows_total = a.bh_count * a.t;
+    const int64_t rows_total = a.bh_count * a.row_stride;
     uint8_t* wsm = smem + size_t(warp) * S * STAGE_BYTES;
     const float* kg = static_cast<const float*>(a.k);
     const float* vg = static_cast<const float*>(a.v);
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     auto issue = [&](int64_t kk, int s) {
         const int64_t x = x0 + warp + kk * W;
         const int64_t bh = x / a.tiles_per_bh;
-        const int64_t row = bh * a.t + (x - bh * a.tiles_per_bh) * T;
+        const int64_t row = bh * a.row_stride + (x - bh * a.tiles_per_bh) * T;
         const int64_t avail = rows_total - row;
         const uint32_t bytes = static_cast<uint32_t>((avail < T ? avail : T) * D * 4);
         uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
             }
             const int64_t rem = a.t - tok0;
             const int nvalid = rem < T ? static_cast<int>(rem) : T;
-            const int64_t row0 = bh * a.t + tok0;
+            const int64_t row0 = bh * a.row_stride + tok0;
             float s = -CUDART_INF_F;
             if (lane < nvalid) {
                 const TIn* kr = kg + (row0 + lane) * D;
@@ -1158,6 +1159,7 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.v = v;
     a.bh_count = p.bh_count;
     a.t = p.t;
+    a.row_stride = p.row_stride > 0 ? p.row_stride : p.t;
     a.tiles_per_bh = p.tiles_per_bh;
     a.total_tiles = p.total_tiles;
     a.d = p.d;

@@ -468,6 +468,29 @@ class Worker:
                                 v.data_ptr(), 0 if k.is_cuda else 1))
         self._meta(dtype_of(k), b, n_kv, seq_len, d)
 
+    def append_kv(self, k, v):
+        """Append one token ([b, n_kv, 1, d] or [b, n_kv, d], cache dtype) to the
+        cache: every rank calls it, the token lands on rank p-1's shard."""
+        if self.rank == self.nranks - 1:
+            if dtype_of(k) != self.dtype or dtype_of(v) != self.dtype:
+                raise InvalidArgument(_capi.TD_EINVAL, "append_kv: token dtype differs from the cache")
+            if k.numel() != self.b * self.n_kv * self.d or v.numel() != k.numel():
+                raise InvalidArgument(_capi.TD_EINVAL, "append_kv: token must be [b, n_kv, 1, d]")
+            k, v = k.contiguous(), v.contiguous()
+            self._sync_in(k)
+            self._sync_in(v)
+            check(lib().td_kv_append(self.h, k.data_ptr(), v.data_ptr(), 0 if k.is_cuda else 1))
+            if k.is_cuda:  # the copy runs on the worker's stream: keep the sources alive until it does
+                s = _torch().cuda.ExternalStream(self.stream)
+                k.record_stream(s)
+                v.record_stream(s)
+        else:
+            check(lib().td_kv_append(self.h, None, None, 1))
+        self.seq_len += 1
+
+    def reserve_kv(self, tokens: int):
+        check(lib().td_kv_reserve(self.h, int(tokens)))
+
     def kv_info(self):
         s, n, nb = self._ct.c_int64(), self._ct.c_int64(), self._ct.c_size_t()
         check(lib().td_kv_info(self.h, self._ct.byref(s), self._ct.byref(n), self._ct.byref(nb)))

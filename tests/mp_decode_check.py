@@ -67,6 +67,32 @@ def main():
             print(json.dumps({"world": world, "dtype": "bf16" if dt == BF16 else "f32", "n": n, "b": b, "n_q": n_q,
                               "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring, "p2p_rel_err": e_p2p,
                               "ranks_agree": same, "ok": good}), flush=True)
+    # generation loop: append tokens to rank p-1's shard, decode the grown cache
+    b, n_q, n_kv, d, n0, steps = 1, 8, 2, 128, 4096 * world + 5, 40
+    seed = orc.mix64(7, n0)
+    qh = orc.seeded(orc.mix64(seed, 1), b * n_q * d, BF16).reshape(b, n_q, d)
+    kh = orc.seeded(orc.mix64(seed, 2), b * n_kv * (n0 + steps) * d, BF16).reshape(b, n_kv, n0 + steps, d)
+    vh = orc.seeded(orc.mix64(seed, 3), b * n_kv * (n0 + steps) * d, BF16).reshape(b, n_kv, n0 + steps, d)
+    s0, ln = td.shard_range(n0, world, rank)
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
+    w.place_kv(bf(kh[:, :, s0:s0 + ln]).cuda(), bf(vh[:, :, s0:s0 + ln]).cuda(), seq_len=n0)
+    q = bf(qh).cuda()
+    for s in range(steps):
+        w.append_kv(bf(kh[:, :, n0 + s:n0 + s + 1]).cuda(), bf(vh[:, :, n0 + s:n0 + s + 1]).cuda())
+        if s not in (0, steps - 1):
+            continue
+        tree, ring = w.tree_decode(q), w.ring_decode(q)
+        p2p = w.tree_decode(q, flags=td._capi.TD_P2P)
+        if rank == 0:
+            m = n0 + s + 1
+            want = orc.tree_decode(qh, np.ascontiguousarray(kh[:, :, :m]), np.ascontiguousarray(vh[:, :, :m]),
+                                   world, HIER, 1.0, F64, nthreads=8)
+            mx = np.max(np.abs(want))
+            errs = [float(np.max(np.abs(x.double().cpu().numpy() - want)) / mx) for x in (tree, ring, p2p)]
+            good = max(errs) <= 1e-3
+            ok &= good
+            print(json.dumps({"world": world, "append_step": s, "n": m, "tree_rel_err": errs[0],
+                              "ring_rel_err": errs[1], "p2p_rel_err": errs[2], "ok": good}), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
     w.close()

@@ -266,6 +266,38 @@ def test_worker_generate_and_decode(td, oracle, dtype, n_q, n_kv, n):
     w.close()
 
 
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_worker_append_loop(td, oracle, dtype):
+    """Multi-step decode: append one token per step (through capacity growth,
+    from host and device), decode the grown cache; equals the reference's
+    decode over the concatenated cache."""
+    import torch
+    b, n_q, n_kv, n, d, steps = 2, 8, 2, 1500, 128, 1100
+    q, k, v = make_inputs(oracle, 33, b, n_q, n_kv, n + steps, d, dtype)
+    w = td.Worker(0)
+    w.place_kv(dev(np.ascontiguousarray(k[:, :, :n]), dtype), dev(np.ascontiguousarray(v[:, :, :n]), dtype))
+    tdt = dev(q, dtype).dtype
+    for s in range(steps):
+        kt = torch.from_numpy(np.ascontiguousarray(k[:, :, n + s:n + s + 1])).to(tdt)
+        vt = torch.from_numpy(np.ascontiguousarray(v[:, :, n + s:n + s + 1])).to(tdt)
+        if s % 2:
+            kt, vt = kt.cuda(), vt.cuda()
+        w.append_kv(kt, vt)
+        if s in (0, 1, 1023, 1024, steps - 1):  # around the first capacity growth (+1024)
+            m = n + s + 1
+            out = w.tree_decode(dev(q, dtype))
+            want = oracle.tree_decode(q, np.ascontiguousarray(k[:, :, :m]), np.ascontiguousarray(v[:, :, :m]),
+                                      1, HIER, 1.0, F64)
+            assert rel_err(host(out), want) <= TOL[dtype], (s, rel_err(host(out), want))
+            r = w.ring_decode(dev(q, dtype))
+            assert rel_err(host(r), want) <= TOL[dtype]
+    assert w.kv_info()[1] == n + steps and w.seq_len == n + steps
+    w.reserve_kv(5000)
+    out = w.tree_decode(dev(q, dtype))
+    assert rel_err(host(out), oracle.tree_decode(q, k, v, 1, HIER, 1.0, F64)) <= TOL[dtype]
+    w.close()
+
+
 def test_worker_place_matches_generate(td, oracle):
     import torch
     q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
