@@ -340,7 +340,10 @@ def main():
         decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO | base_flags)
         e2e_times.append(time.perf_counter() - t0)
     e2e_ms = max_over_ranks(1000.0 * sum(e2e_times) / len(e2e_times), world)
-    ok = torch.allclose(out_host, out.cpu())
+    # same result through the host path; the dynamic tile pool regroups the
+    # split-KV sums from call to call (~1e-7 relative), so not bitwise
+    ref_out = out.cpu()
+    ok = float((out_host - ref_out).abs().max()) <= 1e-5 * float(ref_out.abs().max())
 
     # ---- per-phase breakdown (separate pass, not part of the timed number)
     phases = None

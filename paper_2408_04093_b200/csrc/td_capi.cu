@@ -621,6 +621,7 @@ int td_destroy(td_context* ctx) {
     ctx->out_bf16.release();
     for (auto& rb : ctx->ring)
         for (auto& x : rb) x.release();
+    for (auto& x : ctx->ring_own) x.release();
     for (auto& ev : ctx->ring_ev) cudaEventDestroy(ev);
     for (auto& pr : ctx->timers) {
         cudaEventDestroy(pr.first);
@@ -828,9 +829,12 @@ static int kv_grow(td_context* ctx, int64_t cap) {
     for (DevBuf* buf : {&ctx->k, &ctx->v}) {
         void* fresh = nullptr;
         TD_CUDA(cudaMalloc(&fresh, rows * row_new));
-        const cudaError_t e = cudaMemcpy2DAsync(fresh, row_new, buf->p, row_old,
-                                                size_t(ctx->len) * size_t(ctx->d) * esz, rows,
-                                                cudaMemcpyDeviceToDevice, ctx->stream);
+        // the unused tail of every row is read by partial tiles (masked out of the
+        // softmax, but 0 * NaN would poison P.V): keep it zero
+        cudaError_t e = cudaMemsetAsync(fresh, 0, rows * row_new, ctx->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(fresh, row_new, buf->p, row_old, size_t(ctx->len) * size_t(ctx->d) * esz,
+                                  rows, cudaMemcpyDeviceToDevice, ctx->stream);
         if (e != cudaSuccess) {
             cudaFree(fresh);
             TD_CUDA(e);

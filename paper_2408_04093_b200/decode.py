@@ -386,6 +386,7 @@ class Worker:
         check(lib().td_create(device, ctypes.byref(h)))
         self.h = h
         self.device = device
+        self._pending = []  # device tensors an enqueued td_kv_append still reads
         self.nranks, self.rank = 1, 0
         if comm is not None:
             nranks, rank, uid = comm
@@ -429,8 +430,13 @@ class Worker:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().td_destroy(self.h)
+            lib().td_destroy(self.h)  # synchronizes the worker's streams
             self.h = None
+        self._pending = []
+
+    def _sync_worker(self):
+        _torch().cuda.ExternalStream(self.stream).synchronize()
+        self._pending.clear()
 
     def __del__(self):
         try:
@@ -480,10 +486,10 @@ class Worker:
             self._sync_in(k)
             self._sync_in(v)
             check(lib().td_kv_append(self.h, k.data_ptr(), v.data_ptr(), 0 if k.is_cuda else 1))
-            if k.is_cuda:  # the copy runs on the worker's stream: keep the sources alive until it does
-                s = _torch().cuda.ExternalStream(self.stream)
-                k.record_stream(s)
-                v.record_stream(s)
+            if k.is_cuda:  # the copy runs on the worker's stream: hold the sources until it is synced
+                self._pending.append((k, v))
+                if len(self._pending) > 64:
+                    self._sync_worker()
         else:
             check(lib().td_kv_append(self.h, None, None, 1))
         self.seq_len += 1
@@ -514,7 +520,7 @@ class Worker:
         rc = fn(self.h, q.data_ptr(), n_q, float(scale), *extra, out.data_ptr(), flags)
         check(rc)
         if not host:
-            torch.cuda.ExternalStream(self.stream).synchronize()
+            self._sync_worker()
         return out
 
     def tree_decode(self, q, scale: float = 1.0, strategy: ReduceStrategy = ReduceStrategy.Hierarchical,

@@ -20,7 +20,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-HEADER = "algo,N,p,nodes,sim_time_s,elems_intra,elems_inter,peak_elems,rounds,max_abs_err"
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -37,7 +36,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2408_04093_b200 as td
-    from paper_2408_04093_b200 import _capi
+    from paper_2408_04093_b200 import _capi, report  # noqa: F401
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -104,8 +103,9 @@ def main():
             if rank == 0:
                 tc = td.tree_cost(b, n_q, n_kv, n, d, world) if algo == "tree" else td.ring_cost(b, n_q, n_kv, n, d, world)
                 rounds = (2 if comb == "nccl" else 1) if algo == "tree" else world - 1
-                line = f"{algo},{n},{world},1,{ms * 1e-3:.9g},{tc.elems_sent_total():.17g},0,{tc.peak_elems_per_worker},{rounds},nan"
-                lines.append((comb, line))
+                rec = td.report.BenchRecord(algo, n, world, 1, ms * 1e-3, float(tc.elems_sent_total()), 0.0,
+                                            int(tc.peak_elems_per_worker), rounds, math.nan)
+                lines.append((comb, rec))
                 rec = {"algo": algo, "combine": comb if world > 1 else "none", "N": n, "p": world,
                        "us_per_token": ms * 1000.0, "hbm_gbs": kv_rank / (ms * 1e-3) / 1e9,
                        "roofline_frac_of_measured": kv_rank / (ms * 1e-3) / 1e9 / peak,
@@ -114,21 +114,24 @@ def main():
                 print(json.dumps(rec), flush=True)
     if rank == 0:
         for comb in ("nccl", "p2p"):
-            sel = [ln for c, ln in lines if c == comb or (comb == "p2p" and ln.startswith("ring"))]
+            sel = [r for c, r in lines if c == comb or (comb == "p2p" and r.algo == "ring")]
             if not sel or (comb == "p2p" and world == 1):
                 continue
             path = args.out or os.path.join(ROOT, "gpurun_out", f"sweep_p{world}_{comb}.csv")
             if args.out:
                 path = path.replace(".csv", f"_{comb}.csv")
             os.makedirs(os.path.dirname(path), exist_ok=True)
+            seqs = sorted({r.seq_len for r in sel})
+            meta = {"time": "measured (CUDA events, max over ranks)", "device": "B200", "dtype": "bf16",
+                    "batch": str(b), "heads": f"{n_q}q/{n_kv}kv", "head_dim": str(d), "combine": comb,
+                    "algos": "tree ring" if world > 1 else "tree", "clusters": f"1x{world}",
+                    "seq_lens": " ".join(str(x) for x in seqs), "element_bytes": "2", "seed": "synthetic",
+                    "max_abs_err": "nan (parity is checked by tests/, not re-measured at sweep sizes)"}
+            out_ = td.report.SweepOutcome(records=sel, meta=meta)
             with open(path, "w") as f:
-                for k, v in (("time", "measured (CUDA events, max over ranks)"), ("device", "B200"),
-                             ("dtype", "bf16"), ("batch", "1"), ("heads", "32q/8kv"), ("head_dim", "128"),
-                             ("combine", comb), ("seed", "synthetic")):
-                    f.write(f"# {k}={v}\n")
-                f.write(HEADER + "\n")
-                for ln in sel:
-                    f.write(ln + "\n")
+                td.report.write_csv(out_, f)
+            with open(path.replace(".csv", ".json"), "w") as f:
+                td.report.write_json(out_, f)
     w.close()
     if world > 1:
         dist.barrier()

@@ -10,6 +10,10 @@ Fixtures:
                      proj/tests/data/rng_vectors.csv with the bits of
                      seeded_random_tensor produced by the reference library
                      (plus bf16 / f32 rounded values).
+  bench_io.json      `treedec report` file compatibility: inputs (reference
+                     sweeps, measured GPU sweeps, hand-made edge and malformed
+                     files) with the reference bench.cpp's re-emitted CSV/JSON,
+                     report text and exit status (oracle/_ref/ref_bench_tool).
   decode_cases.json  small tree/ring decode problems (seeded inputs, the
                      reference seeding convention of test_decode.cpp:18-23)
                      with the reference's outputs at every dtype, strategy and
@@ -80,8 +84,91 @@ def decode_cases(ref: Reference, orc: Oracle):
     return cases
 
 
+BENCH_TOOL = os.path.join(os.path.dirname(os.path.dirname(HERE)), "oracle", "_ref", "ref_bench_tool")
+_HDR = "algo,N,p,nodes,sim_time_s,elems_intra,elems_inter,peak_elems,rounds,max_abs_err"
+
+
+def _tool(*args) -> tuple[int, str]:
+    import subprocess
+    r = subprocess.run([BENCH_TOOL, *args], capture_output=True, text=True)
+    return r.returncode, r.stdout
+
+
+def bench_io_cases() -> list[dict]:
+    import tempfile
+    inputs = []
+    for fmt in ("csv", "json"):
+        for name, spec in (("f64_small", ("11", "f64", "2", "4", "64,128", "1x1,1x8,2x4")),
+                           ("bf16_mixed", ("5", "bf16", "4", "8", "96,200", "1x2,2x2,1x16"))):
+            rc, text = _tool("sweep", fmt, *spec)
+            assert rc == 0
+            inputs.append((f"ref_sweep_{name}.{fmt}", text))
+    root = os.path.dirname(os.path.dirname(HERE))
+    for fn in ("r1_sweep_p4_nccl.csv", "r1_sweep_p4_p2p.csv"):
+        path = os.path.join(root, "profiles", fn)
+        if os.path.exists(path):
+            inputs.append((f"measured_{fn}", open(path).read()))
+    edge_rows = "\n".join([
+        "tree,64,2,1,0.5,10,0,100,3,0", "ring,64,2,1,0.25,40,0,160,1,0",        # tree slower
+        "tree,128,4,1,0,0,0,0,0,0", "ring,128,4,1,0,0,0,0,0,0",                 # 0/0 cells
+        "tree,256,8,2,1e-300,1e20,1e-7,9223372036854775807,7,nan",             # unpaired, extremes
+        "ring,512,8,1, 2.5e-6,+3,-0,42,1,inf", "tree,512,8,1,0x1p-3,.5,5.,1,1,-inf",
+        "tree,1024,8,1,1.7976931348623157e308,123456789012345678,1e15,5,2,4.9e-300",
+        "ring,1024,8,1,1e16,0.1,1234567890123456,-1,2,2.2250738585072014e-308",
+        "tree,2048,3,1,3,3,3,3,3,3", "tree,2048,3,1,1,1,1,1,1,1", "ring,2048,3,1,2,2,2,2,2,2",  # duplicate: last wins
+    ])
+    inputs += [
+        ("edge_rows.csv", "# note=edge cases\n#novalue\n#  spaced = x=y\n" + _HDR + "\n" + edge_rows + "\n"),
+        ("crlf.csv", "# a=1\r\n" + _HDR + "\r\n\r\ntree,8,2,1,1,2,0,3,1,0\r\nring,8,2,1,2,4,0,5,1,0\r\n"),
+        ("no_trailing_newline.csv", _HDR + "\ntree,8,2,1,1,2,0,3,1,0"),
+        ("header_only.csv", _HDR + "\n"),
+        ("empty.csv", ""),
+        ("underflow.csv", _HDR + "\ntree,64,2,1,0,0,0,0,0,5e-324\n"),
+        ("underflow_zero.csv", _HDR + "\ntree,64,2,1,0,1e-400,0,0,0,0\n"),
+        ("u64_peak.csv", _HDR + "\ntree,64,2,1,0,0,0,18446744073709551615,0,0\n"),
+        ("comments_only.csv", "# a=1\n# b=2\n"),
+        ("missing_header.csv", "tree,64,2,1,0,0,0,0,0,0\n"),
+        ("short_row.csv", _HDR + "\ntree,64,2\n"),
+        ("bad_int.csv", _HDR + "\ntree,64,2,1,0,0,0,0,0,0\nring,sixty,2,1,0,0,0,0,0,0\n"),
+        ("trailing_chars.csv", _HDR + "\ntree,64,2,1,0.5x,0,0,0,0,0\n"),
+        ("bad_algo.csv", _HDR + "\nstar,64,2,1,0,0,0,0,0,0\n"),
+        ("int_overflow.csv", _HDR + "\ntree,99999999999999999999,2,1,0,0,0,0,0,0\n"),
+        ("double_overflow.csv", _HDR + "\ntree,64,2,1,1e999,0,0,0,0,0\n"),
+        ("space_int.csv", _HDR + "\ntree, 64,2,1,0,0,0,0,0,0\n"),
+        ("wrong_header.csv", "algo,N,p\n"),
+        ("bare_array.json", '[{"algo":"tree","N":64,"p":2,"nodes":1,"sim_time_s":0.5,\n"elems_intra":1.0,'
+                            '"elems_inter":2.0,"peak_elems":10,"rounds":3,"max_abs_err":0.0}]'),
+        ("json_int_fields_as_float.json", '{"meta":{"x":"y"},"records":[{"algo":"ring","N":64.0,"p":2,"nodes":1,'
+                                          '"sim_time_s":1,"elems_intra":3,"elems_inter":0,"peak_elems":7,'
+                                          '"rounds":1,"max_abs_err":0}]}'),
+        ("json_truncated.json", '{"records": [{"algo": "tree"'),
+        ("json_missing_key.json", '{"records": [{"algo": "tree", "N": 1}]}'),
+        ("json_no_records.json", '{"meta": {}}'),
+        ("json_multiline_error.json", '{\n  "records": [\n    {"algo": "tree",\n     "N": 12,,\n  ]\n}'),
+        ("leading_blank.json", '\n\n  [ ]'),
+    ]
+    cases = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, text in inputs:
+            path = os.path.join(tmp, name)
+            with open(path, "w", newline="") as f:
+                f.write(text)
+            c = {"name": name, "input": text}
+            for key, args in (("report", ("report", path)), ("csv", ("reemit", "csv", path)),
+                              ("json", ("reemit", "json", path))):
+                rc, out = _tool(*args)
+                c[key] = {"rc": rc, "stdout": out.replace(path, "FILE")}
+            cases.append(c)
+    return cases
+
+
 def main():
     build(ref=True)
+    if os.path.exists(BENCH_TOOL):
+        with open(os.path.join(HERE, "bench_io.json"), "w") as f:
+            json.dump({"source": "reference bench.cpp (write_csv / write_json / parse_bench_file / "
+                                 "write_report) via oracle/_ref/ref_bench_tool", "cases": bench_io_cases()},
+                      f, indent=1)
     ref, orc = Reference(), Oracle()
     with open(os.path.join(HERE, "rng_vectors.json"), "w") as f:
         json.dump({"source": "reference seeded_random_tensor via oracle/_ref; triples from "
