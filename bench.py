@@ -179,24 +179,25 @@ def align_streams(world, stream):
 # ---------------------------------------------------------------- CPU reference (oracle/_ref)
 def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
     """Times the reference's own tree_decode (compiled from /root/reference by
-    oracle/Makefile into oracle/_ref) on a bounded sample: `sample_heads`
-    q-heads of kv head 0 at the full sequence length, p = n_gpus workers
-    (parallel_workers when p > 1), the sampled rows spread over `nthreads` host
-    threads; scaled linearly to all b * n_q rows. Inputs are built once (not
-    timed, like shard_kv in BASELINE.md section 3); returns the per-step values."""
+    oracle/Makefile into oracle/_ref) on a bounded sample: `sample_heads` query
+    rows, all reading one kv head at the full sequence length (a row's cost
+    does not depend on which kv head it reads, and one kv head keeps the f64
+    inputs at 2 GB), p = n_gpus workers (parallel_workers when p > 1), the
+    sampled rows spread over `nthreads` host threads; scaled linearly to all
+    b * n_q rows. Inputs are built once (not timed, like shard_kv in
+    BASELINE.md section 3); returns the per-step values."""
     from oracle.oracle import BF16, F32, HIER, Oracle, Reference
     _, b, n_q, n_kv, n, d, dt = wl
     n = args.seq_len or n
     orc, ref = Oracle(), Reference()
     dtc = BF16 if dt == "bf16" else F32
     seed = orc.mix64(0, n)
-    g = n_q // n_kv
-    sample_heads = max(1, min(sample_heads, g))
+    rows = b * n_q
+    sample_heads = max(1, min(sample_heads, rows))
     nthreads = max(1, min(nthreads, sample_heads))
     qh = orc.seeded(orc.mix64(seed, 1), sample_heads * d, dtc).reshape(1, sample_heads, d)
     k0 = orc.seeded(orc.mix64(seed, 2), n * d, dtc).reshape(1, 1, n, d)
     v0 = orc.seeded(orc.mix64(seed, 3), n * d, dtc).reshape(1, 1, n, d)
-    rows = b * n_q
     vals = []
     with ref.prepare(qh, k0, v0, n_gpus, dtc) as pr:
         del k0, v0
@@ -206,7 +207,7 @@ def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
                 vals.append(secs / sample_heads * rows * 1e6 / b)  # us per decoded token
     cores = nthreads * (n_gpus if n_gpus > 1 else 1)
     return vals, {
-        "sample": f"{sample_heads} q-head(s) of kv head 0 at N={n}, p={n_gpus} worker(s), {nthreads} row "
+        "sample": f"{sample_heads} query row(s) over one kv head at N={n}, p={n_gpus} worker(s), {nthreads} row "
                   f"thread(s); scaled x{rows / sample_heads:g} to b*n_q={rows} rows; inputs built once (untimed)",
         "cores": cores,
     }
@@ -217,10 +218,9 @@ def run_reference_arm(args, wl, world, rank):
         return
     nproc = os.cpu_count() or 1
     _, b, n_q, n_kv, n, d, dt = wl
-    g = n_q // n_kv
     # every host thread: p = N workers per call (threads), sampled rows in parallel
-    row_threads = max(1, nproc // max(1, args.gpus))
-    heads = min(g, row_threads)
+    row_threads = max(1, min(b * n_q, nproc // max(1, args.gpus)))
+    heads = row_threads
     t0 = time.time()
     vals, info = reference_cpu(args, wl, args.gpus, heads, row_threads, steps=args.steps, warmup=args.warmup)
     value = sum(vals) / len(vals)
@@ -360,7 +360,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            heads = args.cpu_sample_heads or (n_q // n_kv)
+            heads = args.cpu_sample_heads or min(b * n_q, os.cpu_count() or 1)
             vals, info = reference_cpu(args, wl, 1, heads, os.cpu_count() or 1, steps=3)
             cpu = {"value": min(vals), "unit": "µs/token", "cores": info["cores"], "kind": "reference",
                    "sample": info["sample"] + f"; host nproc={os.cpu_count()}"}

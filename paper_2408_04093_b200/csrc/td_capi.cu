@@ -951,7 +951,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         xa.rank = ctx->rank;
         xa.epoch = ++ctx->x_epoch;
         xa.max_rows = ctx->x_max_rows;
-        xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 2 * int64_t(ctx->sm_count));
+        xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
         xa.error = static_cast<int*>(ctx->x_err.p);
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
         const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
@@ -964,8 +964,6 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
             e1 = (*ctx->cur_phase)[ctx->cur_mark++];
         }
         float* xdst = (flags & TD_HOST_IO) ? ctx->out : out;
-        if (ctx->b * ctx->n_kv > td::kXchgBlocks)
-            return set_err(TD_EINVAL, "tree_decode: TD_P2P supports at most 1024 (batch, kv-head) rows");
         TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                            ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
         phase_mark(ctx);

@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 #include "td_device.cuh"
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int c = (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const int64_t A = a.tiles_per_bh;  // static tiles per bh (the pool holds the rest)
     const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
     const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int c = (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
     const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
     const int64_t span = x1 - x0;
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = a.reverse ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int c = (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
     const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
     const int64_t span = x1 - x0;
@@ -802,97 +803,136 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
 // an empty chunk (attention.cpp:56-61). One block of K2_THREADS per row;
 // warps stride over the candidate (cta, warp) slots.
 // =========================================================================
-constexpr int K2_THREADS = 512;
+constexpr int K2_THREADS = 32;  // one warp (= one output row) per block: rows spread over SMs
 
-struct K2Smem {
-    float m[K2_THREADS];    // per-group running max (log2 units)
-    float l[K2_THREADS];    // per-group running sum
-    float acc[K2_THREADS];  // per-group running o, [grp][j]
+// The CTA states covering one bh: CTAs c_lo .. c_lo + S - 1; the first one
+// holds bh in its segment seg_lo, the others in segment 0. Reads only
+// host-written tables, so K2 computes it before griddepcontrol.wait.
+struct Cover {
+    int64_t c_lo = 0, seg_lo = 0;
+    int S = 0;
 };
-
-// Merges the CTA states of row r (over bh_count * group) into out_row (D
-// floats, any address space) and returns (lse, row_max) in natural log units.
-// One round of independent loads: thread (grp, j) streams the candidates
-// grp, grp + NG, ... of its d-column with an online rescale, then the NG
-// group states are merged through shared memory (one barrier). Only the
-// first covering CTA can start in an earlier bh, so no per-candidate
-// division is needed. All threads of the block call it.
-__device__ void merge_row(const K1Args& a, int64_t r, K2Smem& sm, float* out_row, float& lse_o,
-                          float& rmax_o) {
-    const int64_t bh = r / a.group;
-    const int h = static_cast<int>(r % a.group);
-    const int D = a.d, g = a.group;
-    int64_t c_lo = 0, c_hi = -1, seg_lo = 0;
+__device__ __forceinline__ Cover cover_of(const K1Args& a, int64_t bh) {
+    Cover cv;
+    int64_t c_hi = -1;
     if (a.bh_table) {
-        c_lo = __ldg(a.bh_table + 3 * bh);
+        cv.c_lo = __ldg(a.bh_table + 3 * bh);
         c_hi = __ldg(a.bh_table + 3 * bh + 1);
-        seg_lo = __ldg(a.bh_table + 3 * bh + 2);
+        cv.seg_lo = __ldg(a.bh_table + 3 * bh + 2);
     } else if (a.tiles_per_bh > 0 && a.total_tiles > 0) {
         const int64_t X = bh * a.tiles_per_bh, Xe = X + a.tiles_per_bh - 1;
-        c_lo = div_nn((X + 1) * a.ctas + a.total_tiles - 1, a.total_tiles) - 1;
+        cv.c_lo = div_nn((X + 1) * a.ctas + a.total_tiles - 1, a.total_tiles) - 1;
         c_hi = div_nn((Xe + 1) * a.ctas + a.total_tiles - 1, a.total_tiles) - 1;
-        seg_lo = bh - div_nn(cta_begin(a.total_tiles, static_cast<int>(c_lo), a.ctas), a.tiles_per_bh);
+        cv.seg_lo = bh - div_nn(cta_begin(a.total_tiles, static_cast<int>(cv.c_lo), a.ctas), a.tiles_per_bh);
     }
-    const int S = static_cast<int>(c_hi - c_lo + 1);
-    const int SP = S;
-    const bool wide = blockDim.x >= static_cast<unsigned>(D);
-    const int NG = wide ? static_cast<int>(blockDim.x) / D : 1;
-    const int grp = wide ? static_cast<int>(threadIdx.x) / D : 0;
-    const int jstep = wide ? D : static_cast<int>(blockDim.x);
-    if (grp < NG) {
-        for (int j = wide ? threadIdx.x % D : threadIdx.x; j < D; j += jstep) {
-            float mt = -CUDART_INF_F, lt = 0.f, at = 0.f;
-            for (int i0 = grp; i0 < SP; i0 += 8 * NG) {
-                float mv[8], lv[8], ov[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u * NG;
-                    if (i < S) {  // static CTA state
-                        const int64_t cs = (c_lo + i) * a.maxseg + (i == 0 ? seg_lo : 0);
-                        mv[u] = __ldcg(a.cslot_m + cs * g + h);
-                        lv[u] = __ldcg(a.cslot_l + cs * g + h);
-                        ov[u] = __ldcg(a.cslot_o + (cs * g + h) * D + j);
-                    } else {
-                        mv[u] = -CUDART_INF_F;
-                        lv[u] = ov[u] = 0.f;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (mv[u] == -CUDART_INF_F) continue;
-                    if (mv[u] > mt) {
-                        const float sc = fast_exp2(mt - mv[u]);  // 0 when mt = -inf
-                        at *= sc;
-                        lt *= sc;
-                        mt = mv[u];
-                    }
-                    const float e = fast_exp2(mv[u] - mt);
-                    at += e * ov[u];
-                    lt += e * lv[u];
-                }
+    cv.S = static_cast<int>(c_hi - cv.c_lo + 1);
+    return cv;
+}
+
+// Lane columns of a row of D floats: chunk c, element v is column
+// (c * 32 + lane) * V + v (V = 4: float4 loads).
+template <int V, int NC>
+struct LaneRow {
+    float v[NC][V];
+};
+
+// Merges the CTA states of row r into the lane's columns and returns
+// (lse, row_max) in natural log units; one warp per row, no shared memory,
+// no barrier. Every lane loads the (m, l, o-columns) of BO candidates at
+// once -- m and l are broadcast loads -- so a row with S <= BO candidates
+// costs a single L2 round trip; M is the max over the candidates already in
+// registers (a lane-parallel pass + shuffles only when S > BO).
+template <int V, int NC, int BO>
+__device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const Cover& cv, LaneRow<V, NC>& res,
+                                               float& lse_o, float& rmax_o) {
+    using vec = typename std::conditional<V == 4, float4, float>::type;
+    static_assert(BO <= 32, "one candidate (m, l) per lane");
+    const int lane = threadIdx.x & 31;
+    const int h = static_cast<int>(r % a.group);
+    const int D = a.d, g = a.group, S = cv.S;
+    auto cs_of = [&](int i) { return (cv.c_lo + i) * a.maxseg + (i == 0 ? cv.seg_lo : 0); };
+    // 32-bit float offsets (the CTA-state arrays are small): candidate i >= 1 sits at
+    // a fixed stride from candidate 1; candidate 0 has its own segment
+    const int st = a.maxseg * g;
+    const int b0 = static_cast<int>(cs_of(0) * g + h), b1 = static_cast<int>(cs_of(1) * g + h);
+    const int col0 = lane * V;
+    vec ov[BO][NC];
+    float ml = -CUDART_INF_F, ll = 0.f;  // lane i holds (m, l) of candidate i0 + i (BO <= 32)
+    auto load = [&](int i0) {
+        {
+            const int i = i0 + lane;
+            const int off = i == 0 ? b0 : b1 + (i - 1) * st;
+            ml = -CUDART_INF_F;
+            ll = 0.f;
+            if (lane < BO && i < S) {
+                ml = __ldcg(a.cslot_m + off);
+                ll = __ldcg(a.cslot_l + off);
             }
-            sm.acc[grp * D + j] = at;
-            if (j == (wide ? 0 : static_cast<int>(threadIdx.x)) && (wide || threadIdx.x == 0)) {
-                sm.m[grp] = mt;
-                sm.l[grp] = lt;
+        }
+#pragma unroll
+        for (int u = 0; u < BO; ++u) {
+            const int i = i0 + u;
+            const int off = i == 0 ? b0 : b1 + (i - 1) * st;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (i < S && col0 + c * 32 * V < D)
+                    ov[u][c] = __ldcg(reinterpret_cast<const vec*>(a.cslot_o + off * D + col0 + c * 32 * V));
+        }
+    };
+    load(0);
+    float M = -CUDART_INF_F;
+    if (S <= BO) {
+        M = ml;
+    } else {
+        for (int i = lane; i < S; i += 32) M = fmaxf(M, __ldcg(a.cslot_m + (i == 0 ? b0 : b1 + (i - 1) * st)));
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float acc[NC][V], L = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[c][v] = 0.f;
+    for (int i0 = 0; i0 < S; i0 += BO) {
+        if (i0 > 0) load(i0);
+        // lane-parallel weights, then broadcast per candidate
+        const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - M);
+        float lsum = e_l * ll;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+        L += lsum;
+#pragma unroll
+        for (int u = 0; u < BO; ++u) {
+            const float e = __shfl_sync(0xffffffffu, e_l, u);
+            if (i0 + u < S) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const float* o = reinterpret_cast<const float*>(&ov[u][c]);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[c][v] += e * o[v];
+                }
             }
         }
     }
-    __syncthreads();
-    float M = -CUDART_INF_F;
-    for (int q = 0; q < NG; ++q) M = fmaxf(M, sm.m[q]);
-    float L = 0.f;
-    for (int q = 0; q < NG; ++q)
-        if (sm.m[q] != -CUDART_INF_F) L += fast_exp2(sm.m[q] - M) * sm.l[q];
-    for (int jj = threadIdx.x; jj < D; jj += blockDim.x) {
-        float O = 0.f;
-        for (int q = 0; q < NG; ++q)
-            if (sm.m[q] != -CUDART_INF_F) O += fast_exp2(sm.m[q] - M) * sm.acc[q * D + jj];
-        out_row[jj] = (M == -CUDART_INF_F) ? 0.f : O / L;
+    const bool empty = M == -CUDART_INF_F;
+    const float inv = empty ? 0.f : 1.f / L;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) res.v[c][v] = acc[c][v] * inv;
+    lse_o = empty ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
+    rmax_o = empty ? -CUDART_INF_F : M * kLn2;
+}
+
+template <int V, int NC>
+__device__ __forceinline__ void store_row(float* dst, int D, const LaneRow<V, NC>& res) {
+    using vec = typename std::conditional<V == 4, float4, float>::type;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int col = (c * 32 + lane) * V;
+        if (col < D) *reinterpret_cast<vec*>(dst + col) = *reinterpret_cast<const vec*>(res.v[c]);
     }
-    lse_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
-    rmax_o = (M == -CUDART_INF_F) ? -CUDART_INF_F : M * kLn2;
-    __syncthreads();  // sm is reused by the next row
 }
 
 __device__ __forceinline__ int64_t out_row_of(const K1Args& a, int64_t r) {
@@ -900,72 +940,76 @@ __device__ __forceinline__ int64_t out_row_of(const K1Args& a, int64_t r) {
     return (bh / a.n_kv) * a.n_q + (bh % a.n_kv) * a.group + h;
 }
 
-constexpr int kXchgMaxBlocks = kXchgBlocks;
-
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // =========================================================================
 // K2 (launched with programmatic dependent launch: its blocks are scheduled
 // as K1's CTAs retire and wait in griddepcontrol.wait, so the kernel
-// boundary costs no launch latency). Each block merges rows r = blockIdx,
-// blockIdx + grid, ... of the shard (merge_row over the CTA states) and, per
-// a.tail.mode:
+// boundary costs no launch latency). Warp w of the grid merges rows
+// r = w, w + warps, ... of the shard (merge_row_warp over the CTA states) and,
+// per a.tail.mode:
 //   kTailPartial  row_max / lse / out of the shard -- attention_chunk_partial
 //                 (attention.cpp:146-168), combine_partials across CTAs
 //                 (attention.cpp:207-241)
 //   kTailFinal    out only (p = 1: the partial is the decode result)
 // =========================================================================
+template <int V, int NC, int BO>
 __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
-    __shared__ K2Smem sm;
+    const unsigned long long t_pre = a.dbg ? gtimer() : 0ull;
+    const int64_t rows = a.bh_count * a.group;
+    const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    // host-written tables only: overlaps K1's tail
+    const Cover cv0 = w0 < rows ? cover_of(a, w0 / a.group) : Cover{};
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // the other parity's pool counters are the next launch's: zero them
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
              i += int64_t(gridDim.x) * blockDim.x)
             a.pool_next[i] = 0u;
-    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
-    if (ts && threadIdx.x == 0) ts[0] = gtimer();
+    unsigned long long* ts = (a.dbg && w0 < 512 && (threadIdx.x & 31) == 0) ? a.dbg + 8 + 8 * w0 : nullptr;
+    if (ts) {
+        ts[0] = gtimer();
+        ts[3] = t_pre;
+    }
     const Tail& t = a.tail;
-    const int64_t rows = a.bh_count * a.group;
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int64_t r = w0; r < rows; r += nw) {
         const int64_t orow = out_row_of(a, r);
         float l, m;
-        merge_row(a, r, sm, t.out + orow * a.d, l, m);
-        if (ts && threadIdx.x == 0 && r == blockIdx.x) ts[2] = gtimer();
-        if (t.mode == kTailPartial && threadIdx.x == 0) {
+        LaneRow<V, NC> res;
+        merge_row_warp<V, NC, BO>(a, r, r == w0 ? cv0 : cover_of(a, r / a.group), res, l, m);
+        store_row(t.out + orow * a.d, a.d, res);
+        if (ts && r == w0) ts[2] = gtimer();
+        if (t.mode == kTailPartial && (threadIdx.x & 31) == 0) {
             t.lse[orow] = l;
             t.row_max[orow] = m;
         }
     }
-    if (ts && threadIdx.x == 0) ts[4] = gtimer();
+    if (ts) ts[4] = gtimer();
 }
 
 // =========================================================================
 // K2x: K2 fused with the one-shot NVLink exchange (kTailExchange), LL
 // protocol: every 8-byte word of the exchange buffer is (value, epoch), so a
 // word's data and its readiness travel in one single-copy-atomic store over
-// NVLink -- no system fence, no separate flag. Each block merges its rows
-// (merge_row) and stores [out | lse] of them into slot `rank` of every peer's
-// buffer (CUDA-IPC mapped HBM); then it reads, word by word, the p sources of
-// its rows (spinning until a word carries this step's epoch) and combines:
-// shift = max lse, w = e^(lse - shift), out = sum w o / sum w -- the
+// NVLink -- no system fence, no separate flag. Each warp merges its rows
+// (merge_row_warp) and stores [out | lse] of them into slot `rank` of every
+// peer's buffer (CUDA-IPC mapped HBM); then it reads, word by word, the p
+// sources of its rows (spinning until a word carries this step's epoch) and
+// combines: shift = max lse, w = e^(lse - shift), out = sum w o / sum w -- the
 // allreduce(max), partial_to_numerator, allreduce(sum) and n/d of
 // decode.cpp:129-173 in one exchange. Slots alternate by epoch parity (a rank
 // cannot overwrite a slot a peer still reads: it would first need the peer's
 // next-step words). The grid never exceeds the co-resident capacity and every
-// block pushes before it reads, so the exchange cannot deadlock; each spin is
-// bounded (~2 s) and reports through x.error.
+// warp pushes all its rows before it reads, so the exchange cannot deadlock;
+// each spin is bounded (~2 s) and reports through x.error.
 // =========================================================================
 __device__ __forceinline__ void st_ll(uint2* p, float v, unsigned e) {
     asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(e)
                  : "memory");
+}
+__device__ __forceinline__ uint2 ld_word(const uint2* p) {  // one poll, no wait
+    uint2 w;
+    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(p) : "memory");
+    return w;
 }
 __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
     unsigned v, f;
@@ -981,58 +1025,137 @@ __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
     return __uint_as_float(v);
 }
 
+template <int V, int NC, int BO>
 __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
-    __shared__ K2Smem sm;
-    __shared__ float row[256];
+    const int64_t rows = a.bh_count * a.group;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const Cover cv0 = w0 < rows ? cover_of(a, w0 / a.group) : Cover{};
+    const Xchg& x = a.tail.x;
+    constexpr int PMAX = 8;  // peers held in registers (the exchange spans one NVLink domain)
+    uint2* pp[PMAX];         // peer buffers, read before the wait (host-written)
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) pp[k] = k < x.p ? reinterpret_cast<uint2* const*>(x.peers)[k] : nullptr;
+    const uint2* own = reinterpret_cast<uint2* const*>(x.peers)[x.rank];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // the other parity's pool counters are the next launch's: zero them
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
              i += int64_t(gridDim.x) * blockDim.x)
             a.pool_next[i] = 0u;
-    const Xchg& x = a.tail.x;
-    const int64_t rows = a.bh_count * a.group;
     const int D = a.d;
     const unsigned par = x.epoch & 1u;
     const int64_t stride = x.max_rows * int64_t(D + 1);  // words per (parity, source)
     uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
-    unsigned long long* ts = (a.dbg && blockIdx.x < 512) ? a.dbg + 8 + 8 * blockIdx.x : nullptr;
-    if (ts && threadIdx.x == 0) ts[0] = gtimer();
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // merge + push
+    unsigned long long* ts = (a.dbg && w0 < 512 && lane == 0) ? a.dbg + 8 + 8 * w0 : nullptr;
+    if (ts) ts[0] = gtimer();
+    for (int64_t r = w0; r < rows; r += nw) {  // merge + push
         const int64_t orow = out_row_of(a, r);
         float l, m;
-        merge_row(a, r, sm, row, l, m);  // ends with a barrier
-        if (ts && threadIdx.x == 0 && r == blockIdx.x) ts[2] = gtimer();
+        LaneRow<V, NC> res;
+        merge_row_warp<V, NC, BO>(a, r, r == w0 ? cv0 : cover_of(a, r / a.group), res, l, m);
+        if (ts && r == w0) ts[2] = gtimer();
         const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
-        for (int j = threadIdx.x; j <= D; j += blockDim.x) {
-            const float v = j < D ? row[j] : l;
-            for (int q = 0; q < x.p; ++q) st_ll(peers[q] + off + j, v, x.epoch);
-        }
+        auto push = [&](uint2* dst) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const int col = (c * 32 + lane) * V + v;
+                    if (col < D) st_ll(dst + col, res.v[c][v], x.epoch);
+                }
+            if (lane == 0) st_ll(dst + D, l, x.epoch);
+        };
+#pragma unroll
+        for (int q = 0; q < PMAX; ++q)
+            if (q < x.p) push(pp[q] + off);
+        for (int q = PMAX; q < x.p; ++q) push(peers[q] + off);
     }
-    if (ts && threadIdx.x == 0) ts[1] = gtimer();
-    const uint2* own = peers[x.rank];
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {  // exact combine of the p partials
+    if (ts) ts[1] = gtimer();
+    for (int64_t r = w0; r < rows; r += nw) {  // exact combine of the p partials
         const int64_t orow = out_row_of(a, r);
-        for (int j = threadIdx.x; j < D; j += blockDim.x) {
-            float lq[8], shift = -CUDART_INF_F;
-            for (int q = 0; q < x.p; ++q) {
-                const float l = ld_ll(own + (int64_t(par) * x.p + q) * stride + orow * (D + 1) + D, x.epoch, x.error);
-                if (q < 8) lq[q] = l;
-                shift = fmaxf(shift, l);
+        const uint2* base = own + int64_t(par) * x.p * stride + orow * (D + 1);
+        // every word of the first PMAX sources (lse + this lane's columns) is polled in
+        // one batch, and re-polled -- again as a batch -- until all carry this epoch
+        uint2 wl[PMAX], wo[PMAX][NC][V];
+        const long long t0 = clock64();
+        for (;;) {
+            bool all = true;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                const uint2* slot = base + k * stride;
+                wl[k] = ld_word(slot + D);
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const int col = (c * 32 + lane) * V + v;
+                        if (col < D) wo[k][c][v] = ld_word(slot + col);
+                    }
             }
-            float num = 0.f, den = 0.f;
-            for (int q = 0; q < x.p; ++q) {
-                const uint2* slot = own + (int64_t(par) * x.p + q) * stride + orow * (D + 1);
-                const float l = q < 8 ? lq[q] : ld_ll(slot + D, x.epoch, x.error);
-                const float w = l == -CUDART_INF_F ? 0.f : expf(l - shift);
-                den += w;
-                num += w * ld_ll(slot + j, x.epoch, x.error);
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                all &= wl[k].y == x.epoch;
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        if ((c * 32 + lane) * V + v < D) all &= wo[k][c][v].y == x.epoch;
             }
-            a.tail.out[orow * D + j] = num / den;
+            if (__all_sync(0xffffffffu, all)) break;
+            if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
+                atomicExch(x.error, 1);
+                break;
+            }
         }
+        if (ts && r == w0) ts[3] = gtimer();
+        float shift = -CUDART_INF_F, den = 0.f;
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k)
+            if (k < x.p) shift = fmaxf(shift, __uint_as_float(wl[k].x));
+        for (int q = PMAX; q < x.p; ++q) shift = fmaxf(shift, ld_ll(base + q * stride + D, x.epoch, x.error));
+        float num[NC][V];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) num[c][v] = 0.f;
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k) {
+            if (k >= x.p) continue;
+            const float l = __uint_as_float(wl[k].x);
+            const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - shift);
+            den += wgt;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) num[c][v] += wgt * __uint_as_float(wo[k][c][v].x);
+        }
+        for (int q = PMAX; q < x.p; ++q) {  // beyond one NVLink domain: word by word
+            const uint2* slot = base + q * stride;
+            const float l = ld_ll(slot + D, x.epoch, x.error);
+            const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - shift);
+            den += wgt;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const int col = (c * 32 + lane) * V + v;
+                    if (col < D) num[c][v] += wgt * ld_ll(slot + col, x.epoch, x.error);
+                }
+        }
+        float* dst = a.tail.out + orow * D;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int col = (c * 32 + lane) * V + v;
+                if (col < D) dst[col] = num[c][v] / den;
+            }
     }
-    if (ts && threadIdx.x == 0) ts[3] = gtimer();
-    if (ts && threadIdx.x == 0) ts[4] = gtimer();
+    if (ts) ts[4] = gtimer();
 }
 
 // =========================================================================
@@ -1393,7 +1516,6 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
         }
     } else {
         size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
-        if (sm < sizeof(K2Smem)) sm = sizeof(K2Smem);
         if (p.dtype == kBF16) {
             if ((e = set_smem(k1_generic<__nv_bfloat16>, sm)) != cudaSuccess) return e;
             k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
@@ -1411,10 +1533,12 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
 
 namespace {
 
-// K2 right behind K1 with programmatic stream serialization (PDL).
-cudaError_t launch_k2(const K1Args& a, int64_t grid, bool exchange, cudaStream_t st) {
+// K2 right behind K1 with programmatic stream serialization (PDL); one warp
+// per row, the lane-column layout chosen by d.
+template <int V, int NC, int BO>
+cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, bool exchange, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid < 1 ? 1 : grid));
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks < 1 ? 1 : blocks));
     cfg.blockDim = dim3(K2_THREADS);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
@@ -1423,7 +1547,18 @@ cudaError_t launch_k2(const K1Args& a, int64_t grid, bool exchange, cudaStream_t
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange, a) : cudaLaunchKernelEx(&cfg, k2_combine, a);
+    return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange<V, NC, BO>, a)
+                    : cudaLaunchKernelEx(&cfg, k2_combine<V, NC, BO>, a);
+}
+
+cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaStream_t st) {
+    const int64_t rows = a.bh_count * a.group;
+    constexpr int WPB = K2_THREADS / 32;
+    int64_t blocks = (rows + WPB - 1) / WPB;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (a.d % 4 == 0 && a.d <= 128) return launch_k2_t<4, 1, 32>(a, blocks, exchange, st);
+    if (a.d % 4 == 0) return launch_k2_t<4, 2, 16>(a, blocks, exchange, st);
+    return launch_k2_t<1, 8, 8>(a, blocks, exchange, st);
 }
 
 }  // namespace
@@ -1440,8 +1575,7 @@ cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void*
     a.tail.out = out;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
-    const int64_t rows = p.bh_count * p.group;
-    return launch_k2(a, rows < 4096 ? rows : 4096, false, st);
+    return launch_k2(a, 4096, false, st);
 }
 
 cudaError_t launch_decode_final(const SplitPlan& p, const void* q, const void* k, const void* v,
@@ -1453,8 +1587,7 @@ cudaError_t launch_decode_final(const SplitPlan& p, const void* q, const void* k
     a.tail.out = out;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
-    const int64_t rows = p.bh_count * p.group;
-    return launch_k2(a, rows < 4096 ? rows : 4096, false, st);
+    return launch_k2(a, 4096, false, st);
 }
 
 cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void* k, const void* v,
@@ -1474,8 +1607,7 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.x.error = xa.error;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
-    const int64_t rows = p.bh_count * p.group;
-    return launch_k2(a, rows < xa.max_blocks ? rows : xa.max_blocks, true, st);
+    return launch_k2(a, xa.max_blocks, true, st);
 }
 
 namespace {

@@ -47,14 +47,17 @@ def main():
         t0 = st[0]
         ends = sorted((st[4097 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4097 + 2 * c])
         starts = sorted((st[4096 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4096 + 2 * c])
-        blocks = [st[8 + 8 * i: 8 + 8 * i + 5] for i in range(64) if st[8 + 8 * i] != 0]
+        blocks = [st[8 + 8 * i: 8 + 8 * i + 8] for i in range(64) if st[8 + 8 * i] != 0]
         rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
         summary = {"k1_end": rel(st[1])}
         if ends:
             qt = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
             summary["cta_start_q"] = [qt(starts, f) for f in (0.0, 0.5, 1.0)]
             summary["cta_end_q"] = [qt(ends, f) for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
-        for k, name in enumerate(["k2_entry", "pushed", "merged", "seen", "done"]):
+        names = ["k2_entry", "pushed", "merged", "seen", "done"]
+        if world == 1:
+            names[3] = "k2_prewait"
+        for k, name in enumerate(names):
             vals = [bl[k] for bl in blocks if bl[k]]
             if vals:
                 summary[name + "_min"] = rel(min(vals))
