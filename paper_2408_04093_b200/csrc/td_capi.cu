@@ -184,11 +184,16 @@ struct td_context {
     bool x_ready = false;
 
     DevBuf dbg;  // TD_DEBUG_TS stamps
+    int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
+    DevBuf tlbuf;           // TD_DEBUG_TIMELINE stamps (read back as dbg[5000..6144))
 
     // calibrated static partition: per-CTA streaming speed of this GPU's SMs
     // (blocks land on the same SMs launch after launch), measured once
     std::vector<float> cal_w;
     bool cal_failed = false;
+    DevBuf sm_map, claims;      // SM affinity of the calibrated CTA indices
+    bool sm_map_ok = false;
+    unsigned claim_epoch = 0;
     DevBuf cal_q;
     struct PartTab {
         int64_t total = -1, per_bh = 0, bh = 0;
@@ -245,6 +250,14 @@ bool calibration_enabled() {
     return on;
 }
 
+bool sm_affinity_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TD_SM_AFFINITY");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // Device tables of the speed-weighted static partition of `plan` (cached).
 int apply_partition(td_context* ctx, SplitPlan& plan) {
     for (auto& tb : ctx->tabs)
@@ -279,9 +292,11 @@ int ensure_rows(td_context* ctx, int64_t rows, int64_t d);
 
 // Measures how fast each CTA of the split kernel streams on this GPU (per-CTA
 // globaltimer stamps, static split, two rounds: equal ranges, then ranges
-// weighted by the first round's speeds) and keeps speed weights per block
-// index. Block b lands on the same SM in every launch of this grid, so the
-// weights carry over; they only move work, never change what is computed.
+// weighted by the first round's speeds) and keeps speed weights per CTA index
+// together with the SM each index ran on (sm_map): later launches give index c
+// to the CTA that lands on that SM, so the weights hold whatever order the CTAs
+// launch in (e.g. early, under PDL). They only move work, never change what is
+// computed.
 int calibrate(td_context* ctx, int64_t n_q) {
     SplitPlan p;
     std::string msg;
@@ -348,6 +363,22 @@ int calibrate(td_context* ctx, int64_t n_q) {
                                                  : w[size_t(c)];
     }
     ctx->cal_w = w;
+    // SM affinity from the last round's stamps (dbg[2048 + c] = %smid of CTA c)
+    std::vector<int> m(1024, -1);
+    bool ok = true;
+    for (int c = 0; c < G && ok; ++c) {
+        const unsigned long long sm = st[2048 + size_t(c)];
+        if (c >= 1024 || sm >= 1024 || m[size_t(sm)] != -1) ok = false;
+        else m[size_t(sm)] = c;
+    }
+    ctx->sm_map_ok = false;
+    if (ok) {
+        TD_CUDA(ctx->sm_map.ensure(m.size() * sizeof(int)));
+        TD_CUDA(cudaMemcpy(ctx->sm_map.p, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice));
+        TD_CUDA(ctx->claims.ensure(size_t(G) * sizeof(unsigned)));
+        TD_CUDA(cudaMemset(ctx->claims.p, 0, size_t(G) * sizeof(unsigned)));
+        ctx->sm_map_ok = true;
+    }
     return TD_OK;
 }
 
@@ -364,8 +395,15 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
         if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
             if (calibrate(ctx, n_q) != TD_OK) ctx->cal_failed = true;  // keep the equal split
         }
-        if (ctx->cal_w.size() == size_t(plan.ctas))
+        if (ctx->cal_w.size() == size_t(plan.ctas)) {
             if (int rc = apply_partition(ctx, plan)) return rc;
+            if (ctx->sm_map_ok && sm_affinity_enabled()) {
+                plan.sm_to_cta = static_cast<const int*>(ctx->sm_map.p);
+                plan.claims = static_cast<unsigned*>(ctx->claims.p);
+                if (++ctx->claim_epoch == 0) ++ctx->claim_epoch;  // 0 marks "never claimed"
+                plan.epoch = ctx->claim_epoch;
+            }
+        }
     }
     TD_CUDA(ctx->ws.ensure(plan.workspace_bytes()));
     if (plan.pool_tiles > 0) {
@@ -633,6 +671,9 @@ int td_destroy(td_context* ctx) {
     ctx->x_err.release();
     ctx->ctr.release();
     ctx->dbg.release();
+    ctx->tlbuf.release();
+    ctx->sm_map.release();
+    ctx->claims.release();
     ctx->cal_q.release();
     for (auto& tb : ctx->tabs) tb.buf.release();
     cudaStreamDestroy(ctx->stream);
@@ -896,7 +937,30 @@ int td_kv_pointers(td_context* ctx, void** k, void** v) {
     return TD_OK;
 }
 
+// TD_DEBUG_TIMELINE=1: every decode call stamps [K1 first start, first CTA past
+// the PDL wait, K1 last end, K2 last done] into dbg[5000 + 4 * (call % 286)],
+// without any extra operation on the stream (see scripts/timeline_probe.py).
+static int timeline_step(td_context* ctx) {
+    static const bool on = [] { const char* e = std::getenv("TD_DEBUG_TIMELINE"); return e && std::atoi(e) != 0; }();
+    if (!on) {
+        td::set_timeline(nullptr);
+        return TD_OK;
+    }
+    if (ctx->tl_count < 0) {
+        std::vector<unsigned long long> init(6144 - 5000);
+        for (size_t i = 0; i < init.size(); ++i) init[i] = (i % 4) < 2 ? ~0ull : 0ull;
+        TD_CUDA(ctx->tlbuf.ensure(init.size() * sizeof(unsigned long long)));
+        TD_CUDA(cudaMemcpy(ctx->tlbuf.p, init.data(), init.size() * sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice));
+        ctx->tl_count = 0;
+    }
+    td::set_timeline(static_cast<unsigned long long*>(ctx->tlbuf.p) + 4 * (ctx->tl_count % 286));
+    ++ctx->tl_count;
+    return TD_OK;
+}
+
 static int debug_begin(td_context* ctx, int flags) {
+    if (int rc = timeline_step(ctx)) return rc;
     if (!(flags & TD_DEBUG_TS)) {
         td::set_debug_stamps(nullptr);
         return TD_OK;
@@ -910,10 +974,14 @@ static int debug_begin(td_context* ctx, int flags) {
 
 int td_debug_stamps(td_context* ctx, unsigned long long* out, int n) {
     if (int rc = require_ctx(ctx)) return rc;
-    if (!ctx->dbg.p) return set_err(TD_ESTATE, "no TD_DEBUG_TS call made");
+    if (!ctx->dbg.p && !ctx->tlbuf.p) return set_err(TD_ESTATE, "no TD_DEBUG_TS call made");
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
-    TD_CUDA(cudaMemcpy(out, ctx->dbg.p, sizeof(unsigned long long) * size_t(std::min(n, 6144)),
-                       cudaMemcpyDeviceToHost));
+    if (ctx->dbg.p)
+        TD_CUDA(cudaMemcpy(out, ctx->dbg.p, sizeof(unsigned long long) * size_t(std::min(n, 6144)),
+                           cudaMemcpyDeviceToHost));
+    if (ctx->tlbuf.p && n > 5000)
+        TD_CUDA(cudaMemcpy(out + 5000, ctx->tlbuf.p, sizeof(unsigned long long) * size_t(std::min(n, 6144) - 5000),
+                           cudaMemcpyDeviceToHost));
     return TD_OK;
 }
 
@@ -985,8 +1053,11 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
             e0 = pr[0];
             e1 = pr[1];
         }
+        unsigned long long* dbg = (flags & TD_DEBUG_TS) ? static_cast<unsigned long long*>(ctx->dbg.p) : nullptr;
+        if (dbg) TD_CUDA(td::launch_stamp(dbg + 2, ctx->stream));
         TD_CUDA(td::launch_decode_final(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                         ctx->ws.p, dst, ctx->stream, e0, e1));
+        if (dbg) TD_CUDA(td::launch_stamp(dbg + 3, ctx->stream));
         phase_mark(ctx);
         ctx->last_kernels = 2;  // K1 + K2
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *

@@ -41,6 +41,13 @@ struct SplitPlan {
     // build_partition): CTA c owns static tiles [x_table[c], x_table[c+1])
     const int64_t* x_table = nullptr;
     const int* bh_table = nullptr;
+    // SM affinity of the calibrated partition (optional): the CTA on SM s takes
+    // index sm_to_cta[s] (claimed with claims[c] = epoch; a CTA whose SM is
+    // already taken in this launch takes the next free index), so CTA c runs
+    // where its speed weight was measured whatever order the CTAs launch in
+    const int* sm_to_cta = nullptr;
+    unsigned* claims = nullptr;
+    unsigned epoch = 0;
     int64_t slots() const { return int64_t(ctas) * slot_warps * maxseg; }
     // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32),
     // then the per-CTA merged states [ctas * maxseg][group] (+ [..][d])
@@ -53,6 +60,10 @@ struct SplitPlan {
 // TD_DEBUG_TS: kernels write %globaltimer stamps into buf (nullptr = off):
 // [0] min K1 CTA start, [1] max K1 CTA end, [8 + 8*blk + k] K2 block stages.
 void set_debug_stamps(unsigned long long* buf);
+// TD_DEBUG_TIMELINE: per-step slot of 4 stamps (nullptr = off), see K1Args::tl.
+void set_timeline(unsigned long long* slot);
+// TD_DEBUG_TS: a one-thread kernel writing %globaltimer to *p (front-end gaps).
+cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
 
 // Chooses the kernel and grid for a shard. Returns false (with msg) when the
 // shape is unsupported.

@@ -72,6 +72,8 @@ struct K1Args {
     float* cslot_l;
     float* cslot_o; // [ctas * maxseg][group][d]
     unsigned long long* dbg;  // optional globaltimer stamps (TD_DEBUG_TS)
+    unsigned long long* tl;   // optional per-step timeline (TD_DEBUG_TIMELINE): [K1 first start,
+                              // first CTA past the PDL wait, K1 last end, K2 last done]
     int reverse;              // debug: CTA c takes range ctas-1-c (TD_DEBUG_REVERSE)
     // dynamic "home" pool (k1_bf16): tiles [pool_first, pool_first + pool_tiles)
     // of every bh are handed out at run time in chunks of pool_chunk tiles to
@@ -87,6 +89,9 @@ struct K1Args {
     // CTA covering bh and bh's segment index in the first one
     const int64_t* x_table;
     const int* bh_table;
+    const int* sm_to_cta;     // SM affinity of the calibrated partition (SplitPlan)
+    unsigned* claims;
+    unsigned epoch;
     Tail tail;
 };
 
@@ -157,6 +162,28 @@ __device__ void cta_merge(const K1Args& a, int c, float* sm) {
     }
 }
 
+// Logical CTA index: blockIdx, or -- with a calibrated partition -- the index
+// calibrated on this SM (SplitPlan::sm_to_cta), claimed for this launch; a CTA
+// whose SM already hosts one of this grid's CTAs takes the next free index.
+__device__ __forceinline__ int cta_index(const K1Args& a) {
+    if (!a.sm_to_cta) return (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    __shared__ int s_c;
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        int c0 = smid < 1024 ? a.sm_to_cta[smid] : -1;
+        if (c0 < 0 || c0 >= a.ctas) c0 = static_cast<int>(blockIdx.x);
+        int cc = c0;
+        for (int k = 0; k < a.ctas; ++k) {
+            cc = c0 + k < a.ctas ? c0 + k : c0 + k - a.ctas;
+            if (atomicExch(a.claims + cc, a.epoch) != a.epoch) break;
+        }
+        s_c = cc;
+    }
+    __syncthreads();
+    return s_c;
+}
+
 // =========================================================================
 // K1, bf16: tokens on M (16 per m-tile), heads on N (8), d on K.
 // S^T[tok][head] = K[tok][:] . Q[head][:]   (A = K via ldmatrix, B = Q^T regs)
@@ -182,12 +209,12 @@ __global__ void __launch_bounds__(W * 32, 1)
     __shared__ int st_rec[W][S];                   // -1: static tile, else pool record
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
-    const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
+    const unsigned long long t_start = (a.dbg || a.tl) ? gtimer() : 0ull;
     // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int c = cta_index(a);
     const int64_t A = a.tiles_per_bh;  // static tiles per bh (the pool holds the rest)
     const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
     const int64_t x1 = a.x_table ? a.x_table[c + 1] : cta_begin(a.total_tiles, c + 1, a.ctas);
@@ -279,6 +306,13 @@ __global__ void __launch_bounds__(W * 32, 1)
         }
         __syncwarp();
     };
+    // this grid is itself a programmatic dependent (launch_pdl): q, K, V, the
+    // workspace and the pool counters only after the preceding kernel is done
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.tl && threadIdx.x == 0) {
+        atomicMin(a.tl + 0, t_start);
+        atomicMin(a.tl + 1, gtimer());
+    }
     for (int s = 0; s < S; ++s) refill(s);
 
     const int hA = 2 * (lane & 3), hB = hA + 1;  // this lane's heads (N columns)
@@ -482,6 +516,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncthreads();
     if (phases == 2) cta_merge<2 * W>(a, c, reinterpret_cast<float*>(smem));
     else cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    if (a.tl && threadIdx.x == 0) atomicMax(a.tl + 2, gtimer());
     if (a.dbg && threadIdx.x == 0) {
         const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
@@ -532,6 +567,8 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         mbar_fence_init();
     }
     __syncwarp();
+    // this grid is itself a programmatic dependent: inputs only after the wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int64_t kk, int s) {
         const int64_t x = x0 + warp + kk * W;
@@ -702,11 +739,12 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
     constexpr int T = 32;
     constexpr int W = 4;
     extern __shared__ float gen_smem[];
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
     // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // this grid is itself a programmatic dependent: inputs only after the wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = (a.reverse & 1) ? a.ctas - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const int64_t x0 = a.x_table ? a.x_table[c] : cta_begin(a.total_tiles, c, a.ctas);
@@ -954,6 +992,7 @@ __device__ __forceinline__ int64_t out_row_of(const K1Args& a, int64_t r) {
 template <int V, int NC, int BO>
 __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     const unsigned long long t_pre = a.dbg ? gtimer() : 0ull;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
     const int64_t rows = a.bh_count * a.group;
     const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -984,6 +1023,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
         }
     }
     if (ts) ts[4] = gtimer();
+    if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
 }
 
 // =========================================================================
@@ -1027,6 +1067,7 @@ __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
 
 template <int V, int NC, int BO>
 __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
     const int64_t rows = a.bh_count * a.group;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -1156,6 +1197,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
             }
     }
     if (ts) ts[4] = gtimer();
+    if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
 }
 
 // =========================================================================
@@ -1270,11 +1312,13 @@ size_t bf16_smem() {
 size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 * 4 + 128; }
 
 unsigned long long* g_dbg = nullptr;  // set by set_debug_stamps
+unsigned long long* g_tl = nullptr;   // set by set_timeline
 
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
     K1Args a{};
     a.dbg = g_dbg;
+    a.tl = g_tl;
     static const int rev = [] { const char* e = std::getenv("TD_DEBUG_REVERSE"); return e ? std::atoi(e) : 0; }();
     a.reverse = rev;
     a.q = q;
@@ -1307,6 +1351,9 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.pool_chunk = p.pool_chunk;
     a.slot_warps = p.slot_warps;
     a.x_table = p.x_table;
+    a.sm_to_cta = p.sm_to_cta;
+    a.claims = p.claims;
+    a.epoch = p.epoch;
     a.bh_table = p.bh_table;
     if (p.pool_tiles > 0) {
         unsigned* cnt = p.counters;  // [2 parities][bh_count]
@@ -1333,9 +1380,36 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return e;
 }
 
+// Kernels sharing the stream with K1 ask for K1's shared-memory carveout, so an
+// SM never has to be reconfigured (drained) between K1 and its neighbours.
+template <typename K>
+cudaError_t prefer_max_smem(K kernel) {
+    static const bool on = [] { const char* e = std::getenv("TD_CARVEOUT"); return !e || std::atoi(e) != 0; }();
+    if (!on) return cudaSuccess;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, bool> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    bool& d = done[{reinterpret_cast<const void*>(kernel), dev}];
+    if (d) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) d = true;
+    return e;
+}
+
 }  // namespace
 
 void set_debug_stamps(unsigned long long* buf) { g_dbg = buf; }
+void set_timeline(unsigned long long* slot) { g_tl = slot; }
+
+__global__ void k_stamp(unsigned long long* p) { *p = gtimer(); }
+cudaError_t launch_stamp(unsigned long long* p, cudaStream_t st) {
+    prefer_max_smem(k_stamp);
+    k_stamp<<<1, 1, 0, st>>>(p);
+    return cudaGetLastError();
+}
 
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
                 SplitPlan& p, std::string& msg, bool allow_pool) {
@@ -1477,6 +1551,26 @@ bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, in
 
 namespace {
 
+// K1 is launched as a programmatic dependent of whatever kernel precedes it on
+// the stream (typically the previous step's K2): its CTAs get resident while
+// that kernel drains and wait in griddepcontrol.wait before touching any input,
+// so the ~3-5 us kernel-to-kernel launch gap leaves the critical path.
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    static const bool on = [] { const char* e = std::getenv("TD_K1_PDL"); return !e || std::atoi(e) != 0; }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(block));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // One K1 launch (any variant) with the tail configured in a.
 cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tmk,
                       const CUtensorMap* tmv, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
@@ -1490,7 +1584,7 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
         auto kern = k1_bf16<DD, kBf16Tile, bf16_warps(DD), bf16_stages(DD)>;                \
         const size_t sm = bf16_smem<DD>();                                                  \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;                              \
-        kern<<<p.ctas, bf16_warps(DD) * 32, sm, st>>>(a, *tmk, *tmv);                       \
+        if ((e = launch_pdl(kern, p.ctas, bf16_warps(DD) * 32, sm, st, a, *tmk, *tmv)) != cudaSuccess) return e; \
         break;                                                                              \
     }
             TD_LAUNCH_BF16(64)
@@ -1506,7 +1600,7 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
     case GG: {                                                              \
         auto kern = k1_f32<kF32Tile, kF32Warps, kF32Stages, GG>;            \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;              \
-        kern<<<p.ctas, kF32Warps * 32, sm, st>>>(a);                        \
+        if ((e = launch_pdl(kern, p.ctas, kF32Warps * 32, sm, st, a)) != cudaSuccess) return e; \
         break;                                                              \
     }
             TD_LAUNCH_F32(1)
@@ -1518,10 +1612,10 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
         size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
         if (p.dtype == kBF16) {
             if ((e = set_smem(k1_generic<__nv_bfloat16>, sm)) != cudaSuccess) return e;
-            k1_generic<__nv_bfloat16><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
+            if ((e = launch_pdl(k1_generic<__nv_bfloat16>, p.ctas, kGenWarps * 32, sm, st, a)) != cudaSuccess) return e;
         } else {
             if ((e = set_smem(k1_generic<float>, sm)) != cudaSuccess) return e;
-            k1_generic<float><<<p.ctas, kGenWarps * 32, sm, st>>>(a);
+            if ((e = launch_pdl(k1_generic<float>, p.ctas, kGenWarps * 32, sm, st, a)) != cudaSuccess) return e;
         }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1547,6 +1641,8 @@ cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, bool exchange, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    cudaError_t e = exchange ? prefer_max_smem(k2_exchange<V, NC, BO>) : prefer_max_smem(k2_combine<V, NC, BO>);
+    if (e != cudaSuccess) return e;
     return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange<V, NC, BO>, a)
                     : cudaLaunchKernelEx(&cfg, k2_combine<V, NC, BO>, a);
 }

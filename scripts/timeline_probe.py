@@ -1,0 +1,46 @@
+#!/usr/bin/env python3
+"""Device timeline of back-to-back decode steps (TD_DEBUG_TIMELINE=1): per step
+the first K1 CTA start, the first CTA past K1's PDL wait, the last K1 CTA end
+and the last K2 warp done (globaltimer, no extra stream operations).
+  TD_DEBUG_TIMELINE=1 python scripts/timeline_probe.py [--seq-len N] [--steps K]"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seq-len", type=int, default=131072)
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2408_04093_b200 as td
+    w = td.Worker(0)
+    w.generate_kv(td.DType.Bf16, 1, 8, args.seq_len, 128, 2, 3)
+    q = td.seeded_tensor([1, 32, 128], 1, 1.0, td.DType.Bf16)
+    out = torch.empty(1, 32, 128, device="cuda")
+    for _ in range(args.steps):
+        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, 0)
+    torch.cuda.synchronize()
+    st = w.debug_stamps(6144)
+    rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(args.steps)]
+    t0 = rows[0][0]
+    us = lambda x: round((x - t0) / 1000.0, 2)  # noqa: E731
+    tl = [[us(x) for x in r] for r in rows]
+    gaps = [round(tl[i + 1][0] - tl[i][3], 2) for i in range(len(tl) - 1)]
+    waits = [round(tl[i + 1][1] - tl[i][3], 2) for i in range(len(tl) - 1)]
+    steps = [round(tl[i + 1][1] - tl[i][1], 2) for i in range(len(tl) - 1)]
+    print(json.dumps({"seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
+                      "k1_start_minus_prev_k2_done": gaps, "k1_past_wait_minus_prev_k2_done": waits,
+                      "step_period": steps, "k1_span": [round(r[2] - r[1], 2) for r in tl],
+                      "tail": [round(r[3] - r[2], 2) for r in tl]}))
+    w.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -49,7 +49,7 @@ def main():
         starts = sorted((st[4096 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4096 + 2 * c])
         blocks = [st[8 + 8 * i: 8 + 8 * i + 8] for i in range(64) if st[8 + 8 * i] != 0]
         rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
-        summary = {"k1_end": rel(st[1])}
+        summary = {"k1_end": rel(st[1]), "pre_k1_stamp": rel(st[2]), "post_k2_stamp": rel(st[3])}
         if ends:
             qt = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
             summary["cta_start_q"] = [qt(starts, f) for f in (0.0, 0.5, 1.0)]
