@@ -1021,6 +1021,8 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         xa.max_rows = ctx->x_max_rows;
         xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
         xa.error = static_cast<int*>(ctx->x_err.p);
+        static const int pull = [] { const char* e = std::getenv("TD_XCHG_PULL"); return e ? std::atoi(e) : 0; }();
+        xa.pull = pull;
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
         const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;

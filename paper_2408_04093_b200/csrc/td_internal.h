@@ -104,6 +104,7 @@ struct XchgArgs {
     int64_t max_rows = 0;
     int64_t max_blocks = 0;
     int* error = nullptr;
+    int pull = 0;  // see k2_exchange
 };
 constexpr int kXchgBlocks = 1024;
 

@@ -45,6 +45,7 @@ struct Xchg {
     unsigned epoch;
     int64_t max_rows;
     int* error;           // set on timeout
+    int pull;             // 0: push own rows into every peer's buffer; 1: write own buffer, read peers'
 };
 
 // What K2 does with the merged rows.
@@ -1065,6 +1066,7 @@ __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
     return __uint_as_float(v);
 }
 
+
 template <int V, int NC, int BO>
 __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
@@ -1098,7 +1100,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
         merge_row_warp<V, NC, BO>(a, r, r == w0 ? cv0 : cover_of(a, r / a.group), res, l, m);
         if (ts && r == w0) ts[2] = gtimer();
         const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
-        auto push = [&](uint2* dst) {
+        auto push = [&](uint2* dst) {  // LL words of this row into slot `rank` of one buffer
 #pragma unroll
             for (int c = 0; c < NC; ++c)
 #pragma unroll
@@ -1108,15 +1110,21 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
                 }
             if (lane == 0) st_ll(dst + D, l, x.epoch);
         };
+        if (x.pull) {
+            push(peers[x.rank] + off);  // own buffer only: the peers read it over NVLink
+        } else {
 #pragma unroll
-        for (int q = 0; q < PMAX; ++q)
-            if (q < x.p) push(pp[q] + off);
-        for (int q = PMAX; q < x.p; ++q) push(peers[q] + off);
+            for (int q = 0; q < PMAX; ++q)
+                if (q < x.p) push(pp[q] + off);
+            for (int q = PMAX; q < x.p; ++q) push(peers[q] + off);
+        }
     }
     if (ts) ts[1] = gtimer();
     for (int64_t r = w0; r < rows; r += nw) {  // exact combine of the p partials
         const int64_t orow = out_row_of(a, r);
-        const uint2* base = own + int64_t(par) * x.p * stride + orow * (D + 1);
+        // source k's words: push -- slot k of the own buffer; pull -- slot k of k's buffer
+        const int64_t roff = int64_t(par) * x.p * stride + orow * (D + 1);
+        const uint2* base = own + roff;
         // every word of the first PMAX sources (lse + this lane's columns) is polled in
         // one batch, and re-polled -- again as a batch -- until all carry this epoch
         uint2 wl[PMAX], wo[PMAX][NC][V];
@@ -1126,7 +1134,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
 #pragma unroll
             for (int k = 0; k < PMAX; ++k) {
                 if (k >= x.p) continue;
-                const uint2* slot = base + k * stride;
+                const uint2* slot = (x.pull ? pp[k] + roff : base) + k * stride;
                 wl[k] = ld_word(slot + D);
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
@@ -1157,7 +1165,8 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
 #pragma unroll
         for (int k = 0; k < PMAX; ++k)
             if (k < x.p) shift = fmaxf(shift, __uint_as_float(wl[k].x));
-        for (int q = PMAX; q < x.p; ++q) shift = fmaxf(shift, ld_ll(base + q * stride + D, x.epoch, x.error));
+        for (int q = PMAX; q < x.p; ++q)
+            shift = fmaxf(shift, ld_ll((x.pull ? peers[q] + roff : base) + q * stride + D, x.epoch, x.error));
         float num[NC][V];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
@@ -1175,7 +1184,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
                 for (int v = 0; v < V; ++v) num[c][v] += wgt * __uint_as_float(wo[k][c][v].x);
         }
         for (int q = PMAX; q < x.p; ++q) {  // beyond one NVLink domain: word by word
-            const uint2* slot = base + q * stride;
+            const uint2* slot = (x.pull ? peers[q] + roff : base) + q * stride;
             const float l = ld_ll(slot + D, x.epoch, x.error);
             const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - shift);
             den += wgt;
@@ -1701,6 +1710,7 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.x.epoch = xa.epoch;
     a.tail.x.max_rows = xa.max_rows;
     a.tail.x.error = xa.error;
+    a.tail.x.pull = xa.pull;
     cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
     if (e != cudaSuccess) return e;
     return launch_k2(a, xa.max_blocks, true, st);

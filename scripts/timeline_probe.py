@@ -18,28 +18,49 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     args = ap.parse_args()
     import torch
+    import torch.distributed as dist
 
     import paper_2408_04093_b200 as td
-    w = td.Worker(0)
+    from paper_2408_04093_b200 import _capi
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    flags = 0
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        w = td.Worker.from_torch_distributed(local)
+        w.enable_p2p(32, 128)
+        flags = _capi.TD_P2P
+    else:
+        w = td.Worker(local)
     w.generate_kv(td.DType.Bf16, 1, 8, args.seq_len, 128, 2, 3)
     q = td.seeded_tensor([1, 32, 128], 1, 1.0, td.DType.Bf16)
     out = torch.empty(1, 32, 128, device="cuda")
+    for _ in range(3):
+        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, flags)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     for _ in range(args.steps):
-        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, 0)
+        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, flags)
     torch.cuda.synchronize()
     st = w.debug_stamps(6144)
-    rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(args.steps)]
+    rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(3, 3 + args.steps)]
     t0 = rows[0][0]
     us = lambda x: round((x - t0) / 1000.0, 2)  # noqa: E731
     tl = [[us(x) for x in r] for r in rows]
     gaps = [round(tl[i + 1][0] - tl[i][3], 2) for i in range(len(tl) - 1)]
     waits = [round(tl[i + 1][1] - tl[i][3], 2) for i in range(len(tl) - 1)]
     steps = [round(tl[i + 1][1] - tl[i][1], 2) for i in range(len(tl) - 1)]
-    print(json.dumps({"seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
+    print(json.dumps({"rank": local, "world": world, "seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
+                      "abs_k1_start_us": [round(r[0] / 1000.0, 2) for r in rows],
                       "k1_start_minus_prev_k2_done": gaps, "k1_past_wait_minus_prev_k2_done": waits,
                       "step_period": steps, "k1_span": [round(r[2] - r[1], 2) for r in tl],
                       "tail": [round(r[3] - r[2], 2) for r in tl]}))
     w.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
