@@ -81,6 +81,10 @@ class Oracle:
                                         ctypes.c_int, ctypes.c_int, _c_double_p])
         lib.orc_attention_naive.argtypes = ([_c_double_p] * 3 + [_i64] * 5 + [ctypes.c_double, ctypes.c_int,
                                             ctypes.c_int, _c_double_p])
+        lib.orc_energy_forward_parallel.argtypes = ([_c_double_p] * 4 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int]
+                                                    + [_c_double_p] * 3)
+        lib.orc_energy_grad_parallel.argtypes = ([_c_double_p] * 5 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int,
+                                                 _c_double_p])
         self.lib = lib
 
     # -- numerics ---------------------------------------------------------
@@ -152,6 +156,33 @@ class Oracle:
             raise ValueError(f"ring_decode: invalid arguments (rc={rc})")
         return out
 
+    # -- energy formulation (energy.cpp:152-259) ---------------------------
+    def energy_forward_parallel(self, q, k, v, source, chunks, dtype=F64):
+        """q, source [b, h, nq, d] (source None: zero), k, v [b, h, n, d] ->
+        (value, row_max, shifted_lse), each [b, h, nq]."""
+        b, h, nq, d = q.shape
+        n = k.shape[2]
+        value, rmax, sh = (np.empty((b, h, nq)) for _ in range(3))
+        src = None if source is None else np.ascontiguousarray(source, dtype=np.float64)
+        rc = self.lib.orc_energy_forward_parallel(_dp(np.ascontiguousarray(q)), _dp(np.ascontiguousarray(k)),
+                                                  _dp(np.ascontiguousarray(v)), None if src is None else _dp(src),
+                                                  b, h, nq, n, d, chunks, dtype, _dp(value), _dp(rmax), _dp(sh))
+        if rc != 0:
+            raise ValueError("energy_forward_parallel: need 1 <= chunks <= N")
+        return value, rmax, sh
+
+    def energy_grad_parallel(self, q, k, v, row_max, shifted, chunks, dtype=F64):
+        b, h, nq, d = q.shape
+        n = k.shape[2]
+        grad = np.empty((b, h, nq, d))
+        rc = self.lib.orc_energy_grad_parallel(_dp(np.ascontiguousarray(q)), _dp(np.ascontiguousarray(k)),
+                                               _dp(np.ascontiguousarray(v)), _dp(np.ascontiguousarray(row_max)),
+                                               _dp(np.ascontiguousarray(shifted)), b, h, nq, n, d, chunks, dtype,
+                                               _dp(grad))
+        if rc != 0:
+            raise ValueError("energy_grad_parallel: need 1 <= chunks <= N")
+        return grad
+
     def attention_naive(self, q, k, v, scale=1.0, dtype=F64, nthreads=1):
         b, n_q, d = q.shape
         _, n_kv, seq, _ = k.shape
@@ -181,6 +212,10 @@ class Reference:
         lib.ref_prepare.restype = ctypes.c_void_p
         lib.ref_prepare.argtypes = [_c_double_p] * 3 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int]
         lib.ref_release.argtypes = [ctypes.c_void_p]
+        lib.ref_energy_forward_parallel.argtypes = ([_c_double_p] * 4 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int]
+                                                    + [_c_double_p] * 3)
+        lib.ref_energy_grad_parallel.argtypes = ([_c_double_p] * 6 + [_i64] * 5 + [ctypes.c_int, ctypes.c_int,
+                                                 _c_double_p])
         lib.ref_decode.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                    _i64, _i64, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p]
         self.lib = lib
@@ -233,6 +268,30 @@ class Reference:
         if not h:
             raise ValueError(self.error())
         return PreparedRef(self, h, b * n_q, d, (b, n_q, d))
+
+    def energy_forward_parallel(self, q, k, v, source, chunks, dtype=F64):
+        b, h, nq, d = q.shape
+        n = k.shape[2]
+        value, rmax, sh = (np.empty((b, h, nq)) for _ in range(3))
+        src = None if source is None else np.ascontiguousarray(source, dtype=np.float64)
+        rc = self.lib.ref_energy_forward_parallel(_dp(np.ascontiguousarray(q)), _dp(np.ascontiguousarray(k)),
+                                                  _dp(np.ascontiguousarray(v)), None if src is None else _dp(src),
+                                                  b, h, nq, n, d, chunks, dtype, _dp(value), _dp(rmax), _dp(sh))
+        if rc != 0:
+            raise ValueError(self.error())
+        return value, rmax, sh
+
+    def energy_grad_parallel(self, q, k, v, value, row_max, shifted, chunks, dtype=F64):
+        b, h, nq, d = q.shape
+        n = k.shape[2]
+        grad = np.empty((b, h, nq, d))
+        rc = self.lib.ref_energy_grad_parallel(_dp(np.ascontiguousarray(q)), _dp(np.ascontiguousarray(k)),
+                                               _dp(np.ascontiguousarray(v)), _dp(np.ascontiguousarray(value)),
+                                               _dp(np.ascontiguousarray(row_max)), _dp(np.ascontiguousarray(shifted)),
+                                               b, h, nq, n, d, chunks, dtype, _dp(grad))
+        if rc != 0:
+            raise ValueError(self.error())
+        return grad
 
     def tree_decode(self, q, k, v, p, strategy=HIER, scale=1.0, dtype=F64, parallel=False):
         with self.prepare(q, k, v, p, dtype) as pr:

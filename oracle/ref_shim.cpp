@@ -9,6 +9,7 @@
 // h / group -- rows of tree_decode are independent, so this equals one call.
 #include "treedec/attention.hpp"
 #include "treedec/decode.hpp"
+#include "treedec/energy.hpp"
 #include "treedec/numerics.hpp"
 
 #include <chrono>
@@ -105,6 +106,54 @@ int ref_chunk_partial(const double* q, const double* k, const double* v, std::in
         std::memcpy(row_max, part.row_max.data().data(), sizeof(double) * static_cast<std::size_t>(b * h));
         std::memcpy(lse, part.lse.data().data(), sizeof(double) * static_cast<std::size_t>(b * h));
         std::memcpy(out, part.out.data().data(), sizeof(double) * static_cast<std::size_t>(b * h * d));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
+// energy_forward_parallel (energy.cpp:152-203): q, src [b,h,nq,d] (src may be
+// null: empty source), k, v [b,h,n,d]; value, row_max, shifted [b,h,nq].
+int ref_energy_forward_parallel(const double* q, const double* k, const double* v, const double* src,
+                                std::int64_t b, std::int64_t h, std::int64_t nq, std::int64_t n,
+                                std::int64_t d, int chunks, int dtype, double* value, double* row_max,
+                                double* shifted) {
+    try {
+        const DType dt = to_dtype(dtype);
+        const Tensor tq({b, h, nq, d}, std::vector<double>(q, q + b * h * nq * d), dt);
+        const Tensor tk({b, h, n, d}, std::vector<double>(k, k + b * h * n * d), dt);
+        const Tensor tv({b, h, n, d}, std::vector<double>(v, v + b * h * n * d), dt);
+        const Tensor ts = src ? Tensor({b, h, nq, d}, std::vector<double>(src, src + b * h * nq * d), dt) : Tensor{};
+        const EnergyEval e = energy_forward_parallel(tq, tk, tv, ts, chunks);
+        const std::size_t rows = static_cast<std::size_t>(b * h * nq);
+        std::memcpy(value, e.value.data().data(), sizeof(double) * rows);
+        std::memcpy(row_max, e.row_max.data().data(), sizeof(double) * rows);
+        std::memcpy(shifted, e.shifted_lse.data().data(), sizeof(double) * rows);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
+// energy_grad_parallel (energy.cpp:205-259) with saved (value, row_max, shifted).
+int ref_energy_grad_parallel(const double* q, const double* k, const double* v, const double* value,
+                             const double* row_max, const double* shifted, std::int64_t b, std::int64_t h,
+                             std::int64_t nq, std::int64_t n, std::int64_t d, int chunks, int dtype,
+                             double* grad) {
+    try {
+        const DType dt = to_dtype(dtype);
+        const DType sdt = stats_dtype(dt);
+        const Tensor tq({b, h, nq, d}, std::vector<double>(q, q + b * h * nq * d), dt);
+        const Tensor tk({b, h, n, d}, std::vector<double>(k, k + b * h * n * d), dt);
+        const Tensor tv({b, h, n, d}, std::vector<double>(v, v + b * h * n * d), dt);
+        const std::size_t rows = static_cast<std::size_t>(b * h * nq);
+        EnergyEval saved{Tensor::zeros({b, h, nq}, sdt), Tensor::zeros({b, h, nq}, sdt),
+                         Tensor::zeros({b, h, nq}, sdt)};
+        std::memcpy(saved.value.data().data(), value, sizeof(double) * rows);
+        std::memcpy(saved.row_max.data().data(), row_max, sizeof(double) * rows);
+        std::memcpy(saved.shifted_lse.data().data(), shifted, sizeof(double) * rows);
+        const Tensor g = energy_grad_parallel(tq, tk, tv, saved, chunks);
+        std::memcpy(grad, g.data().data(), sizeof(double) * rows * static_cast<std::size_t>(d));
         return 0;
     } catch (const std::exception& e) {
         return fail(e, -1);

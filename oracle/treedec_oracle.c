@@ -560,3 +560,147 @@ int orc_attention_naive(const double* q, const double* k, const double* v, int64
     free(l);
     return rc;
 }
+
+/* ---- energy.cpp: the energy formulation ------------------
+ * Layouts: q, source [b][h][nq][d]; k, v [b][h][n][d]; per-row stats [b][h][nq];
+ * grad [b][h][nq][d]. The reference requires k.extent(1) == q.extent(1): no GQA
+ * (energy.cpp:15-25). */
+
+/* energy_scores, energy.cpp:27-47: one dot per key, q.k then source.v into the
+ * same accumulator, rounded to dt once. */
+static void energy_scores(const double* q, const double* k, const double* v, const double* src,
+                          int64_t qo, int64_t kvrow0, int64_t k0, int64_t k1, int64_t d, int dtype,
+                          double* scores) {
+    for (int64_t i = k0; i < k1; ++i) {
+        double dot = 0.0;
+        const int64_t ko = (kvrow0 + i) * d;
+        for (int64_t j = 0; j < d; ++j) dot += q[qo + j] * k[ko + j];
+        if (src)
+            for (int64_t j = 0; j < d; ++j) dot += src[qo + j] * v[ko + j];
+        scores[i - k0] = orc_round(dot, dtype);
+    }
+}
+
+static void combine_max1(const double* a, const double* b, double* dst, int64_t width, const void* ctx) {
+    (void)ctx;
+    for (int64_t i = 0; i < width; ++i) dst[i] = a[i] > b[i] ? a[i] : b[i];
+}
+
+typedef struct {
+    int sdt;
+} sdt_ctx;
+
+/* energy.cpp:189-191: round(lse_combine(a, b), sdt) */
+static void combine_lse1(const double* a, const double* b, double* dst, int64_t width, const void* vctx) {
+    const sdt_ctx* c = (const sdt_ctx*)vctx;
+    for (int64_t i = 0; i < width; ++i) dst[i] = orc_round(orc_lse_combine(a[i], b[i]), c->sdt);
+}
+
+typedef struct {
+    int dtype;
+} dt_ctx;
+
+/* energy.cpp:244-249: elementwise round(a + b, dt) */
+static void combine_sum_dt(const double* a, const double* b, double* dst, int64_t width, const void* vctx) {
+    const dt_ctx* c = (const dt_ctx*)vctx;
+    for (int64_t i = 0; i < width; ++i) dst[i] = orc_round(a[i] + b[i], c->dtype);
+}
+
+/* tree_reduce (reduce.hpp:97-104): the reduce-only tree schedule
+ * (reduce.cpp:60-66); the result is participant 0's slot. */
+static void tree_reduce_slots(double* values, int participants, int64_t width, combine_fn f,
+                              const void* ctx) {
+    schedule_t s;
+    sched_init(&s, participants);
+    append_tree_reduce(&s, 0, participants, 1);
+    execute_schedule(&s, values, width, f, ctx);
+    sched_free(&s);
+}
+
+int orc_energy_forward_parallel(const double* q, const double* k, const double* v, const double* src,
+                                int64_t b, int64_t h, int64_t nq, int64_t n, int64_t d, int chunks,
+                                int dtype, double* value, double* row_max, double* shifted) {
+    if (chunks < 1 || chunks > n || b < 1 || h < 1 || nq < 0 || d < 1) return -1;
+    const int sdt = orc_stats_dtype(dtype);
+    int64_t* ext = (int64_t*)malloc(sizeof(int64_t) * (size_t)chunks);
+    orc_chunk_extents(n, chunks, ext);
+    double* scores = (double*)malloc(sizeof(double) * (size_t)n);
+    double* lmax = (double*)malloc(sizeof(double) * (size_t)chunks);
+    double* llse = (double*)malloc(sizeof(double) * (size_t)chunks);
+    sdt_ctx sc = {sdt};
+    for (int64_t ib = 0; ib < b; ++ib)
+        for (int64_t ih = 0; ih < h; ++ih)
+            for (int64_t iq = 0; iq < nq; ++iq) {
+                const int64_t r = (ib * h + ih) * nq + iq;
+                const int64_t qo = r * d, kvrow0 = (ib * h + ih) * n;
+                /* energy.cpp:169-180: all chunk scores, per-chunk maxima */
+                energy_scores(q, k, v, src, qo, kvrow0, 0, n, d, dtype, scores);
+                int64_t begin = 0;
+                for (int c = 0; c < chunks; ++c) {
+                    double m = NEG_INF;
+                    for (int64_t a = begin; a < begin + ext[c]; ++a) m = scores[a] > m ? scores[a] : m;
+                    lmax[c] = m;
+                    begin += ext[c];
+                }
+                tree_reduce_slots(lmax, chunks, 1, combine_max1, NULL); /* :181-183 */
+                const double m = lmax[0];
+                begin = 0;
+                for (int c = 0; c < chunks; ++c) { /* :185-193 */
+                    double sum = 0.0;
+                    for (int64_t a = begin; a < begin + ext[c]; ++a) {
+                        scores[a] = orc_round(scores[a] - m, dtype);
+                        sum += exp(scores[a]);
+                    }
+                    llse[c] = ext[c] == 0 ? NEG_INF : orc_round(log(sum), sdt);
+                    begin += ext[c];
+                }
+                tree_reduce_slots(llse, chunks, 1, combine_lse1, &sc); /* :194-198 */
+                row_max[r] = m;
+                shifted[r] = llse[0];
+                value[r] = orc_round(llse[0] + m, sdt); /* store into an sdt tensor */
+            }
+    free(ext);
+    free(scores);
+    free(lmax);
+    free(llse);
+    return 0;
+}
+
+int orc_energy_grad_parallel(const double* q, const double* k, const double* v, const double* row_max,
+                             const double* shifted, int64_t b, int64_t h, int64_t nq, int64_t n,
+                             int64_t d, int chunks, int dtype, double* grad) {
+    if (chunks < 1 || chunks > n || b < 1 || h < 1 || nq < 0 || d < 1) return -1;
+    const int sdt = orc_stats_dtype(dtype);
+    int64_t* ext = (int64_t*)malloc(sizeof(int64_t) * (size_t)chunks);
+    orc_chunk_extents(n, chunks, ext);
+    double* scores = (double*)malloc(sizeof(double) * (size_t)n);
+    double* acc = (double*)malloc(sizeof(double) * (size_t)(chunks * d));
+    dt_ctx dc = {dtype};
+    for (int64_t ib = 0; ib < b; ++ib)
+        for (int64_t ih = 0; ih < h; ++ih)
+            for (int64_t iq = 0; iq < nq; ++iq) {
+                const int64_t r = (ib * h + ih) * nq + iq;
+                const int64_t qo = r * d, kvrow0 = (ib * h + ih) * n;
+                const double m = row_max[r], sh = shifted[r];
+                energy_scores(q, k, v, NULL, qo, kvrow0, 0, n, d, dtype, scores);
+                int64_t begin = 0;
+                for (int c = 0; c < chunks; ++c) { /* energy.cpp:232-243 */
+                    double* ac = acc + (size_t)c * (size_t)d;
+                    for (int64_t j = 0; j < d; ++j) ac[j] = 0.0;
+                    for (int64_t a = begin; a < begin + ext[c]; ++a) {
+                        const double rr = orc_round(scores[a] - m, dtype);
+                        const double w = orc_round(exp(rr - sh), sdt);
+                        const int64_t vo = (kvrow0 + a) * d;
+                        for (int64_t j = 0; j < d; ++j) ac[j] += w * v[vo + j];
+                    }
+                    for (int64_t j = 0; j < d; ++j) ac[j] = orc_round(ac[j], dtype);
+                    begin += ext[c];
+                }
+                tree_reduce_slots(acc, chunks, d, combine_sum_dt, &dc); /* :244-251 */
+                for (int64_t j = 0; j < d; ++j) grad[qo + j] = orc_round(acc[j], dtype);
+            }
+    free(ext);
+    free(scores);
+    free(acc);
+    return 0;
+}

@@ -101,6 +101,19 @@ int orc_attention_naive(const double* q, const double* k, const double* v, int64
                         int64_t n_q, int64_t n_kv, int64_t seq, int64_t d, double scale,
                         int dtype, int nthreads, double* out);
 
+/* energy_forward_parallel (energy.cpp:152-203): q, src [b][h][nq][d] (src may
+ * be NULL: zero source), k, v [b][h][n][d]; value, row_max, shifted [b][h][nq].
+ * Returns -1 unless 1 <= chunks <= n. */
+int orc_energy_forward_parallel(const double* q, const double* k, const double* v, const double* src,
+                                int64_t b, int64_t h, int64_t nq, int64_t n, int64_t d, int chunks,
+                                int dtype, double* value, double* row_max, double* shifted);
+
+/* energy_grad_parallel (energy.cpp:205-259) replaying a zero-source forward:
+ * grad [b][h][nq][d] = the attention output. */
+int orc_energy_grad_parallel(const double* q, const double* k, const double* v, const double* row_max,
+                             const double* shifted, int64_t b, int64_t h, int64_t nq, int64_t n,
+                             int64_t d, int chunks, int dtype, double* grad);
+
 #ifdef __cplusplus
 }
 #endif

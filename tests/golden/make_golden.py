@@ -14,6 +14,9 @@ Fixtures:
                      sweeps, measured GPU sweeps, hand-made edge and malformed
                      files) with the reference bench.cpp's re-emitted CSV/JSON,
                      report text and exit status (oracle/_ref/ref_bench_tool).
+  energy_cases.json  energy_forward_parallel / energy_grad_parallel
+                     (energy.cpp:152-259) outputs of the reference, with and
+                     without a source, every dtype and several chunk counts.
   decode_cases.json  small tree/ring decode problems (seeded inputs, the
                      reference seeding convention of test_decode.cpp:18-23)
                      with the reference's outputs at every dtype, strategy and
@@ -80,6 +83,29 @@ def decode_cases(ref: Reference, orc: Oracle):
                 for st_name, st in (("tree", TREE_BINARY), ("ring", RING), ("hier", HIER)):
                     entry["tree"][st_name] = hexarr(ref.tree_decode(q, k, v, p, st, 1.0, dt))
                 entry["ring"] = hexarr(ref.ring_decode(q, k, v, p, 1.0, dt))
+                cases.append(entry)
+    return cases
+
+
+def energy_cases(ref: Reference, orc: Oracle):
+    """Inputs q, k, v from seeds mix64(seed, 1..3); source from mix64(seed, 4)
+    at scale 0.5; shapes [b, h, nq, d] / [b, h, n, d]."""
+    cases = []
+    for seed, b, h, nq, n, d, chunks in [(31, 1, 2, 3, 17, 4, [1, 2, 5, 17]),
+                                          (32, 2, 1, 1, 64, 8, [1, 3, 8]),
+                                          (33, 1, 3, 2, 40, 16, [1, 4, 7])]:
+        for dt_name, dt in (("f64", F64), ("f32", F32), ("bf16", BF16)):
+            q = orc.seeded(orc.mix64(seed, 1), b * h * nq * d, dt).reshape(b, h, nq, d)
+            k = orc.seeded(orc.mix64(seed, 2), b * h * n * d, dt).reshape(b, h, n, d)
+            v = orc.seeded(orc.mix64(seed, 3), b * h * n * d, dt).reshape(b, h, n, d)
+            src = orc.seeded(orc.mix64(seed, 4), b * h * nq * d, dt, scale=0.5).reshape(b, h, nq, d)
+            for c in chunks:
+                entry = {"seed": seed, "b": b, "h": h, "nq": nq, "n": n, "d": d, "chunks": c, "dtype": dt_name}
+                for tag, s_ in (("zero", None), ("source", src)):
+                    val, rm, sh = ref.energy_forward_parallel(q, k, v, s_, c, dt)
+                    entry[tag] = {"value": hexarr(val), "row_max": hexarr(rm), "shifted": hexarr(sh)}
+                val, rm, sh = ref.energy_forward_parallel(q, k, v, None, c, dt)
+                entry["grad"] = hexarr(ref.energy_grad_parallel(q, k, v, val, rm, sh, c, dt))
                 cases.append(entry)
     return cases
 
@@ -173,6 +199,9 @@ def main():
     with open(os.path.join(HERE, "rng_vectors.json"), "w") as f:
         json.dump({"source": "reference seeded_random_tensor via oracle/_ref; triples from "
                              "proj/tests/data/rng_vectors.csv", "vectors": rng_vectors(ref)}, f, indent=0)
+    with open(os.path.join(HERE, "energy_cases.json"), "w") as f:
+        json.dump({"source": "reference energy_forward_parallel / energy_grad_parallel via oracle/_ref",
+                   "cases": energy_cases(ref, orc)}, f, separators=(",", ":"))
     with open(os.path.join(HERE, "decode_cases.json"), "w") as f:
         json.dump({"source": "reference tree_decode / ring_decode via oracle/_ref; inputs "
                              "q,k,v = seeded_random_tensor(shape, mix64(seed, 1|2|3), 1.0, dtype)",
