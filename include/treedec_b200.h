@@ -167,6 +167,40 @@ int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host);
 /* Reserves room for `tokens` more appended tokens on rank p-1 (no-op elsewhere). */
 int td_kv_reserve(td_context* ctx, int64_t tokens);
 
+/* ---- Energy formulation (energy.hpp:24-58) --------
+ * The attention energy of a query row is F = log sum_a exp(q.k_a + src.v_a)
+ * (no 1/sqrt(d) scale, like the reference); at src = 0 its gradient with
+ * respect to src is the attention output. Layouts: q, src [b][h][nq][d] (nq
+ * query rows per head), k, v [b][h][t][d] (MHA: the reference requires equal
+ * q and kv heads, energy.cpp:15-25). Stats are fp32, natural log.
+ *
+ * td_energy_partial: one key chunk -> per row (row_max, lse, out), out the
+ * softmax-weighted values. src may be NULL (zero source).
+ * td_energy_combine: energy_forward_parallel's reductions (energy.cpp:181-198)
+ * over P chunk partials ([P][rows]) -> value, row_max, shifted_lse.
+ * td_energy_grad_combine: energy_grad_parallel (energy.cpp:205-259) from P
+ * zero-source chunk partials and the saved forward: grad = sum_c
+ * e^(lse_c - row_max - shifted) out_c. */
+int td_energy_workspace_bytes(int dtype, int64_t b, int64_t h, int64_t nq, int64_t t, int64_t d,
+                              size_t* bytes);
+int td_energy_partial(int dtype, const void* q, const void* src, const void* k, const void* v,
+                      int64_t b, int64_t h, int64_t nq, int64_t t, int64_t d, float* row_max,
+                      float* lse, float* out, void* workspace, size_t workspace_bytes, void* stream);
+int td_energy_combine(int P, const float* row_max, const float* lse, int64_t rows, float* value,
+                      float* row_max_out, float* shifted, void* stream);
+int td_energy_grad_combine(int P, const float* lse, const float* out, const float* row_max,
+                           const float* shifted, int64_t rows, int64_t d, float* grad, void* stream);
+
+/* The paper's Alg. 1 / Alg. 2 across the ranks of a context (device pointers):
+ * td_energy_forward -- local (row_max, lse) of the placed shard, allreduce(max),
+ * e^(lse - max), allreduce(sum) -> value, row_max, shifted [b][h][nq];
+ * td_energy_grad -- with the saved forward, sum_a e^(s_a - F) v_a over the
+ * shard, allreduce(sum) -> grad [b][h][nq][d] (= the attention output). */
+int td_energy_forward(td_context* ctx, const void* q, const void* src, int64_t nq, float* value,
+                      float* row_max, float* shifted, int flags);
+int td_energy_grad(td_context* ctx, const void* q, int64_t nq, const float* row_max,
+                   const float* shifted, float* grad, int flags);
+
 /* Shard geometry of the placed cache. */
 int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes);
 /* Device pointers of the placed shard (for tests). */

@@ -24,6 +24,8 @@ EXPORTS = [
     "td_finalize", "td_create", "td_destroy", "td_stream", "td_comm_unique_id", "td_comm_init",
     "td_comm_info", "td_p2p_handle", "td_p2p_open", "td_p2p_status", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
     "td_kv_append", "td_kv_reserve",
+    "td_energy_workspace_bytes", "td_energy_partial", "td_energy_combine", "td_energy_grad_combine",
+    "td_energy_forward", "td_energy_grad",
     "td_tree_decode", "td_ring_decode", "td_local_partial", "td_output_bf16", "td_kernel_time",
     "td_reset_kernel_timer", "td_phase_times", "td_debug_stamps", "td_last_launch_stats", "td_memory_bytes",
 ]
@@ -91,6 +93,12 @@ def lib() -> ctypes.CDLL:
     L.td_kv_pointers.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
     L.td_kv_append.argtypes = [_vp, _vp, _vp, ctypes.c_int]
     L.td_kv_reserve.argtypes = [_vp, _i64]
+    L.td_energy_workspace_bytes.argtypes = [ctypes.c_int] + [_i64] * 5 + [ctypes.POINTER(ctypes.c_size_t)]
+    L.td_energy_partial.argtypes = [ctypes.c_int] + [_vp] * 4 + [_i64] * 5 + [_vp] * 4 + [ctypes.c_size_t, _vp]
+    L.td_energy_combine.argtypes = [ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.td_energy_grad_combine.argtypes = [ctypes.c_int] + [_vp] * 4 + [_i64, _i64, _vp, _vp]
+    L.td_energy_forward.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.c_int]
+    L.td_energy_grad.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, ctypes.c_int]
     L.td_tree_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_int, _vp, ctypes.c_int]
     L.td_ring_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, ctypes.c_int]
     L.td_local_partial.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, ctypes.c_int]

@@ -384,11 +384,12 @@ int calibrate(td_context* ctx, int64_t n_q) {
 
 // stride: tokens per bh row in memory (the placed shard's capacity; 0 for a
 // contiguous [bh][t][d] buffer such as a ring chunk)
-int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t stride) {
+int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t stride,
+             bool generic_only = false) {
     std::string msg;
     if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
     if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), t,
-                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det))
+                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det, generic_only))
         return set_err(TD_EINVAL, msg);
     plan.row_stride = stride;
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
@@ -583,6 +584,55 @@ int td_decode_partial(int dtype, const void* q, const void* k, const void* v, in
     }
     TD_CUDA(td::launch_decode_partial(plan, q, k, v, static_cast<float>(scale), &mk, &mv, workspace,
                                       row_max, lse, out, static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+// ---- energy formulation ----------------------------------
+int td_energy_workspace_bytes(int dtype, int64_t b, int64_t h, int64_t nq, int64_t t, int64_t d,
+                              size_t* bytes) {
+    SplitPlan plan;
+    std::string msg;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (nq < 1 || h < 1) return set_err(TD_EINVAL, "energy: need h >= 1 and nq >= 1");
+    if (!td::plan_split(dtype, b, static_cast<int>(h * nq), static_cast<int>(h), t, static_cast<int>(d),
+                        sm_count_of(dev), plan, msg, false, true))
+        return set_err(TD_EINVAL, msg);
+    *bytes = plan.workspace_bytes();
+    return TD_OK;
+}
+
+int td_energy_partial(int dtype, const void* q, const void* src, const void* k, const void* v, int64_t b,
+                      int64_t h, int64_t nq, int64_t t, int64_t d, float* row_max, float* lse, float* out,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+    SplitPlan plan;
+    std::string msg;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (nq < 1 || h < 1) return set_err(TD_EINVAL, "energy: need h >= 1 and nq >= 1");
+    // the nq query rows of head h are a GQA group of size nq over kv head h
+    if (!td::plan_split(dtype, b, static_cast<int>(h * nq), static_cast<int>(h), t, static_cast<int>(d),
+                        sm_count_of(dev), plan, msg, false, true))
+        return set_err(TD_EINVAL, msg);
+    if (workspace_bytes < plan.workspace_bytes()) return set_err(TD_EINVAL, "td_energy_partial: workspace too small");
+    TD_CUDA(td::launch_decode_partial(plan, q, k, v, 1.0f, nullptr, nullptr, workspace, row_max, lse, out,
+                                      static_cast<cudaStream_t>(stream), nullptr, nullptr, src));
+    return TD_OK;
+}
+
+int td_energy_combine(int P, const float* row_max, const float* lse, int64_t rows, float* value,
+                      float* row_max_out, float* shifted, void* stream) {
+    if (P < 1 || rows < 0) return set_err(TD_EINVAL, "energy_combine: no parts");
+    TD_CUDA(td::launch_energy_combine(P, row_max, lse, rows, value, row_max_out, shifted,
+                                      static_cast<cudaStream_t>(stream)));
+    return TD_OK;
+}
+
+int td_energy_grad_combine(int P, const float* lse, const float* out, const float* row_max,
+                           const float* shifted, int64_t rows, int64_t d, float* grad, void* stream) {
+    if (P < 1 || rows < 0 || d < 1) return set_err(TD_EINVAL, "energy_grad_combine: bad arguments");
+    TD_CUDA(td::launch_energy_grad_combine(P, lse, out, row_max, shifted, rows, static_cast<int>(d), grad,
+                                           static_cast<cudaStream_t>(stream)));
     return TD_OK;
 }
 
@@ -1123,6 +1173,65 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
         TD_CUDA(cudaMemcpyAsync(out, ctx->r_out, rows * d * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         TD_CUDA(cudaStreamSynchronize(ctx->stream));
     }
+    return TD_OK;
+}
+
+// Alg. 1 (energy_forward_parallel over the ranks' shards): local (row_max,
+// lse) of q.k + src.v -> allreduce(max) -> e^(lse - max) -> allreduce(sum) ->
+// shifted = log(sum), value = max + shifted. Device pointers; q, src
+// [b][h][nq][d] with h = the shard's kv heads.
+int td_energy_forward(td_context* ctx, const void* q, const void* src, int64_t nq, float* value,
+                      float* row_max, float* shifted, int flags) {
+    if (int rc = require_ctx(ctx)) return rc;
+    (void)flags;
+    ctx->det = g_deterministic != 0;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "energy_forward: no KV shard placed");
+    if (nq < 1) return set_err(TD_EINVAL, "energy_forward: need nq >= 1");
+    if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "energy_forward: more workers than keys");
+    const int64_t n_q = ctx->n_kv * nq, rows = ctx->b * n_q, d = ctx->d;
+    if (int rc = ensure_rows(ctx, rows, d)) return rc;
+    SplitPlan plan;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap, true)) return rc;
+    TD_CUDA(td::launch_decode_partial(plan, q, ctx->k.p, ctx->v.p, 1.0f, nullptr, nullptr, ctx->ws.p, ctx->r_max,
+                                      ctx->r_lse, ctx->out_local, ctx->stream, nullptr, nullptr, src));
+    if (ctx->nranks == 1) {
+        TD_CUDA(td::launch_energy_combine(1, ctx->r_max, ctx->r_lse, rows, value, row_max, shifted, ctx->stream));
+        ctx->last_kernels = 3;
+        return TD_OK;
+    }
+    TD_NCCL(nccl().AllReduce(ctx->r_max, ctx->shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm, ctx->stream));
+    TD_CUDA(td::launch_energy_shift(ctx->r_lse, ctx->shift, rows, ctx->lse, ctx->stream));
+    TD_NCCL(nccl().AllReduce(ctx->lse, ctx->lse, size_t(rows), ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+    TD_CUDA(td::launch_energy_finish(ctx->shift, ctx->lse, rows, value, row_max, shifted, ctx->stream));
+    ctx->last_kernels = 4;
+    return TD_OK;
+}
+
+// Alg. 2 (energy_grad_parallel): with the saved forward F = row_max + shifted,
+// each rank's sum_a e^(s_a - F) v_a over its shard, then one allreduce(sum).
+// No source (the gradient at zero source is the attention output).
+int td_energy_grad(td_context* ctx, const void* q, int64_t nq, const float* row_max, const float* shifted,
+                   float* grad, int flags) {
+    if (int rc = require_ctx(ctx)) return rc;
+    (void)flags;
+    ctx->det = g_deterministic != 0;
+    if (!ctx->kv_ok) return set_err(TD_ESTATE, "energy_grad: no KV shard placed");
+    if (nq < 1) return set_err(TD_EINVAL, "energy_grad: need nq >= 1");
+    if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "energy_grad: more workers than keys");
+    const int64_t n_q = ctx->n_kv * nq, rows = ctx->b * n_q, d = ctx->d;
+    if (int rc = ensure_rows(ctx, rows, d)) return rc;
+    SplitPlan plan;
+    if (int rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap, true)) return rc;
+    TD_CUDA(td::launch_decode_partial(plan, q, ctx->k.p, ctx->v.p, 1.0f, nullptr, nullptr, ctx->ws.p, ctx->r_max,
+                                      ctx->r_lse, ctx->out_local, ctx->stream));
+    TD_CUDA(td::launch_energy_logz(row_max, shifted, rows, ctx->shift, ctx->stream));
+    // n = out * e^(lse - F): the partial_to_numerator kernel with shift F
+    TD_CUDA(td::launch_to_numerator(ctx->r_lse, ctx->out_local, ctx->shift, rows, static_cast<int>(d), ctx->nd,
+                                    ctx->stream));
+    if (ctx->nranks > 1)
+        TD_NCCL(nccl().AllReduce(ctx->nd, ctx->nd, size_t(rows * d), ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+    TD_CUDA(cudaMemcpyAsync(grad, ctx->nd, size_t(rows * d) * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->last_kernels = 4;
     return TD_OK;
 }
 

@@ -68,8 +68,9 @@ cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
 // Chooses the kernel and grid for a shard. Returns false (with msg) when the
 // shape is unsupported.
 // allow_pool = false gives a static split: bitwise-reproducible results.
+// generic_only forces k1_generic (needed for an energy source term).
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& plan, std::string& msg, bool allow_pool = true);
+                SplitPlan& plan, std::string& msg, bool allow_pool = true, bool generic_only = false);
 
 // Static partition proportional to per-CTA speeds (weights[c] > 0, size
 // plan.ctas): x[c] = first static tile of CTA c (x has ctas + 1 entries),
@@ -84,7 +85,8 @@ cudaError_t launch_decode_partial(const SplitPlan& plan, const void* q, const vo
                                   const void* v, float scale, const CUtensorMap* tmk,
                                   const CUtensorMap* tmv, void* workspace, float* row_max,
                                   float* lse, float* out, cudaStream_t stream,
-                                  cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+                                  cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr,
+                                  const void* src = nullptr);
 
 // K1 with the final-output tail (p = 1: the local partial is the answer).
 cudaError_t launch_decode_final(const SplitPlan& plan, const void* q, const void* k, const void* v,
@@ -138,6 +140,16 @@ cudaError_t launch_combine_partials(int P, const float* lse, const float* out, i
 cudaError_t launch_seeded_fill(int dtype, void* dst, uint64_t seed, double scale,
                                int64_t bh_count, int64_t seq, int64_t start, int64_t len,
                                int64_t d, cudaStream_t stream);
-// Casts host-visible f32 to bf16 etc. are not needed on the hot path.
+// Energy formulation (energy.cpp:152-259), see td_kernels.cu.
+cudaError_t launch_energy_combine(int P, const float* rmax, const float* lse, int64_t rows, float* value,
+                                  float* rmax_out, float* shifted, cudaStream_t stream);
+cudaError_t launch_energy_grad_combine(int P, const float* lse, const float* out, const float* rmax,
+                                       const float* shifted, int64_t rows, int d, float* grad,
+                                       cudaStream_t stream);
+cudaError_t launch_energy_shift(const float* lse, const float* m, int64_t rows, float* x, cudaStream_t stream);
+cudaError_t launch_energy_finish(const float* m, const float* s, int64_t rows, float* value, float* rmax_out,
+                                 float* shifted, cudaStream_t stream);
+cudaError_t launch_energy_logz(const float* rmax, const float* shifted, int64_t rows, float* f,
+                               cudaStream_t stream);
 
 }  // namespace td

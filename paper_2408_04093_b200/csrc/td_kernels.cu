@@ -60,6 +60,7 @@ struct Tail {
 
 struct K1Args {
     const void* q;  // [b][n_q][d], kv dtype
+    const void* src;  // optional energy source, q's layout: score += src . v (k1_generic)
     const void* k;  // [bh][t][d]
     const void* v;
     int64_t bh_count, t, tiles_per_bh, total_tiles;
@@ -765,6 +766,7 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
         int64_t cur_bh = -1;
         uint32_t flushed = 0;
         const TIn* qrow = nullptr;
+        const TIn* srow = nullptr;
         auto flush = [&](int seg) {
             float lt = l;
             for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
@@ -793,16 +795,25 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
                 cur_bh = bh;
                 const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
                 qrow = q + (b * a.n_q + kvh * a.group + h) * int64_t(D);
+                if (a.src) srow = static_cast<const TIn*>(a.src) + (b * a.n_q + kvh * a.group + h) * int64_t(D);
             }
             const int64_t rem = a.t - tok0;
             const int nvalid = rem < T ? static_cast<int>(rem) : T;
             const int64_t row0 = bh * a.row_stride + tok0;
             float s = -CUDART_INF_F;
             if (lane < nvalid) {
+                // fp32 inputs: the dot in double, so the score carries only the
+                // fp32 rounding of the reference's Float32 mode (energy stats are
+                // log-domain values judged to 1e-5 absolute)
+                using Acc = typename std::conditional<std::is_same<TIn, float>::value, double, float>::type;
                 const TIn* kr = kg + (row0 + lane) * D;
-                float acc = 0.f;
-                for (int j = 0; j < D; ++j) acc += to_f(qrow[j]) * to_f(kr[j]);
-                s = acc * a.scale_log2;
+                Acc acc = 0;
+                for (int j = 0; j < D; ++j) acc += Acc(to_f(qrow[j])) * Acc(to_f(kr[j]));
+                if (srow) {  // energy source (energy.cpp:27-47): + source . v_a
+                    const TIn* vr = vg + (row0 + lane) * D;
+                    for (int j = 0; j < D; ++j) acc += Acc(to_f(srow[j])) * Acc(to_f(vr[j]));
+                }
+                s = static_cast<float>(acc) * a.scale_log2;
             }
             float mx = s;
             for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
@@ -1421,7 +1432,7 @@ cudaError_t launch_stamp(unsigned long long* p, cudaStream_t st) {
 }
 
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& p, std::string& msg, bool allow_pool) {
+                SplitPlan& p, std::string& msg, bool allow_pool, bool generic_only) {
     if (b < 1 || n_q < 1 || n_kv < 1 || d < 1 || t < 0) {
         msg = "decode: dimensions must be positive";
         return false;
@@ -1446,9 +1457,9 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     p.n_q = n_q;
     p.n_kv = n_kv;
     p.group = n_q / n_kv;
-    const bool mma_ok = dtype == kBF16 && (d == 64 || d == 128 || d == 256) && p.group <= 8 &&
+    const bool mma_ok = !generic_only && dtype == kBF16 && (d == 64 || d == 128 || d == 256) && p.group <= 8 &&
                         p.bh_count * t < (int64_t(1) << 31);
-    const bool f32_ok = dtype == kF32 && d == 128 && (p.group == 1 || p.group == 2);
+    const bool f32_ok = !generic_only && dtype == kF32 && d == 128 && (p.group == 1 || p.group == 2);
     if (mma_ok) {
         p.kernel = 1;
         p.tile = kBf16Tile;
@@ -1672,8 +1683,10 @@ cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void*
                                   const void* v, float scale, const CUtensorMap* tmk,
                                   const CUtensorMap* tmv, void* ws, float* row_max, float* lse,
                                   float* out, cudaStream_t st, cudaEvent_t ev0,
-                                  cudaEvent_t ev1) {
+                                  cudaEvent_t ev1, const void* src) {
+    if (src && p.kernel != 0) return cudaErrorInvalidValue;  // the source term lives in k1_generic
     K1Args a = make_args(p, q, k, v, scale, ws);
+    a.src = src;
     a.tail.mode = kTailPartial;
     a.tail.row_max = row_max;
     a.tail.lse = lse;
@@ -1764,6 +1777,93 @@ cudaError_t launch_combine_partials(int P, const float* lse, const float* out, i
     if (rows < 1) return cudaSuccess;
     k_combine_partials<<<static_cast<unsigned>(rows), 128, 0, st>>>(P, lse, out, rows, d, result,
                                                                      bad_row);
+    return cudaGetLastError();
+}
+
+// ---- energy formulation (energy.cpp:152-259) -------------
+// Per row, from P partials (row_max, lse natural log) of disjoint key chunks:
+// row_max = max_c row_max_c, shifted = log sum_c e^(lse_c - row_max), value =
+// row_max + shifted -- the tree max and lse reductions of
+// energy_forward_parallel. Empty rows give (-inf, -inf, -inf).
+__global__ void k_energy_combine(int P, const float* rmax, const float* lse, int64_t rows, float* value,
+                                 float* rmax_out, float* shifted) {
+    const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (r >= rows) return;
+    float m = -CUDART_INF_F;
+    for (int c = 0; c < P; ++c) m = fmaxf(m, rmax[c * rows + r]);
+    float s = 0.f;
+    if (m != -CUDART_INF_F)
+        for (int c = 0; c < P; ++c) {
+            const float l = lse[c * rows + r];
+            if (l != -CUDART_INF_F) s += expf(l - m);
+        }
+    const float sh = m == -CUDART_INF_F ? -CUDART_INF_F : logf(s);
+    rmax_out[r] = m;
+    shifted[r] = sh;
+    value[r] = m == -CUDART_INF_F ? -CUDART_INF_F : m + sh;
+}
+
+// grad = sum_c e^(lse_c - F) out_c with F = row_max + shifted (the saved
+// forward): energy_grad_parallel's per-chunk sums sum_a e^(s_a - F) v_a, since a
+// chunk partial holds out_c = sum_a e^(s_a - lse_c) v_a.
+__global__ void k_energy_grad_combine(int P, const float* lse, const float* out, const float* rmax,
+                                      const float* shifted, int64_t rows, int d, float* grad) {
+    const int64_t n = rows * d;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / d;
+        const float f = rmax[r] + shifted[r];
+        float g = 0.f;
+        for (int c = 0; c < P; ++c) {
+            const float l = lse[c * rows + r];
+            if (l != -CUDART_INF_F) g += expf(l - f) * out[c * n + i];
+        }
+        grad[i] = g;
+    }
+}
+
+// Distributed forward, step 2 (after allreduce(max) of row_max into m):
+// x = e^(lse - m); step 3 (after allreduce(sum) of x into s): the outputs.
+__global__ void k_energy_shift(const float* lse, const float* m, int64_t rows, float* x) {
+    const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (r < rows) x[r] = (lse[r] == -CUDART_INF_F || m[r] == -CUDART_INF_F) ? 0.f : expf(lse[r] - m[r]);
+}
+__global__ void k_energy_finish(const float* m, const float* s, int64_t rows, float* value, float* rmax_out,
+                                float* shifted) {
+    const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (r >= rows) return;
+    const float mm = m[r];
+    const float sh = mm == -CUDART_INF_F ? -CUDART_INF_F : logf(s[r]);
+    rmax_out[r] = mm;
+    shifted[r] = sh;
+    value[r] = mm == -CUDART_INF_F ? -CUDART_INF_F : mm + sh;
+}
+// F = row_max + shifted (the log partition function of the saved forward)
+__global__ void k_energy_logz(const float* rmax, const float* shifted, int64_t rows, float* f) {
+    const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (r < rows) f[r] = rmax[r] + shifted[r];
+}
+
+cudaError_t launch_energy_combine(int P, const float* rmax, const float* lse, int64_t rows, float* value,
+                                  float* rmax_out, float* shifted, cudaStream_t st) {
+    k_energy_combine<<<grid_for(rows, 256), 256, 0, st>>>(P, rmax, lse, rows, value, rmax_out, shifted);
+    return cudaGetLastError();
+}
+cudaError_t launch_energy_grad_combine(int P, const float* lse, const float* out, const float* rmax,
+                                       const float* shifted, int64_t rows, int d, float* grad, cudaStream_t st) {
+    k_energy_grad_combine<<<grid_for(rows * d, 256), 256, 0, st>>>(P, lse, out, rmax, shifted, rows, d, grad);
+    return cudaGetLastError();
+}
+cudaError_t launch_energy_shift(const float* lse, const float* m, int64_t rows, float* x, cudaStream_t st) {
+    k_energy_shift<<<grid_for(rows, 256), 256, 0, st>>>(lse, m, rows, x);
+    return cudaGetLastError();
+}
+cudaError_t launch_energy_finish(const float* m, const float* s, int64_t rows, float* value, float* rmax_out,
+                                 float* shifted, cudaStream_t st) {
+    k_energy_finish<<<grid_for(rows, 256), 256, 0, st>>>(m, s, rows, value, rmax_out, shifted);
+    return cudaGetLastError();
+}
+cudaError_t launch_energy_logz(const float* rmax, const float* shifted, int64_t rows, float* f, cudaStream_t st) {
+    k_energy_logz<<<grid_for(rows, 256), 256, 0, st>>>(rmax, shifted, rows, f);
     return cudaGetLastError();
 }
 

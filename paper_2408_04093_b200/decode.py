@@ -230,6 +230,102 @@ def attention_chunk_partial(q, k, v, scale: float = 1.0) -> SoftmaxPartial:
     return SoftmaxPartial(rm, lse, out)
 
 
+# ---------------------------------------------------------------- energy formulation
+@dataclass
+class EnergyEval:  # energy.hpp:16-18: per query row, fp32 on the device, natural log
+    value: object        # logsumexp_a(q.k_a + source.v_a) = shifted_lse + row_max
+    row_max: object
+    shifted_lse: object
+
+
+def _check_energy(q, k, v, source, what):
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: rank-4 tensors required")
+    if k.shape[0] != q.shape[0] or k.shape[1] != q.shape[1] or k.shape[3] != q.shape[3]:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: q/k shape mismatch")
+    if v.shape != k.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: k/v shape mismatch")
+    if source is not None and source.shape != q.shape:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: source must have the query shape")
+    if dtype_of(q) != dtype_of(k) or dtype_of(k) != dtype_of(v) or (source is not None and dtype_of(source) != dtype_of(q)):
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: mixed dtypes")
+
+
+def energy_partial(q, k, v, source=None) -> SoftmaxPartial:
+    """One key chunk of the energy (energy.cpp:27-47 scores q.k_a + source.v_a,
+    no 1/sqrt(d) scale): per row (row_max, lse, out), q/source [b, h, nq, d],
+    k/v [b, h, t, d]."""
+    torch = _torch()
+    _check_energy(q, k, v, source, "energy_partial")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    src = None if source is None else source.contiguous()
+    b, h, nq, d = q.shape
+    t = k.shape[2]
+    ws = _ctypes_size()
+    check(lib().td_energy_workspace_bytes(int(dtype_of(q)), b, h, nq, t, d, ws))
+    work = torch.empty(max(ws.value, 16), dtype=torch.uint8, device=q.device)
+    rm = torch.empty(b, h, nq, dtype=torch.float32, device=q.device)
+    lse = torch.empty(b, h, nq, dtype=torch.float32, device=q.device)
+    out = torch.empty(b, h, nq, d, dtype=torch.float32, device=q.device)
+    check(lib().td_energy_partial(int(dtype_of(q)), q.data_ptr(), None if src is None else src.data_ptr(),
+                                  k.data_ptr(), v.data_ptr(), b, h, nq, t, d, rm.data_ptr(), lse.data_ptr(),
+                                  out.data_ptr(), work.data_ptr(), work.numel(), _stream_ptr()))
+    return SoftmaxPartial(rm, lse, out)
+
+
+def _energy_chunks(k, v, chunks, what):
+    n = k.shape[2]
+    if chunks < 1 or chunks > n:
+        raise InvalidArgument(_capi.TD_EINVAL, f"{what}: need 1 <= chunks <= N")
+    begin = 0
+    for ext in chunk_extents(n, chunks):
+        yield k[:, :, begin:begin + ext], v[:, :, begin:begin + ext]
+        begin += ext
+
+
+def energy_forward_parallel(q, k, v, source=None, chunks: int = 1) -> EnergyEval:
+    """energy_forward_parallel (energy.cpp:152-203): the key axis in `chunks`
+    pieces, local (max, lse) per piece, then the max and logsumexp reductions.
+    Equal to the one-chunk energy for every chunk count."""
+    torch = _torch()
+    _check_energy(q, k, v, source, "energy_forward_parallel")
+    parts = [energy_partial(q, kc, vc, source) for kc, vc in _energy_chunks(k, v, chunks, "energy_forward_parallel")]
+    rows = parts[0].lse.numel()
+    rm = torch.stack([p.row_max.reshape(-1) for p in parts]).contiguous()
+    lse = torch.stack([p.lse.reshape(-1) for p in parts]).contiguous()
+    shape = parts[0].lse.shape
+    value, row_max, shifted = (torch.empty(shape, dtype=torch.float32, device=q.device) for _ in range(3))
+    check(lib().td_energy_combine(len(parts), rm.data_ptr(), lse.data_ptr(), rows, value.data_ptr(),
+                                  row_max.data_ptr(), shifted.data_ptr(), _stream_ptr()))
+    return EnergyEval(value, row_max, shifted)
+
+
+def energy(q, k, v, source=None) -> EnergyEval:
+    """energy (energy.cpp:63-83): the one-chunk forward."""
+    return energy_forward_parallel(q, k, v, source, 1)
+
+
+def energy_grad_parallel(q, k, v, saved: EnergyEval, chunks: int = 1):
+    """energy_grad_parallel (energy.cpp:205-259): the source-free gradient
+    replaying `saved`, sum_a e^(q.k_a - row_max - shifted) v_a per chunk, summed
+    over chunks. Equals the attention output."""
+    torch = _torch()
+    _check_energy(q, k, v, None, "energy_grad_parallel")
+    b, h, nq, d = q.shape
+    if tuple(saved.row_max.shape) != (b, h, nq) or tuple(saved.shifted_lse.shape) != (b, h, nq):
+        raise InvalidArgument(_capi.TD_EINVAL, "energy_grad_parallel: saved evaluation does not match inputs")
+    parts = [energy_partial(q, kc, vc, None) for kc, vc in _energy_chunks(k, v, chunks, "energy_grad_parallel")]
+    rows = b * h * nq
+    lse = torch.stack([p.lse.reshape(-1) for p in parts]).contiguous()
+    out = torch.stack([p.out.reshape(rows, d) for p in parts]).contiguous()
+    grad = torch.empty(b, h, nq, d, dtype=torch.float32, device=q.device)
+    rm = saved.row_max.to(torch.float32).contiguous()
+    sh = saved.shifted_lse.to(torch.float32).contiguous()
+    check(lib().td_energy_grad_combine(len(parts), lse.data_ptr(), out.data_ptr(), rm.data_ptr(), sh.data_ptr(),
+                                       rows, d, grad.data_ptr(), _stream_ptr()))
+    return grad
+
+
 def _ctypes_size():
     import ctypes
     return ctypes.c_size_t()
@@ -493,6 +589,39 @@ class Worker:
         else:
             check(lib().td_kv_append(self.h, None, None, 1))
         self.seq_len += 1
+
+    def energy_forward(self, q, source=None) -> EnergyEval:
+        """Alg. 1 over the ranks' shards: q, source [b, n_kv, nq, d] on this
+        rank's device -> EnergyEval (identical on every rank)."""
+        torch = _torch()
+        if q.dim() != 4 or q.shape[0] != self.b or q.shape[1] != self.n_kv or q.shape[3] != self.d:
+            raise InvalidArgument(_capi.TD_EINVAL, "energy_forward: q must be [b, kv_heads, nq, d]")
+        if source is not None and source.shape != q.shape:
+            raise InvalidArgument(_capi.TD_EINVAL, "energy_forward: source must have the query shape")
+        q = q.contiguous()
+        src = None if source is None else source.contiguous()
+        shape = q.shape[:3]
+        value, rm, sh = (torch.empty(shape, dtype=torch.float32, device=q.device) for _ in range(3))
+        self._sync_in(q)
+        check(lib().td_energy_forward(self.h, q.data_ptr(), None if src is None else src.data_ptr(), q.shape[2],
+                                      value.data_ptr(), rm.data_ptr(), sh.data_ptr(), 0))
+        self._sync_worker()
+        return EnergyEval(value, rm, sh)
+
+    def energy_grad(self, q, saved: EnergyEval):
+        """Alg. 2: the source-free gradient from the saved forward (= the
+        attention output), identical on every rank."""
+        torch = _torch()
+        if q.dim() != 4 or q.shape[0] != self.b or q.shape[1] != self.n_kv or q.shape[3] != self.d:
+            raise InvalidArgument(_capi.TD_EINVAL, "energy_grad: q must be [b, kv_heads, nq, d]")
+        q = q.contiguous()
+        rm = saved.row_max.to(torch.float32).contiguous()
+        sh = saved.shifted_lse.to(torch.float32).contiguous()
+        grad = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        self._sync_in(q)
+        check(lib().td_energy_grad(self.h, q.data_ptr(), q.shape[2], rm.data_ptr(), sh.data_ptr(), grad.data_ptr(), 0))
+        self._sync_worker()
+        return grad
 
     def reserve_kv(self, tokens: int):
         check(lib().td_kv_reserve(self.h, int(tokens)))

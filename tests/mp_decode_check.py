@@ -93,6 +93,28 @@ def main():
             ok &= good
             print(json.dumps({"world": world, "append_step": s, "n": m, "tree_rel_err": errs[0],
                               "ring_rel_err": errs[1], "p2p_rel_err": errs[2], "ok": good}), flush=True)
+    # energy formulation across the ranks (Alg. 1 / Alg. 2, energy.cpp:152-259)
+    b, h, nq, n, d = 1, 4, 2, 2048 * world + 3, 128
+    seed = orc.mix64(9, n)
+    qe = orc.seeded(orc.mix64(seed, 1), b * h * nq * d, BF16).reshape(b, h, nq, d)
+    ke = orc.seeded(orc.mix64(seed, 2), b * h * n * d, BF16).reshape(b, h, n, d)
+    ve = orc.seeded(orc.mix64(seed, 3), b * h * n * d, BF16).reshape(b, h, n, d)
+    se = orc.seeded(orc.mix64(seed, 4), b * h * nq * d, BF16, scale=0.5).reshape(b, h, nq, d)
+    s0, ln = td.shard_range(n, world, rank)
+    w.place_kv(bf(ke[:, :, s0:s0 + ln]).cuda(), bf(ve[:, :, s0:s0 + ln]).cuda(), seq_len=n)
+    ev = w.energy_forward(bf(qe).cuda(), bf(se).cuda())
+    e0 = w.energy_forward(bf(qe).cuda())
+    gr = w.energy_grad(bf(qe).cuda(), e0)
+    if rank == 0:
+        want = orc.energy_forward_parallel(qe, ke, ve, se, world, F64)
+        errs = [float(np.max(np.abs(x.double().cpu().numpy() - y)) / max(1.0, np.max(np.abs(y))))
+                for x, y in zip((ev.value, ev.row_max, ev.shifted_lse), want)]
+        _, rm, sh = orc.energy_forward_parallel(qe, ke, ve, None, world, F64)
+        gw = orc.energy_grad_parallel(qe, ke, ve, rm, sh, world, F64)
+        eg = float(np.max(np.abs(gr.double().cpu().numpy() - gw)) / np.max(np.abs(gw)))
+        good = max(errs) <= 1e-3 and eg <= 1e-3
+        ok &= good
+        print(json.dumps({"world": world, "energy_forward_errs": errs, "energy_grad_err": eg, "ok": good}), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
     w.close()
