@@ -54,8 +54,9 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
     ap.add_argument("--seq-len", type=int, default=None)
     ap.add_argument("--algo", choices=["tree", "ring"], default="tree")
-    ap.add_argument("--combine", choices=["nccl", "p2p"], default="nccl",
-                    help="tree exchange: two NCCL allreduces (paper-literal) or one-shot NVLink push")
+    ap.add_argument("--combine", choices=["nccl", "p2p"], default="p2p",
+                    help="tree exchange (N > 1): one-shot NVLink exchange (default; falls back to nccl "
+                         "if CUDA IPC is unavailable on any rank) or two NCCL allreduces (paper-literal)")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=None)
@@ -282,8 +283,19 @@ def main():
     flags_timed = _capi.TD_TIME_KERNELS
     base_flags = 0
     if args.combine == "p2p" and world > 1 and args.algo == "tree":
-        w.enable_p2p(b * n_q, d)
-        base_flags = _capi.TD_P2P
+        import torch.distributed as dist
+        ok = 1
+        try:
+            w.enable_p2p(b * n_q, d)
+        except Exception as e:  # every rank must agree before the first exchange
+            print(f"rank {rank}: P2P exchange unavailable ({e}); using the NCCL path", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            base_flags = _capi.TD_P2P
+        else:
+            args.combine = "nccl"
 
     def step(flags):
         decode(q.data_ptr(), n_q, out.data_ptr(), args.scale, flags | base_flags)

@@ -100,8 +100,9 @@ void timeit(const char* name, size_t bytes, int ctas, F launch, uint8_t* flush, 
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     std::vector<float> ms;
+    static const bool no_flush = getenv("NOFLUSH") != nullptr;
     for (int it = 0; it < 23; ++it) {
-        CK(cudaMemsetAsync(flush, it & 255, flush_bytes));
+        if (!no_flush) CK(cudaMemsetAsync(flush, it & 255, flush_bytes));
         CK(cudaEventRecord(a));
         launch();
         CK(cudaEventRecord(b));
@@ -112,9 +113,9 @@ void timeit(const char* name, size_t bytes, int ctas, F launch, uint8_t* flush, 
     }
     CK(cudaGetLastError());
     std::sort(ms.begin(), ms.end());
-    printf("{\"variant\": \"%s\", \"ctas\": %d, \"mb\": %.1f, \"best_us\": %.2f, \"median_us\": %.2f, "
+    printf("{\"flush\": %d, \"variant\": \"%s\", \"ctas\": %d, \"mb\": %.1f, \"best_us\": %.2f, \"median_us\": %.2f, "
            "\"best_gbs\": %.1f, \"median_gbs\": %.1f}\n",
-           name, ctas, bytes / 1e6, ms[0] * 1e3, ms[ms.size() / 2] * 1e3, bytes / (ms[0] * 1e-3) / 1e9,
+           no_flush ? 0 : 1, name, ctas, bytes / 1e6, ms[0] * 1e3, ms[ms.size() / 2] * 1e3, bytes / (ms[0] * 1e-3) / 1e9,
            bytes / (ms[ms.size() / 2] * 1e-3) / 1e9);
     fflush(stdout);
 }
