@@ -185,6 +185,8 @@ struct td_context {
 
     DevBuf dbg;  // TD_DEBUG_TS stamps
     int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
+    float* mapped_for = nullptr;   // this call's host output buffer and its device alias (or null)
+    float* mapped_dev = nullptr;
     DevBuf tlbuf;           // TD_DEBUG_TIMELINE stamps (read back as dbg[5000..6144))
 
     // calibrated static partition: per-CTA streaming speed of this GPU's SMs
@@ -502,6 +504,20 @@ const void* stage_q(td_context* ctx, const void* q, int64_t n_q, int flags, int*
     return ctx->q_dev.p;
 }
 
+// The device alias of a pinned (cudaHostAlloc / registered) host buffer, or
+// nullptr for pageable memory. With UVA pinned memory is mapped, so the final
+// kernel can store the result straight into it (no D2H copy on the step).
+float* mapped_host(td_context* ctx, float* host) {
+    cudaPointerAttributes at{};  // queried on every call: the buffer may have been freed and reused
+    float* dev = nullptr;
+    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+        dev = static_cast<float*>(at.devicePointer);
+    cudaGetLastError();
+    ctx->mapped_for = host;
+    ctx->mapped_dev = dev;
+    return dev;
+}
+
 int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int flags) {
     const size_t bytes = size_t(rows) * size_t(ctx->d) * sizeof(float);
     if (flags & TD_BF16_OUT) {
@@ -510,7 +526,8 @@ int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int
         ctx->last_kernels += 1;
     }
     if (flags & TD_HOST_IO) {
-        TD_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (src != ctx->mapped_dev || ctx->mapped_for != out)  // else the kernel stored into `out` already
+            TD_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         TD_CUDA(cudaStreamSynchronize(ctx->stream));
     } else if (out != src) {
         TD_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1083,7 +1100,11 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         } else if (ctx->cur_phase) {
             e1 = (*ctx->cur_phase)[ctx->cur_mark++];
         }
-        float* xdst = (flags & TD_HOST_IO) ? ctx->out : out;
+        float* xdst = out;
+        if (flags & TD_HOST_IO) {
+            float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
+            xdst = m ? m : ctx->out;
+        }
         TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                            ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
         phase_mark(ctx);
@@ -1096,7 +1117,11 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     if (ctx->nranks == 1) {
         // p = 1: the shard partial is the result (shift = lse, w = 1): one kernel,
         // written straight into the caller's buffer when it is on the device
-        float* dst = (flags & TD_HOST_IO) ? ctx->out : out;
+        float* dst = out;
+        if (flags & TD_HOST_IO) {
+            float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
+            dst = m ? m : ctx->out;
+        }
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
         const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
