@@ -64,6 +64,30 @@ def parse():
     return ap.parse_args()
 
 
+def interconnect(args, world, b, n_q, n_kv, n, d, esz, ms):
+    """NVLink payload per rank per step and its rate over the step (a lower bound
+    on the bus rate: the transfers overlap compute). Ring: the p-1 KV chunks each
+    rank receives; tree: the exchange (LL words of [out | lse] to every peer, or
+    the payload of NCCL's max and sum allreduces)."""
+    if world == 1:
+        return None
+    rows = b * n_q
+    if args.algo == "ring":
+        per_tok = b * n_kv * d * esz * 2
+        base, extra = divmod(n, world)
+        chunk = [base + (1 if i < extra else 0) for i in range(world)]
+        nbytes = sum(chunk) - chunk[0]  # every rank receives all chunks but its own (max over ranks ~ this)
+        nbytes *= per_tok
+        what = "ring pass-KV: KV chunks received per rank (NCCL send/recv)"
+    elif args.combine == "p2p":
+        nbytes = (world - 1) * rows * (d + 1) * 8
+        what = "one-shot exchange: LL words (value, epoch) of [out | lse] pushed to every peer"
+    else:
+        nbytes = rows * 4 + rows * (d + 1) * 4
+        what = "NCCL allreduce(max) of lse + allreduce(sum) of [n | d] (payload)"
+    return {"kind": "nvlink", "bytes_per_rank_per_step": nbytes, "gbs": nbytes / (ms * 1e-3) / 1e9, "what": what}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -398,7 +422,8 @@ def main():
             "data": "synthetic (reference SplitMix64 generator, generated on device)",
             "config": {"workload": args.workload, "desc": desc, "seq_len": n, "batch": b, "q_heads": n_q,
                        "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": shard_len,
-                       "algo": args.algo, "combine": args.combine if world > 1 else "none", "scale": args.scale,
+                       "algo": args.algo, "combine": args.combine if world > 1 and args.algo == "tree" else "none",
+                       "scale": args.scale,
                        "l2": "flushed between steps" if flush else "inputs larger than L2 (KV shard > 4x126 MB)",
                        "parallelism": f"sp{world} (sequence-sharded KV)"},
             "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
@@ -413,6 +438,7 @@ def main():
             "e2e": {"value": e2e_ms * 1000.0 / b, "unit": "µs/token",
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
                     "matches_device_output": bool(ok)},
+            "interconnect": interconnect(args, world, b, n_q, n_kv, n, d, esz, ms),
             "phases_us": phases,
             "gpu_launches": kernels_per_step * args.steps,
             "kernels_per_step": kernels_per_step,

@@ -16,6 +16,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--b", type=int, default=1)
+    ap.add_argument("--nq", type=int, default=32)
+    ap.add_argument("--nkv", type=int, default=8)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -29,20 +32,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         w = td.Worker.from_torch_distributed(local)
-        w.enable_p2p(32, 128)
+        w.enable_p2p(args.b * args.nq, 128)
         flags = _capi.TD_P2P
     else:
         w = td.Worker(local)
-    w.generate_kv(td.DType.Bf16, 1, 8, args.seq_len, 128, 2, 3)
-    q = td.seeded_tensor([1, 32, 128], 1, 1.0, td.DType.Bf16)
-    out = torch.empty(1, 32, 128, device="cuda")
+    w.generate_kv(td.DType.Bf16, args.b, args.nkv, args.seq_len, 128, 2, 3)
+    q = td.seeded_tensor([args.b, args.nq, 128], 1, 1.0, td.DType.Bf16)
+    out = torch.empty(args.b, args.nq, 128, device="cuda")
     for _ in range(3):
-        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, flags)
+        w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     for _ in range(args.steps):
-        w.tree_decode_async(q.data_ptr(), 32, out.data_ptr(), 1.0, flags)
+        w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
     torch.cuda.synchronize()
     st = w.debug_stamps(6144)
     rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(3, 3 + args.steps)]
