@@ -1021,7 +1021,9 @@ static int timeline_step(td_context* ctx) {
                            cudaMemcpyHostToDevice));
         ctx->tl_count = 0;
     }
-    td::set_timeline(static_cast<unsigned long long*>(ctx->tlbuf.p) + 4 * (ctx->tl_count % 286));
+    TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
+    td::set_timeline(static_cast<unsigned long long*>(ctx->tlbuf.p) + 4 * (ctx->tl_count % 286),
+                     static_cast<unsigned long long*>(ctx->dbg.p));
     ++ctx->tl_count;
     return TD_OK;
 }

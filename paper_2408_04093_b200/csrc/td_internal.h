@@ -61,7 +61,7 @@ struct SplitPlan {
 // [0] min K1 CTA start, [1] max K1 CTA end, [8 + 8*blk + k] K2 block stages.
 void set_debug_stamps(unsigned long long* buf);
 // TD_DEBUG_TIMELINE: per-step slot of 4 stamps (nullptr = off), see K1Args::tl.
-void set_timeline(unsigned long long* slot);
+void set_timeline(unsigned long long* slot, unsigned long long* cta = nullptr);
 // TD_DEBUG_TS: a one-thread kernel writing %globaltimer to *p (front-end gaps).
 cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
 

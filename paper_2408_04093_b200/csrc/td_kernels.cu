@@ -76,6 +76,8 @@ struct K1Args {
     unsigned long long* dbg;  // optional globaltimer stamps (TD_DEBUG_TS)
     unsigned long long* tl;   // optional per-step timeline (TD_DEBUG_TIMELINE): [K1 first start,
                               // first CTA past the PDL wait, K1 last end, K2 last done]
+    unsigned long long* tl_cta;  // TD_DEBUG_TIMELINE: per CTA index c, [2048 + c] smid,
+                                 // [4096 + 2c] past the PDL wait, [4097 + 2c] end (last step)
     int reverse;              // debug: CTA c takes range ctas-1-c (TD_DEBUG_REVERSE)
     // dynamic "home" pool (k1_bf16): tiles [pool_first, pool_first + pool_tiles)
     // of every bh are handed out at run time in chunks of pool_chunk tiles to
@@ -94,6 +96,7 @@ struct K1Args {
     const int* sm_to_cta;     // SM affinity of the calibrated partition (SplitPlan)
     unsigned* claims;
     unsigned epoch;
+    int early_trigger;        // debug: PDL trigger at K1 entry instead of after the main loop
     Tail tail;
 };
 
@@ -212,9 +215,12 @@ __global__ void __launch_bounds__(W * 32, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
     const unsigned long long t_start = (a.dbg || a.tl) ? gtimer() : 0ull;
-    // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
-    // (griddepcontrol.wait) for this grid's completion before reading.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // PDL: K2 may be scheduled once every CTA of this grid has triggered (or
+    // exited); it waits (griddepcontrol.wait) for this grid's completion before
+    // reading. The trigger comes after the main loop: K2's warps, parked in
+    // their wait, would otherwise sit on the SMs for the whole of K1, unevenly
+    // when they land while the previous step drains, and slow the SMs they share.
+    if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = cta_index(a);
     const int64_t A = a.tiles_per_bh;  // static tiles per bh (the pool holds the rest)
@@ -311,9 +317,11 @@ __global__ void __launch_bounds__(W * 32, 1)
     // this grid is itself a programmatic dependent (launch_pdl): q, K, V, the
     // workspace and the pool counters only after the preceding kernel is done
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    unsigned long long t_go = 0;
     if (a.tl && threadIdx.x == 0) {
+        t_go = gtimer();
         atomicMin(a.tl + 0, t_start);
-        atomicMin(a.tl + 1, gtimer());
+        atomicMin(a.tl + 1, t_go);
     }
     for (int s = 0; s < S; ++s) refill(s);
 
@@ -502,6 +510,7 @@ __global__ void __launch_bounds__(W * 32, 1)
         __syncwarp();
         refill(s);
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (cur_bh >= 0) flush(cur_bh, cur_rec);
     // untouched slots are empty partials (m = -inf)
     const int phases = a.slot_warps == W ? 1 : 2;
@@ -518,7 +527,17 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncthreads();
     if (phases == 2) cta_merge<2 * W>(a, c, reinterpret_cast<float*>(smem));
     else cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
-    if (a.tl && threadIdx.x == 0) atomicMax(a.tl + 2, gtimer());
+    if (a.tl && threadIdx.x == 0) {
+        const unsigned long long t_end = gtimer();
+        atomicMax(a.tl + 2, t_end);
+        if (a.tl_cta && c < 1024) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.tl_cta[2048 + c] = smid;
+            a.tl_cta[4096 + 2 * c] = t_go;
+            a.tl_cta[4097 + 2 * c] = t_end;
+        }
+    }
     if (a.dbg && threadIdx.x == 0) {
         const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
@@ -853,7 +872,7 @@ __global__ void __launch_bounds__(128) k1_generic(const K1Args a) {
 // an empty chunk (attention.cpp:56-61). One block of K2_THREADS per row;
 // warps stride over the candidate (cta, warp) slots.
 // =========================================================================
-constexpr int K2_THREADS = 32;  // one warp (= one output row) per block: rows spread over SMs
+constexpr int K2_THREADS = 128;  // at most 4 warps (= 4 output rows at a time) per block
 
 // The CTA states covering one bh: CTAs c_lo .. c_lo + S - 1; the first one
 // holds bh in its segment seg_lo, the others in segment 0. Reads only
@@ -1333,12 +1352,16 @@ size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 *
 
 unsigned long long* g_dbg = nullptr;  // set by set_debug_stamps
 unsigned long long* g_tl = nullptr;   // set by set_timeline
+unsigned long long* g_tl_cta = nullptr;
 
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
     K1Args a{};
     a.dbg = g_dbg;
     a.tl = g_tl;
+    a.tl_cta = g_tl_cta;
+    static const int early = [] { const char* e = std::getenv("TD_K1_EARLY_TRIGGER"); return e ? std::atoi(e) : 0; }();
+    a.early_trigger = early;
     static const int rev = [] { const char* e = std::getenv("TD_DEBUG_REVERSE"); return e ? std::atoi(e) : 0; }();
     a.reverse = rev;
     a.q = q;
@@ -1422,7 +1445,10 @@ cudaError_t prefer_max_smem(K kernel) {
 }  // namespace
 
 void set_debug_stamps(unsigned long long* buf) { g_dbg = buf; }
-void set_timeline(unsigned long long* slot) { g_tl = slot; }
+void set_timeline(unsigned long long* slot, unsigned long long* cta) {
+    g_tl = slot;
+    g_tl_cta = cta;
+}
 
 __global__ void k_stamp(unsigned long long* p) { *p = gtimer(); }
 cudaError_t launch_stamp(unsigned long long* p, cudaStream_t st) {
@@ -1650,10 +1676,10 @@ namespace {
 // K2 right behind K1 with programmatic stream serialization (PDL); one warp
 // per row, the lane-column layout chosen by d.
 template <int V, int NC, int BO>
-cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, bool exchange, cudaStream_t st) {
+cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, int warps, bool exchange, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(blocks < 1 ? 1 : blocks));
-    cfg.blockDim = dim3(K2_THREADS);
+    cfg.blockDim = dim3(32 * warps);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1667,14 +1693,27 @@ cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, bool exchange, cudaStre
                     : cudaLaunchKernelEx(&cfg, k2_combine<V, NC, BO>, a);
 }
 
+// One warp per output row, one warp per block, at most one block per SM (ctas
+// blocks): large row counts (batch x heads) loop over the warps. Every extra
+// resident K2 warp measurably slows the neighbouring K1 under PDL: with 1024
+// rows (cfg4), one warp per row made the step 7 % slower, and 4-warp blocks
+// (592 warps) were as slow; 148 single warps match the serial launch. The
+// longer K2 tail (~13 us at 1024 rows) is the cheaper side of that trade.
 cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaStream_t st) {
     const int64_t rows = a.bh_count * a.group;
-    constexpr int WPB = K2_THREADS / 32;
-    int64_t blocks = (rows + WPB - 1) / WPB;
-    if (blocks > max_blocks) blocks = max_blocks;
-    if (a.d % 4 == 0 && a.d <= 128) return launch_k2_t<4, 1, 32>(a, blocks, exchange, st);
-    if (a.d % 4 == 0) return launch_k2_t<4, 2, 16>(a, blocks, exchange, st);
-    return launch_k2_t<1, 8, 8>(a, blocks, exchange, st);
+    static const int cap = [] { const char* e = std::getenv("TD_K2_MAX_BLOCKS"); return e ? std::atoi(e) : 0; }();
+    int64_t limit = cap > 0 ? cap : (a.ctas > 0 ? a.ctas : 1);
+    if (limit > max_blocks) limit = max_blocks;
+    static const int force_w = [] { const char* e = std::getenv("TD_K2_WARPS"); return e ? std::atoi(e) : 0; }();
+    int warps = force_w > 0 ? force_w : 1;
+    warps = warps < 1 ? 1 : (warps > K2_THREADS / 32 ? K2_THREADS / 32 : warps);
+    int64_t blocks = (rows + warps - 1) / warps;
+    if (blocks > limit) blocks = limit;
+#define TD_K2(VV, NN, BB) launch_k2_t<VV, NN, BB>(a, blocks, warps, exchange, st)
+    if (a.d % 4 == 0 && a.d <= 128) return TD_K2(4, 1, 32);
+    if (a.d % 4 == 0) return TD_K2(4, 2, 16);
+    return TD_K2(1, 8, 8);
+#undef TD_K2
 }
 
 }  // namespace

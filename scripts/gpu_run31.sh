@@ -1,6 +1,9 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 export CUDA_VISIBLE_DEVICES=0
-TD_DEBUG_TIMELINE=1 timeout 300 python scripts/timeline_probe.py --b 16 --nq 64 --nkv 8 --seq-len 131072 > gpurun_out/tl_cfg4.log 2>&1
-TD_DEBUG_TIMELINE=1 TD_K1_PDL=0 timeout 300 python scripts/timeline_probe.py --b 16 --nq 64 --nkv 8 --seq-len 131072 >> gpurun_out/tl_cfg4.log 2>&1
-TD_K1_PDL=0 timeout 600 python bench.py --workload cfg4 --steps 20 --no-cpu-baseline > gpurun_out/w_cfg4_nopdl.log 2>&1
+for rep in 1 2; do
+for v in "X=0" "TD_K2_WARPS=1" "TD_K2_WARPS=1 TD_K2_MAX_BLOCKS=4096" "TD_K1_PDL=0" "TD_K1_EARLY_TRIGGER=1"; do
+echo "$v" >> gpurun_out/ab_k2.log
+env $v timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --seq-len 131072 >> gpurun_out/ab_k2.log 2>&1
+env $v timeout 300 python bench.py --steps 10 --warmup 5 --no-cpu-baseline --workload cfg4 >> gpurun_out/ab_k2.log 2>&1
+done; done

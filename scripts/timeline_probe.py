@@ -60,6 +60,11 @@ def main():
                       "k1_start_minus_prev_k2_done": gaps, "k1_past_wait_minus_prev_k2_done": waits,
                       "step_period": steps, "k1_span": [round(r[2] - r[1], 2) for r in tl],
                       "tail": [round(r[3] - r[2], 2) for r in tl]}))
+    if os.environ.get("TL_DUMP_CTAS"):  # the last step, per CTA index: (c, smid, past-wait, end)
+        g0 = min(st[4096 + 2 * c] for c in range(1024) if st[4096 + 2 * c])
+        print(json.dumps({"rank": local, "ctas": [(c, st[2048 + c], round((st[4096 + 2 * c] - g0) / 1000.0, 2),
+                                                   round((st[4097 + 2 * c] - g0) / 1000.0, 2))
+                                                  for c in range(1024) if st[4097 + 2 * c]]}))
     w.close()
     if world > 1:
         dist.barrier()
