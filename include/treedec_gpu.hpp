@@ -31,6 +31,7 @@
 #include "treedec/attention.hpp"
 #include "treedec/cluster.hpp"
 #include "treedec/decode.hpp"
+#include "treedec/energy.hpp"
 #include "treedec/reduce.hpp"
 #include "treedec_b200.h"
 
@@ -77,6 +78,9 @@ template <typename T>
 struct DeviceArray {
     T* p = nullptr;
     explicit DeviceArray(std::size_t n) { cuda(cudaMalloc(&p, sizeof(T) * (n ? n : 1)), "cudaMalloc"); }
+    DeviceArray(DeviceArray&& o) noexcept : p(o.p) { o.p = nullptr; }
+    DeviceArray(const DeviceArray&) = delete;
+    DeviceArray& operator=(const DeviceArray&) = delete;
     ~DeviceArray() { cudaFree(p); }
 };
 
@@ -194,6 +198,116 @@ inline DecodeResult ring_decode(const Tensor& q, const ShardedKVCache& cache, co
     r.overlap_feasible = of.feasible;
     r.overlap_ratio = of.ratio;
     return r;
+}
+
+namespace detail {
+
+// A [b, h, n, d] tensor (or its key rows [k0, k1)) on the device, in its dtype.
+inline DeviceArray<std::uint8_t> upload(const Tensor& t, std::int64_t k0 = 0, std::int64_t k1 = -1) {
+    const int dt = code_of(t.dtype());
+    const std::int64_t b = t.extent(0), h = t.extent(1), n = t.extent(2), d = t.extent(3);
+    if (k1 < 0) k1 = n;
+    const std::int64_t len = k1 - k0;
+    std::vector<double> rows;
+    rows.reserve(std::size_t(b * h * len * d));
+    for (std::int64_t ib = 0; ib < b; ++ib)
+        for (std::int64_t ih = 0; ih < h; ++ih) {
+            const std::int64_t o = t.offset4(ib, ih, k0, 0);
+            rows.insert(rows.end(), t.data().begin() + o, t.data().begin() + o + len * d);
+        }
+    const std::size_t esz = dt == TD_BF16 ? 2 : 4;
+    DeviceArray<std::uint8_t> dev(rows.size() * esz);
+    if (dt == TD_BF16) {
+        const auto x = to_bf16(rows);
+        cuda(cudaMemcpy(dev.p, x.data(), x.size() * 2, cudaMemcpyHostToDevice), "copy");
+    } else {
+        const auto x = to_f32(rows);
+        cuda(cudaMemcpy(dev.p, x.data(), x.size() * 4, cudaMemcpyHostToDevice), "copy");
+    }
+    return dev;
+}
+
+inline void require_energy(const Tensor& q, const Tensor& k, const Tensor& v, const Tensor& source,
+                           const char* what) {
+    if (q.rank() != 4 || k.rank() != 4 || v.rank() != 4)
+        throw std::invalid_argument(std::string(what) + ": rank-4 tensors required");
+    if (k.extent(0) != q.extent(0) || k.extent(1) != q.extent(1) || k.extent(3) != q.extent(3))
+        throw std::invalid_argument(std::string(what) + ": q/k shape mismatch");
+    if (!v.same_shape(k)) throw std::invalid_argument(std::string(what) + ": k/v shape mismatch");
+    if (!source.empty() && !source.same_shape(q))
+        throw std::invalid_argument(std::string(what) + ": source must have the query shape");
+}
+
+// Per-chunk fp32 partials (row_max, lse, out) of q.k + source.v, keys split by chunk_extents.
+inline void energy_chunks(const Tensor& q, const Tensor& k, const Tensor& v, const Tensor& source, int chunks,
+                          DeviceArray<float>& rm, DeviceArray<float>& lse, DeviceArray<float>& out) {
+    const int dt = code_of(q.dtype());
+    const std::int64_t b = q.extent(0), h = q.extent(1), nq = q.extent(2), d = q.extent(3), n = k.extent(2);
+    const std::int64_t rows = b * h * nq;
+    const auto qd = upload(q);
+    const bool with_source = !source.empty();
+    DeviceArray<std::uint8_t> sdev = with_source ? upload(source) : DeviceArray<std::uint8_t>(1);
+    const std::vector<std::int64_t> ext = chunk_extents(n, chunks);
+    std::int64_t k0 = 0;
+    for (int c = 0; c < chunks; ++c) {
+        const std::int64_t t = ext[std::size_t(c)];
+        const auto kd = upload(k, k0, k0 + t), vd = upload(v, k0, k0 + t);
+        std::size_t ws = 0;
+        check(td_energy_workspace_bytes(dt, b, h, nq, t, d, &ws));
+        DeviceArray<std::uint8_t> work(ws);
+        check(td_energy_partial(dt, qd.p, with_source ? sdev.p : nullptr, kd.p, vd.p, b, h, nq, t, d,
+                                rm.p + c * rows, lse.p + c * rows, out.p + c * rows * d, work.p, ws, nullptr));
+        k0 += t;
+    }
+    cuda(cudaDeviceSynchronize(), "energy");
+}
+
+inline Tensor download(const float* dev, std::vector<std::int64_t> shape, DType dt) {
+    std::int64_t n = 1;
+    for (auto e : shape) n *= e;
+    std::vector<float> host(static_cast<std::size_t>(n));
+    cuda(cudaMemcpy(host.data(), dev, host.size() * 4, cudaMemcpyDeviceToHost), "copy");
+    return Tensor(std::move(shape), std::vector<double>(host.begin(), host.end()), dt);
+}
+
+}  // namespace detail
+
+// treedec::energy_forward_parallel (energy.hpp:47-52, energy.cpp:152-203) on the GPU.
+inline EnergyEval energy_forward_parallel(const Tensor& q, const Tensor& k, const Tensor& v, const Tensor& source,
+                                          int chunks) {
+    detail::require_energy(q, k, v, source, "energy_forward_parallel");
+    if (chunks < 1 || chunks > k.extent(2))
+        throw std::invalid_argument("energy_forward_parallel: need 1 <= chunks <= N");
+    const std::int64_t b = q.extent(0), h = q.extent(1), nq = q.extent(2), d = q.extent(3), rows = b * h * nq;
+    detail::DeviceArray<float> rm(std::size_t(chunks) * rows), lse(std::size_t(chunks) * rows),
+        out(std::size_t(chunks) * rows * d), value(rows), rmax(rows), shifted(rows);
+    detail::energy_chunks(q, k, v, source, chunks, rm, lse, out);
+    detail::check(td_energy_combine(chunks, rm.p, lse.p, rows, value.p, rmax.p, shifted.p, nullptr));
+    const DType sdt = stats_dtype(q.dtype());
+    return EnergyEval{detail::download(value.p, {b, h, nq}, sdt), detail::download(rmax.p, {b, h, nq}, sdt),
+                      detail::download(shifted.p, {b, h, nq}, sdt)};
+}
+
+// treedec::energy_grad_parallel (energy.hpp:54-58, energy.cpp:205-259) on the GPU.
+inline Tensor energy_grad_parallel(const Tensor& q, const Tensor& k, const Tensor& v, const EnergyEval& saved,
+                                   int chunks) {
+    detail::require_energy(q, k, v, Tensor{}, "energy_grad_parallel");
+    if (chunks < 1 || chunks > k.extent(2))
+        throw std::invalid_argument("energy_grad_parallel: need 1 <= chunks <= N");
+    const std::int64_t b = q.extent(0), h = q.extent(1), nq = q.extent(2), d = q.extent(3), rows = b * h * nq;
+    const std::vector<std::int64_t> expected{b, h, nq};
+    if (saved.value.shape() != expected || saved.row_max.shape() != expected ||
+        saved.shifted_lse.shape() != expected)
+        throw std::invalid_argument("energy_grad_parallel: saved evaluation does not match inputs");
+    detail::DeviceArray<float> rm(std::size_t(chunks) * rows), lse(std::size_t(chunks) * rows),
+        out(std::size_t(chunks) * rows * d), srm(rows), ssh(rows), grad(rows * d);
+    detail::energy_chunks(q, k, v, Tensor{}, chunks, rm, lse, out);
+    const std::vector<float> hrm(saved.row_max.data().begin(), saved.row_max.data().end());
+    const std::vector<float> hsh(saved.shifted_lse.data().begin(), saved.shifted_lse.data().end());
+    detail::cuda(cudaMemcpy(srm.p, hrm.data(), hrm.size() * 4, cudaMemcpyHostToDevice), "copy");
+    detail::cuda(cudaMemcpy(ssh.p, hsh.data(), hsh.size() * 4, cudaMemcpyHostToDevice), "copy");
+    detail::check(td_energy_grad_combine(chunks, lse.p, out.p, srm.p, ssh.p, rows, d, grad.p, nullptr));
+    return detail::download(grad.p, {b, h, nq, d}, q.dtype());
 }
 
 }  // namespace treedec::gpu

@@ -8,6 +8,7 @@
 
 #include "treedec/numerics.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -106,6 +107,45 @@ int main() {
         }
         expect(threw, "Float64 rejected with invalid_argument", 0, 0);
     }
+    // energy formulation (energy.hpp:47-58) through treedec::gpu against the reference
+    // at Float64 on the same grid values (test_energy.cpp:192-230)
+    for (const DType dt : {DType::Float32, DType::Bf16})
+        for (const std::int64_t n : {17LL, 300LL, 4096LL})
+            for (const std::int64_t nq : {1LL, 3LL}) {
+                const std::int64_t h = 2, d = 64;
+                const std::uint64_t seed = 7 + static_cast<std::uint64_t>(n) + 11 * nq;
+                const Tensor q = seeded_random_tensor({1, h, nq, d}, mix64(seed, 1), 1.0, dt);
+                const Tensor k = seeded_random_tensor({1, h, n, d}, mix64(seed, 2), 1.0, dt);
+                const Tensor v = seeded_random_tensor({1, h, n, d}, mix64(seed, 3), 1.0, dt);
+                const Tensor src = seeded_random_tensor({1, h, nq, d}, mix64(seed, 4), 0.5, dt);
+                const double tol = dt == DType::Bf16 ? 1e-3 : 1e-5;
+                for (const int chunks : {1, 3, 8}) {
+                    if (chunks > n) continue;
+                    const EnergyEval want = energy_forward_parallel(retag(q, DType::Float64), retag(k, DType::Float64),
+                                                                    retag(v, DType::Float64),
+                                                                    retag(src, DType::Float64), chunks);
+                    const EnergyEval got = gpu::energy_forward_parallel(q, k, v, src, chunks);
+                    const double err = std::max({max_abs_diff(got.value, want.value),
+                                                 max_abs_diff(got.row_max, want.row_max),
+                                                 max_abs_diff(got.shifted_lse, want.shifted_lse)});
+                    const double scale = std::max(1.0, max_abs(want.value));
+                    std::snprintf(what, sizeof what, "energy fwd dt=%s n=%lld nq=%lld chunks=%d", dtype_name(dt),
+                                  (long long)n, (long long)nq, chunks);
+                    expect(err <= tol * scale, what, err, tol * scale);
+                    const EnergyEval saved = energy_forward_parallel(retag(q, DType::Float64), retag(k, DType::Float64),
+                                                                     retag(v, DType::Float64), Tensor{}, chunks);
+                    const Tensor gw = energy_grad_parallel(retag(q, DType::Float64), retag(k, DType::Float64),
+                                                           retag(v, DType::Float64), saved, chunks);
+                    const Tensor gg = gpu::energy_grad_parallel(q, k, v, saved, chunks);
+                    // the gradient is stored through the input grid like the reference's
+                    // (Tensor::store): the reference's own bf16 decode tolerance applies
+                    const double eg = max_abs_diff(gg, gw),
+                                 tg = dt == DType::Bf16 ? decode_tolerance_abs(dt, max_abs(gw)) : tol * max_abs(gw);
+                    std::snprintf(what, sizeof what, "energy grad dt=%s n=%lld nq=%lld chunks=%d", dtype_name(dt),
+                                  (long long)n, (long long)nq, chunks);
+                    expect(eg <= tg, what, eg, tg);
+                }
+            }
     std::printf("shim_parity: %d checks, %d failures\n", checks, failures);
     return failures == 0 ? 0 : 1;
 }
