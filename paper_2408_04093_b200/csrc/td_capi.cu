@@ -933,24 +933,31 @@ static int kv_grow(td_context* ctx, int64_t cap) {
     const size_t esz = td::dtype_bytes(ctx->dtype);
     const size_t row_old = size_t(ctx->cap) * size_t(ctx->d) * esz, row_new = size_t(cap) * size_t(ctx->d) * esz;
     const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
+    if (int64_t(rows) * cap >= (int64_t(1) << 31)) return set_err(TD_EINVAL, "kv_append: shard too large for 32-bit TMA rows");
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (DevBuf* buf : {&ctx->k, &ctx->v}) {
-        void* fresh = nullptr;
-        TD_CUDA(cudaMalloc(&fresh, rows * row_new));
+    // both new buffers first, so a failed allocation leaves the shard untouched
+    void* fresh[2] = {nullptr, nullptr};
+    cudaError_t e = cudaMalloc(&fresh[0], rows * row_new);
+    if (e == cudaSuccess) e = cudaMalloc(&fresh[1], rows * row_new);
+    DevBuf* bufs[2] = {&ctx->k, &ctx->v};
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         // the unused tail of every row is read by partial tiles (masked out of the
         // softmax, but 0 * NaN would poison P.V): keep it zero
-        cudaError_t e = cudaMemsetAsync(fresh, 0, rows * row_new, ctx->stream);
+        e = cudaMemsetAsync(fresh[i], 0, rows * row_new, ctx->stream);
         if (e == cudaSuccess)
-            e = cudaMemcpy2DAsync(fresh, row_new, buf->p, row_old, size_t(ctx->len) * size_t(ctx->d) * esz,
+            e = cudaMemcpy2DAsync(fresh[i], row_new, bufs[i]->p, row_old, size_t(ctx->len) * size_t(ctx->d) * esz,
                                   rows, cudaMemcpyDeviceToDevice, ctx->stream);
-        if (e != cudaSuccess) {
-            cudaFree(fresh);
-            TD_CUDA(e);
-        }
-        TD_CUDA(cudaStreamSynchronize(ctx->stream));
-        buf->release();
-        buf->p = fresh;
-        buf->cap = rows * row_new;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        cudaFree(fresh[0]);
+        cudaFree(fresh[1]);
+        TD_CUDA(e);
+    }
+    for (int i = 0; i < 2; ++i) {
+        bufs[i]->release();
+        bufs[i]->p = fresh[i];
+        bufs[i]->cap = rows * row_new;
     }
     ctx->cap = cap;
     for (auto& tb : ctx->tabs) tb.total = -1;  // partition tables follow the new shape
@@ -960,10 +967,13 @@ static int kv_grow(td_context* ctx, int64_t cap) {
 int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host) {
     if (int rc = require_ctx(ctx)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "kv_append: no KV shard placed");
-    ctx->seq_len += 1;  // every rank: the cache is one token longer, on rank p-1
-    ctx->lens.back() += 1;
-    if (ctx->rank != ctx->nranks - 1) return TD_OK;
-    if (ctx->len == ctx->cap)
+    if (ctx->rank != ctx->nranks - 1) {  // every rank: the cache is one token longer, on rank p-1
+        ctx->seq_len += 1;
+        ctx->lens.back() += 1;
+        return TD_OK;
+    }
+    if (!k || !v) return set_err(TD_EINVAL, "kv_append: the last rank needs the token's k and v");
+    if (ctx->len == ctx->cap)  // grows before any state changes: a failure leaves the cache as it was
         if (int rc = kv_grow(ctx, ctx->cap + std::max<int64_t>(1024, ctx->cap / 8))) return rc;
     const size_t esz = td::dtype_bytes(ctx->dtype);
     const size_t tok = size_t(ctx->d) * esz, pitch = size_t(ctx->cap) * tok;
@@ -974,6 +984,8 @@ int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host) {
     TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->v.p) + size_t(ctx->len) * tok, pitch, v, tok, tok, rows,
                               kind, ctx->stream));
     ctx->len += 1;
+    ctx->seq_len += 1;
+    ctx->lens.back() += 1;
     if (from_host) TD_CUDA(cudaStreamSynchronize(ctx->stream));  // the caller may reuse its buffer
     return TD_OK;
 }
