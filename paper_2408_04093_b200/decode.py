@@ -643,6 +643,10 @@ class Worker:
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device="cpu" if host else q.device,
                               pin_memory=host)
+        elif (out.dtype != torch.float32 or out.is_cuda == host or out.numel() != q.numel()
+              or not out.is_contiguous()):
+            raise InvalidArgument(_capi.TD_EINVAL, "decode: out must be a contiguous fp32 tensor of q's shape, "
+                                                   "on the same side (host / device) as q")
         if host:
             flags |= _capi.TD_HOST_IO
         self._sync_in(q)

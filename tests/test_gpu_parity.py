@@ -298,6 +298,29 @@ def test_worker_append_loop(td, oracle, dtype):
     w.close()
 
 
+def test_worker_append_validation_and_output_buffers(td, oracle):
+    """Append errors leave the cache unchanged; host outputs work pinned
+    (zero-copy store) and pageable (D2H copy) alike."""
+    import torch
+    q, k, v = make_inputs(oracle, 35, 1, 8, 2, 700, 128, BF16)
+    w = td.Worker(0)
+    w.place_kv(dev(k, BF16), dev(v, BF16))
+    with pytest.raises(td.InvalidArgument):
+        w.append_kv(torch.zeros(1, 2, 1, 128, dtype=torch.float32), torch.zeros(1, 2, 1, 128, dtype=torch.float32))
+    with pytest.raises(td.InvalidArgument):
+        w.append_kv(torch.zeros(1, 2, 2, 128, dtype=torch.bfloat16), torch.zeros(1, 2, 2, 128, dtype=torch.bfloat16))
+    assert w.kv_info()[1] == 700
+    qh = torch.from_numpy(np.ascontiguousarray(q)).to(torch.bfloat16)
+    pinned = torch.empty(1, 8, 128, dtype=torch.float32).pin_memory()
+    pageable = torch.empty(1, 8, 128, dtype=torch.float32)
+    a = w.tree_decode(qh, out=pinned)
+    b = w.tree_decode(qh, out=pageable)
+    want = oracle.tree_decode(q, k, v, 1, HIER, 1.0, F64)
+    assert rel_err(a.double().numpy(), want) <= 1e-3 and rel_err(b.double().numpy(), want) <= 1e-3
+    assert a.data_ptr() == pinned.data_ptr() and b.data_ptr() == pageable.data_ptr()
+    w.close()
+
+
 def test_worker_place_matches_generate(td, oracle):
     import torch
     q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
