@@ -1077,9 +1077,12 @@ __device__ __forceinline__ void st_ll(uint2* p, float v, unsigned e) {
     asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(e)
                  : "memory");
 }
+#ifndef TD_XCHG_LD
+#define TD_XCHG_LD "ld.volatile.global.v2.u32"
+#endif
 __device__ __forceinline__ uint2 ld_word(const uint2* p) {  // one poll, no wait
     uint2 w;
-    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(p) : "memory");
+    asm volatile(TD_XCHG_LD " {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(p) : "memory");
     return w;
 }
 __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
