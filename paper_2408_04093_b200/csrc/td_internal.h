@@ -37,6 +37,10 @@ struct SplitPlan {
     // parity, and the parity of this launch (alternate between launches)
     unsigned* counters = nullptr;
     int parity = 0;
+    // cross-row stealing: warps whose own rows' pools are empty take chunks of
+    // any row's pool and fold them into one of that row's fslots foreign states
+    // ([bh_count][fslots]; 0 = off)
+    int fslots = 0;
     // calibrated static partition (device tables, optional; see
     // build_partition): CTA c owns static tiles [x_table[c], x_table[c+1])
     const int64_t* x_table = nullptr;
@@ -52,9 +56,11 @@ struct SplitPlan {
     // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32),
     // then the per-CTA merged states [ctas * maxseg][group] (+ [..][d])
     size_t workspace_bytes() const {
-        return sizeof(float) * (size_t(slots()) + size_t(ctas) * maxseg) * size_t(group) * size_t(2 + d);
+        return sizeof(float) * ((size_t(slots()) + size_t(ctas) * maxseg) * size_t(group) * size_t(2 + d) +
+                                size_t(bh_count) * size_t(fslots) * size_t(group) * size_t(2 + d));
     }
-    size_t counters_bytes() const { return sizeof(unsigned) * 2 * size_t(bh_count > 0 ? bh_count : 1); }
+    // [2 parities][bh_count] pool chunk counters, then [2][bh_count] foreign-slot counters
+    size_t counters_bytes() const { return sizeof(unsigned) * 4 * size_t(bh_count > 0 ? bh_count : 1); }
 };
 
 // TD_DEBUG_TS: kernels write %globaltimer stamps into buf (nullptr = off):

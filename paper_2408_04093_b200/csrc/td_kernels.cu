@@ -88,6 +88,15 @@ struct K1Args {
     int slot_warps;           // state slots per CTA and segment (warps * 2 with a pool)
     unsigned* pool_ctr;       // [bh_count] chunks taken (this launch's parity)
     unsigned* pool_next;      // [bh_count] the other parity's counters (zeroed by K2)
+    // cross-row stealing (SplitPlan::fslots): foreign states [bh][fslots][group]
+    // (+ [..][d]); fcnt[bh] counts the claimed ones (this parity), fcnt_next is zeroed by K2
+    int fslots;
+    int steal_scans, steal_min;  // scans per warp; least chunks left worth a visit
+    unsigned* fcnt;
+    unsigned* fcnt_next;
+    float* fslot_m;
+    float* fslot_l;
+    float* fslot_o;
     // calibrated static partition (optional): CTA c owns static tiles
     // [x_table[c], x_table[c+1]); bh_table[3 bh + {0,1,2}] = the first and last
     // CTA covering bh and bh's segment index in the first one
@@ -252,6 +261,20 @@ __global__ void __launch_bounds__(W * 32, 1)
     const int64_t cb_start = last_static >= 0 ? last_static / A : cb_hi;  // stay on the current bh first
     int64_t p_bh = -1, p_pos = 0, p_end = 0, p_tries = 0;
     bool p_done = nch == 0 || ncb <= 0;
+    // cross-row stealing, once the own rows' pools are empty: the row whose pool
+    // has the most chunks left (one coalesced read of the counters), one claimed
+    // foreign state per visit; a claimed state that gets no chunk is written empty
+    int64_t f_bh = -1, f_pos = 0, f_end = 0;
+    int f_slot = 0, f_scans = 0;
+    bool f_got = false, f_on = a.fslots > 0 && nch > 0;
+    uint64_t f_full = 0;  // rows whose foreign states ran out (first 64 rows)
+    auto empty_foreign = [&](int64_t bh, int slot) {
+        const int64_t fs = (bh * a.fslots + slot) * a.group;
+        for (int h = lane; h < a.group; h += 32) {
+            a.fslot_m[fs + h] = -CUDART_INF_F;
+            a.fslot_l[fs + h] = 0.f;
+        }
+    };
     auto next_tile = [&](int64_t& bh, int64_t& tb, int& rec) -> bool {
         if (s_next < x1) {
             bh = s_next / A;
@@ -284,6 +307,70 @@ __global__ void __launch_bounds__(W * 32, 1)
             }
             p_bh = cb_lo + (cb_start - cb_lo + p_tries) % ncb;
             ++p_tries;
+        }
+        while (f_on) {
+            if (f_pos < f_end) {
+                bh = f_bh;
+                tb = f_pos++;
+                rec = 2 + f_slot;
+                f_got = true;
+                return true;
+            }
+            if (f_bh >= 0) {  // next chunk of the row being helped
+                unsigned k = 0;
+                if (lane == 0) k = atomicAdd(a.pool_ctr + f_bh, 1u);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k < nch) {
+                    f_pos = a.pool_first + int64_t(k) * a.pool_chunk;
+                    f_end = min(f_pos + a.pool_chunk, a.pool_first + a.pool_tiles);
+                    continue;
+                }
+                if (!f_got) empty_foreign(f_bh, f_slot);
+                f_bh = -1;
+            }
+            if (++f_scans > a.steal_scans) {
+                f_on = false;
+                break;
+            }
+            unsigned best_left = 0;
+            int64_t best = -1;
+            for (int64_t j0 = 0; j0 < a.bh_count; j0 += 32) {
+                const int64_t j = j0 + lane;
+                unsigned left = 0;
+                if (j < a.bh_count && !(j < 64 && ((f_full >> j) & 1ull))) {
+                    const unsigned used = *reinterpret_cast<volatile const unsigned*>(a.pool_ctr + j);
+                    left = used < unsigned(nch) ? unsigned(nch) - used : 0u;
+                }
+                unsigned bl = left;
+                int64_t bj = j;
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const unsigned ol = __shfl_xor_sync(0xffffffffu, bl, off);
+                    const int64_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
+                    if (ol > bl || (ol == bl && oj < bj)) {
+                        bl = ol;
+                        bj = oj;
+                    }
+                }
+                if (bl > best_left) {
+                    best_left = bl;
+                    best = bj;
+                }
+            }
+            if (best < 0 || best_left < unsigned(a.steal_min)) {  // the owners drain small remainders
+                f_on = false;
+                break;
+            }
+            unsigned fidx = 0;
+            if (lane == 0) fidx = atomicAdd(a.fcnt + best, 1u);
+            fidx = __shfl_sync(0xffffffffu, fidx, 0);
+            if (fidx >= unsigned(a.fslots)) {
+                if (best < 64) f_full |= 1ull << best;
+                continue;
+            }
+            f_bh = best;
+            f_slot = static_cast<int>(fidx);
+            f_got = false;
         }
         return false;
     };
@@ -365,13 +452,21 @@ __global__ void __launch_bounds__(W * 32, 1)
         lb += __shfl_xor_sync(0xffffffffu, lb, 4);
         lb += __shfl_xor_sync(0xffffffffu, lb, 8);
         lb += __shfl_xor_sync(0xffffffffu, lb, 16);
-        const int seg = static_cast<int>(bh - bh_first);
-        const int sub = a.slot_warps == W ? warp : 2 * warp + rec;
-        const int64_t slot = (int64_t(c) * a.slot_warps + sub) * a.maxseg + seg;
-        float* sm = a.slot_m + slot * a.group;
-        float* sl = a.slot_l + slot * a.group;
-        float* so = a.slot_o + slot * a.group * int64_t(D);
-        flushed |= 1ull << (2 * seg + rec);
+        float *sm, *sl, *so;
+        if (rec >= 2) {  // a foreign state of row bh (cross-row stealing)
+            const int64_t fs = bh * a.fslots + (rec - 2);
+            sm = a.fslot_m + fs * a.group;
+            sl = a.fslot_l + fs * a.group;
+            so = a.fslot_o + fs * a.group * int64_t(D);
+        } else {
+            const int seg = static_cast<int>(bh - bh_first);
+            const int sub = a.slot_warps == W ? warp : 2 * warp + rec;
+            const int64_t slot = (int64_t(c) * a.slot_warps + sub) * a.maxseg + seg;
+            sm = a.slot_m + slot * a.group;
+            sl = a.slot_l + slot * a.group;
+            so = a.slot_o + slot * a.group * int64_t(D);
+            flushed |= 1ull << (2 * seg + rec);
+        }
         if (lane < 4) {
             if (hA < a.group) { sm[hA] = m0; sl[hA] = la; }
             if (hB < a.group) { sm[hB] = m1; sl[hB] = lb; }
@@ -880,7 +975,14 @@ constexpr int K2_THREADS = 128;  // at most 4 warps (= 4 output rows at a time) 
 struct Cover {
     int64_t c_lo = 0, seg_lo = 0;
     int S = 0;
+    int nf = 0;  // foreign states (cross-row stealing) of the row's bh: set after the wait
 };
+// The foreign states K1 claimed for bh (read after griddepcontrol.wait).
+__device__ __forceinline__ int foreign_of(const K1Args& a, int64_t bh) {
+    if (a.fslots <= 0 || !a.fcnt) return 0;
+    const unsigned n = __ldcg(a.fcnt + bh);
+    return static_cast<int>(n < unsigned(a.fslots) ? n : unsigned(a.fslots));
+}
 __device__ __forceinline__ Cover cover_of(const K1Args& a, int64_t bh) {
     Cover cv;
     int64_t c_hi = -1;
@@ -918,42 +1020,46 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
     static_assert(BO <= 32, "one candidate (m, l) per lane");
     const int lane = threadIdx.x & 31;
     const int h = static_cast<int>(r % a.group);
-    const int D = a.d, g = a.group, S = cv.S;
+    const int D = a.d, g = a.group, S = cv.S, T = cv.S + cv.nf;
     auto cs_of = [&](int i) { return (cv.c_lo + i) * a.maxseg + (i == 0 ? cv.seg_lo : 0); };
-    // 32-bit float offsets (the CTA-state arrays are small): candidate i >= 1 sits at
-    // a fixed stride from candidate 1; candidate 0 has its own segment
+    // 32-bit float offsets (the state arrays are small): static candidate i >= 1 sits
+    // at a fixed stride from candidate 1, candidate 0 has its own segment; candidates
+    // i >= S are the row's foreign states (cross-row stealing), stride g
     const int st = a.maxseg * g;
     const int b0 = static_cast<int>(cs_of(0) * g + h), b1 = static_cast<int>(cs_of(1) * g + h);
+    const int fb = static_cast<int>((r / g) * a.fslots * g + h);
     const int col0 = lane * V;
+    auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
     vec ov[BO][NC];
     float ml = -CUDART_INF_F, ll = 0.f;  // lane i holds (m, l) of candidate i0 + i (BO <= 32)
     auto load = [&](int i0) {
         {
             const int i = i0 + lane;
-            const int off = i == 0 ? b0 : b1 + (i - 1) * st;
             ml = -CUDART_INF_F;
             ll = 0.f;
-            if (lane < BO && i < S) {
-                ml = __ldcg(a.cslot_m + off);
-                ll = __ldcg(a.cslot_l + off);
+            if (lane < BO && i < T) {
+                const int off = off_of(i);
+                ml = __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off);
+                ll = __ldcg((i >= S ? a.fslot_l : a.cslot_l) + off);
             }
         }
 #pragma unroll
         for (int u = 0; u < BO; ++u) {
             const int i = i0 + u;
-            const int off = i == 0 ? b0 : b1 + (i - 1) * st;
+            const int off = off_of(i);
+            const float* ob = i >= S ? a.fslot_o : a.cslot_o;
 #pragma unroll
             for (int c = 0; c < NC; ++c)
-                if (i < S && col0 + c * 32 * V < D)
-                    ov[u][c] = __ldcg(reinterpret_cast<const vec*>(a.cslot_o + off * D + col0 + c * 32 * V));
+                if (i < T && col0 + c * 32 * V < D)
+                    ov[u][c] = __ldcg(reinterpret_cast<const vec*>(ob + off * D + col0 + c * 32 * V));
         }
     };
     load(0);
     float M = -CUDART_INF_F;
-    if (S <= BO) {
+    if (T <= BO) {
         M = ml;
     } else {
-        for (int i = lane; i < S; i += 32) M = fmaxf(M, __ldcg(a.cslot_m + (i == 0 ? b0 : b1 + (i - 1) * st)));
+        for (int i = lane; i < T; i += 32) M = fmaxf(M, __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off_of(i)));
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
@@ -962,7 +1068,7 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
     for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[c][v] = 0.f;
-    for (int i0 = 0; i0 < S; i0 += BO) {
+    for (int i0 = 0; i0 < T; i0 += BO) {
         if (i0 > 0) load(i0);
         // lane-parallel weights, then broadcast per candidate
         const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - M);
@@ -973,7 +1079,7 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
 #pragma unroll
         for (int u = 0; u < BO; ++u) {
             const float e = __shfl_sync(0xffffffffu, e_l, u);
-            if (i0 + u < S) {
+            if (i0 + u < T) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const float* o = reinterpret_cast<const float*>(&ov[u][c]);
@@ -1033,8 +1139,10 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     // the other parity's pool counters are the next launch's: zero them
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
-             i += int64_t(gridDim.x) * blockDim.x)
+             i += int64_t(gridDim.x) * blockDim.x) {
             a.pool_next[i] = 0u;
+            if (a.fcnt_next) a.fcnt_next[i] = 0u;
+        }
     unsigned long long* ts = (a.dbg && w0 < 512 && (threadIdx.x & 31) == 0) ? a.dbg + 8 + 8 * w0 : nullptr;
     if (ts) {
         ts[0] = gtimer();
@@ -1045,7 +1153,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
         const int64_t orow = out_row_of(a, r);
         float l, m;
         LaneRow<V, NC> res;
-        merge_row_warp<V, NC, BO>(a, r, r == w0 ? cv0 : cover_of(a, r / a.group), res, l, m);
+        Cover cv = r == w0 ? cv0 : cover_of(a, r / a.group);
+        cv.nf = foreign_of(a, r / a.group);
+        merge_row_warp<V, NC, BO>(a, r, cv, res, l, m);
         store_row(t.out + orow * a.d, a.d, res);
         if (ts && r == w0) ts[2] = gtimer();
         if (t.mode == kTailPartial && (threadIdx.x & 31) == 0) {
@@ -1118,8 +1228,10 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     // the other parity's pool counters are the next launch's: zero them
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
-             i += int64_t(gridDim.x) * blockDim.x)
+             i += int64_t(gridDim.x) * blockDim.x) {
             a.pool_next[i] = 0u;
+            if (a.fcnt_next) a.fcnt_next[i] = 0u;
+        }
     const int D = a.d;
     const unsigned par = x.epoch & 1u;
     const int64_t stride = x.max_rows * int64_t(D + 1);  // words per (parity, source)
@@ -1130,7 +1242,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
         const int64_t orow = out_row_of(a, r);
         float l, m;
         LaneRow<V, NC> res;
-        merge_row_warp<V, NC, BO>(a, r, r == w0 ? cv0 : cover_of(a, r / a.group), res, l, m);
+        Cover cv = r == w0 ? cv0 : cover_of(a, r / a.group);
+        cv.nf = foreign_of(a, r / a.group);
+        merge_row_warp<V, NC, BO>(a, r, cv, res, l, m);
         if (ts && r == w0) ts[2] = gtimer();
         const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
         auto push = [&](uint2* dst) {  // LL words of this row into slot `rank` of one buffer
@@ -1402,9 +1516,21 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.epoch = p.epoch;
     a.bh_table = p.bh_table;
     if (p.pool_tiles > 0) {
-        unsigned* cnt = p.counters;  // [2 parities][bh_count]
+        unsigned* cnt = p.counters;  // [2 parities][bh_count] pool, then [2][bh_count] foreign
         a.pool_ctr = cnt + p.parity * p.bh_count;
         a.pool_next = cnt + (1 - p.parity) * p.bh_count;
+        a.fcnt = cnt + (2 + p.parity) * p.bh_count;
+        a.fcnt_next = cnt + (3 - p.parity) * p.bh_count;
+        a.fslots = p.fslots;
+        static const int scans = [] { const char* e = std::getenv("TD_STEAL_SCANS"); return e ? std::atoi(e) : 2; }();
+        static const int smin = [] { const char* e = std::getenv("TD_STEAL_MIN"); return e ? std::atoi(e) : 4; }();
+        a.steal_scans = scans;
+        a.steal_min = smin;
+        float* ff = cf + nc * (2 + int64_t(p.d));
+        const int64_t nf = p.bh_count * int64_t(p.fslots) * p.group;
+        a.fslot_m = ff;
+        a.fslot_l = ff + nf;
+        a.fslot_o = ff + 2 * nf;
     }
     return a;
 }
@@ -1520,6 +1646,17 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     p.pool_tiles = pool;
     p.pool_first = p.full_tiles_per_bh - pool;
     p.pool_chunk = pool_chunk;
+    // cross-row stealing pays on long shards (measured: -2 % at 1M tokens and on
+    // cfg4's 8.6 GB, +1-2 % at 131K, where the scans and the extra merge
+    // candidates cost more than the imbalance they remove): on when a CTA
+    // streams >= 1024 tiles; TD_STEAL_SLOTS forces the slot count (0 = off)
+    static const int fslots_env = [] {
+        const char* e = std::getenv("TD_STEAL_SLOTS");
+        return e ? std::max(0, std::atoi(e)) : -1;
+    }();
+    const int64_t tiles_per_cta = sm_count > 0 ? p.bh_count * p.full_tiles_per_bh / sm_count : 0;
+    const int fslots = fslots_env >= 0 ? fslots_env : (tiles_per_cta >= 1024 ? 16 : 0);
+    p.fslots = pool > 0 ? fslots : 0;
     p.tiles_per_bh = p.full_tiles_per_bh - pool;
     p.total_tiles = p.bh_count * p.tiles_per_bh;
     // one CTA per SM (the per-warp pipelines fill shared memory); without a

@@ -321,6 +321,20 @@ def test_worker_append_validation_and_output_buffers(td, oracle):
     w.close()
 
 
+def test_cross_row_stealing_parity(lib):
+    """Stealing (foreign states merged by K2) forced on small shards, in a
+    subprocess because the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TD_STEAL_SLOTS="16", TD_STEAL_MIN="1", TD_STEAL_SCANS="8")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "steal_check.py")], capture_output=True,
+                       text=True, timeout=600, env=env, cwd=root)
+    print(r.stdout[-2000:])
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
 def test_worker_place_matches_generate(td, oracle):
     import torch
     q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
