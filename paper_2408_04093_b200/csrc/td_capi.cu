@@ -174,11 +174,10 @@ struct td_context {
     int last_split_kernel = -1;
 
     // one-shot NVLink exchange (td_p2p_*)
-    DevBuf xbuf;                      // [2][p][max_rows*(d+1)] floats + flags [2][p][kXchgBlocks]
-    size_t x_data_bytes = 0;
+    DevBuf xbuf;                      // [2][p][max_rows][d + 1] LL words (value, epoch)
     int64_t x_max_rows = 0, x_d = 0;
     std::vector<void*> x_opened;      // IPC mappings to close
-    DevBuf x_ptrs;                    // device arrays: peers[p], peer_flags[p]
+    DevBuf x_ptrs;                    // device array: peers[p]
     DevBuf x_err;
     unsigned x_epoch = 0;
     bool x_ready = false;
@@ -796,13 +795,11 @@ int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char ha
     ctx->x_ready = false;
     // LL words (value, epoch): [2 parities][p sources][max_rows][d + 1] x 8 bytes
     const size_t data = 2 * size_t(ctx->nranks) * size_t(max_rows) * size_t(d + 1) * 2 * sizeof(float);
-    const size_t flags = 2 * size_t(ctx->nranks) * td::kXchgBlocks * sizeof(unsigned);
     ctx->xbuf.release();
-    TD_CUDA(ctx->xbuf.ensure(data + flags));
-    TD_CUDA(cudaMemset(ctx->xbuf.p, 0, data + flags));
+    TD_CUDA(ctx->xbuf.ensure(data));
+    TD_CUDA(cudaMemset(ctx->xbuf.p, 0, data));
     TD_CUDA(ctx->x_err.ensure(sizeof(int)));
     TD_CUDA(cudaMemset(ctx->x_err.p, 0, sizeof(int)));
-    ctx->x_data_bytes = data;
     ctx->x_max_rows = max_rows;
     ctx->x_d = d;
     ctx->x_epoch = 0;
@@ -830,11 +827,7 @@ int td_p2p_open(td_context* ctx, const unsigned char* handles) {
         ctx->x_opened.push_back(ptr);
         base[size_t(q)] = ptr;
     }
-    std::vector<void*> arr(2 * size_t(p));
-    for (int q = 0; q < p; ++q) {
-        arr[size_t(q)] = base[size_t(q)];
-        arr[size_t(p + q)] = static_cast<char*>(base[size_t(q)]) + ctx->x_data_bytes;
-    }
+    const std::vector<void*>& arr = base;
     TD_CUDA(ctx->x_ptrs.ensure(arr.size() * sizeof(void*)));
     TD_CUDA(cudaMemcpy(ctx->x_ptrs.p, arr.data(), arr.size() * sizeof(void*), cudaMemcpyHostToDevice));
     ctx->x_ready = true;
@@ -1094,8 +1087,6 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
             return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
         td::XchgArgs xa;
         xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
-        xa.peer_flags = reinterpret_cast<unsigned* const*>(static_cast<void**>(ctx->x_ptrs.p) + ctx->nranks);
-        xa.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ctx->xbuf.p) + ctx->x_data_bytes);
         xa.p = ctx->nranks;
         xa.rank = ctx->rank;
         xa.epoch = ++ctx->x_epoch;

@@ -101,12 +101,9 @@ cudaError_t launch_decode_final(const SplitPlan& plan, const void* q, const void
                                 cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // One-shot NVLink exchange buffers (td_p2p_*): every rank's exchange buffer
-// holds [2 parities][p sources][max_rows][d out | lse] LL words (value, epoch); flags
-// are [2][p][kXchgMaxBlocks] u32 per rank.
+// holds [2 parities][p sources][max_rows][d out | lse] LL words (value, epoch).
 struct XchgArgs {
     float* const* peers;       // device array [p]
-    unsigned* flags;           // own flags
-    unsigned* const* peer_flags;  // device array [p]
     int p = 1, rank = 0;
     unsigned epoch = 0;
     int64_t max_rows = 0;
@@ -114,7 +111,7 @@ struct XchgArgs {
     int* error = nullptr;
     int pull = 0;  // see k2_exchange
 };
-constexpr int kXchgBlocks = 1024;
+constexpr int kXchgBlocks = 1024;  // upper bound on K2x blocks
 
 // K1 + exchange tail: split-KV partial, merge, one-shot exchange and exact combine;
 // out [b, n_q, d] fp32 final (identical on every rank).

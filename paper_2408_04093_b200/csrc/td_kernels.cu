@@ -39,8 +39,6 @@ namespace td {
 // [max_rows][d out | lse] LL words (value bits, epoch) -- see k2_exchange.
 struct Xchg {
     float* const* peers;  // [p] exchange buffers (own included), device array
-    unsigned* flags;      // own flags
-    unsigned* const* peer_flags;
     int p, rank;
     unsigned epoch;
     int64_t max_rows;
@@ -1895,8 +1893,6 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.mode = kTailExchange;
     a.tail.out = out;
     a.tail.x.peers = xa.peers;
-    a.tail.x.flags = xa.flags;
-    a.tail.x.peer_flags = xa.peer_flags;
     a.tail.x.p = xa.p;
     a.tail.x.rank = xa.rank;
     a.tail.x.epoch = xa.epoch;
