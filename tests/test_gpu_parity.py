@@ -321,6 +321,24 @@ def test_worker_append_validation_and_output_buffers(td, oracle):
     w.close()
 
 
+def test_long_shard_default_path(td, oracle):
+    """A shard long enough (>= 1024 tiles per CTA) for the default to turn
+    cross-row stealing on, with the calibrated partition: the bench's N=1 path."""
+    n, n_q, n_kv = 655360, 32, 8
+    seed = oracle.mix64(0, n)
+    w = td.Worker(0)
+    w.generate_kv(td.DType(BF16), 1, n_kv, n, 128, oracle.mix64(seed, 2), oracle.mix64(seed, 3))
+    q = oracle.seeded(oracle.mix64(seed, 1), n_q * 128, BF16).reshape(1, n_q, 128)
+    outs = [w.tree_decode(dev(q, BF16)) for _ in range(3)]
+    g = n_q // n_kv
+    k0 = oracle.seeded(oracle.mix64(seed, 2), n * 128, BF16).reshape(1, 1, n, 128)
+    v0 = oracle.seeded(oracle.mix64(seed, 3), n * 128, BF16).reshape(1, 1, n, 128)
+    want = oracle.tree_decode(np.ascontiguousarray(q[:, :g]), k0, v0, 1, HIER, 1.0, F64, nthreads=16)
+    for o in outs:
+        assert rel_err(host(o[:, :g]), want) <= TOL[BF16]
+    w.close()
+
+
 def test_cross_row_stealing_parity(lib):
     """Stealing (foreign states merged by K2) forced on small shards, in a
     subprocess because the switch is read once per process."""
