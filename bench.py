@@ -88,6 +88,24 @@ def interconnect(args, world, b, n_q, n_kv, n, d, esz, ms):
     return {"kind": "nvlink", "bytes_per_rank_per_step": nbytes, "gbs": nbytes / (ms * 1e-3) / 1e9, "what": what}
 
 
+def read_ceiling(nbytes):
+    """The measured ceiling of a plain streaming-read kernel at the nearest
+    working-set size (scripts/read_probe.cu, profiles/r1_read_probe_noflush.jsonl):
+    MEASURED_PEAKS.json's HBM figure is a read+write copy, which a read-only
+    stream exceeds."""
+    path = os.path.join(ROOT, "profiles", "r1_read_probe_noflush.jsonl")
+    try:
+        rows = [json.loads(x) for x in open(path) if x.startswith("{")]
+    except OSError:
+        return None
+    if not rows:
+        return None
+    mb = nbytes / 1e6
+    near = min({r["mb"] for r in rows}, key=lambda m: abs(m - mb))
+    best = max(r["best_gbs"] for r in rows if r["mb"] == near)
+    return {"gbs": best, "at_mb": near, "source": "profiles/r1_read_probe_noflush.jsonl (best of the variants)"}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -433,7 +451,8 @@ def main():
                          "kernel": {1: "k1_bf16 (split-KV, TMA + mma.sync)", 2: "k1_f32 (split-KV, bulk copy)",
                                     0: "k1_generic"}.get(split_kernel), "kernel_ms": k1_ms_max,
                          "bytes_per_launch": kv_per_rank, "peak_kind": peak_kind,
-                         "step_frac": kv_per_rank / (ms * 1e-3) / 1e9 / peak},
+                         "step_frac": kv_per_rank / (ms * 1e-3) / 1e9 / peak,
+                         "read_ceiling": read_ceiling(kv_per_rank)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms * 1000.0 / b, "unit": "µs/token",
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
