@@ -199,10 +199,14 @@ struct td_context {
     struct PartTab {
         int64_t total = -1, per_bh = 0, bh = 0;
         int ctas = 0, maxseg = 0;
-        DevBuf buf;  // int64 x[ctas + 1] then int bh[3 * bh_count]
+        DevBuf buf;                   // int64 x[ctas + 1] then int bh[3 * bh_count]
+        void* host = nullptr;         // pinned staging of the tables (async upload)
+        size_t host_cap = 0;
+        cudaEvent_t used = nullptr;   // after the last launch that read buf
     };
     PartTab tabs[4];
     int tab_next = 0;
+    unsigned tabs_touched = 0;        // entries selected since the last note_table_use
 
     bool det = false;  // this call: static split only (TD_DETERMINISTIC)
     DevBuf ctr;        // K1 dynamic-pool counters (SplitPlan::counters)
@@ -260,25 +264,55 @@ bool sm_affinity_enabled() {
 }
 
 // Device tables of the speed-weighted static partition of `plan` (cached).
+// After the launches of a call: the selected partition tables are in use up to here.
+int note_table_use(td_context* ctx) {
+    for (int i = 0; i < 4; ++i) {
+        if (!(ctx->tabs_touched & (1u << i))) continue;
+        auto& tb = ctx->tabs[i];
+        if (!tb.used) TD_CUDA(cudaEventCreateWithFlags(&tb.used, cudaEventDisableTiming));
+        TD_CUDA(cudaEventRecord(tb.used, ctx->stream));
+    }
+    ctx->tabs_touched = 0;
+    return TD_OK;
+}
+
 int apply_partition(td_context* ctx, SplitPlan& plan) {
-    for (auto& tb : ctx->tabs)
+    for (int i = 0; i < 4; ++i) {
+        auto& tb = ctx->tabs[i];
         if (tb.total == plan.total_tiles && tb.per_bh == plan.tiles_per_bh && tb.bh == plan.bh_count &&
             tb.ctas == plan.ctas) {
             plan.maxseg = std::max(plan.maxseg, tb.maxseg);
             plan.x_table = static_cast<const int64_t*>(tb.buf.p);
             plan.bh_table = reinterpret_cast<const int*>(static_cast<const int64_t*>(tb.buf.p) + plan.ctas + 1);
+            ctx->tabs_touched |= 1u << i;
             return TD_OK;
         }
-    auto& tb = ctx->tabs[ctx->tab_next];
+    }
+    const int idx = ctx->tab_next;
+    auto& tb = ctx->tabs[idx];
     ctx->tab_next = (ctx->tab_next + 1) % 4;
     std::vector<int64_t> x(size_t(plan.ctas) + 1);
     std::vector<int> bh(3 * size_t(plan.bh_count));
     td::build_partition(plan, ctx->cal_w.data(), x.data(), bh.data());
     const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
-    TD_CUDA(cudaStreamSynchronize(ctx->stream));  // the buffer may still be read by a launch
+    // no stream drain when the sequence grows (a new shape every 32 appended tokens):
+    // wait only for the last launch that read this entry, then upload from pinned
+    // staging on the stream, ahead of the launch that will read it
+    if (tb.used) TD_CUDA(cudaEventSynchronize(tb.used));
+    if (tb.host_cap < xb + bb) {  // pinned allocations can stall the device: size generously, once
+        if (tb.host) cudaFreeHost(tb.host);
+        tb.host = nullptr;
+        tb.host_cap = 0;
+        const size_t want = std::max<size_t>(xb + bb, 64 * 1024);
+        TD_CUDA(cudaMallocHost(&tb.host, want));
+        tb.host_cap = want;
+    }
+    if (tb.buf.cap < xb + bb) TD_CUDA(tb.buf.ensure(std::max<size_t>(xb + bb, 64 * 1024)));
+    std::memcpy(tb.host, x.data(), xb);
+    std::memcpy(static_cast<char*>(tb.host) + xb, bh.data(), bb);
     TD_CUDA(tb.buf.ensure(xb + bb));
-    TD_CUDA(cudaMemcpy(tb.buf.p, x.data(), xb, cudaMemcpyHostToDevice));
-    TD_CUDA(cudaMemcpy(static_cast<char*>(tb.buf.p) + xb, bh.data(), bb, cudaMemcpyHostToDevice));
+    TD_CUDA(cudaMemcpyAsync(tb.buf.p, tb.host, xb + bb, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->tabs_touched |= 1u << idx;
     tb.total = plan.total_tiles;
     tb.per_bh = plan.tiles_per_bh;
     tb.bh = plan.bh_count;
@@ -395,7 +429,23 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
     plan.row_stride = stride;
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
         if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
-            if (calibrate(ctx, n_q) != TD_OK) ctx->cal_failed = true;  // keep the equal split
+            if (calibrate(ctx, n_q) != TD_OK) {
+                ctx->cal_failed = true;  // keep the equal split
+            } else {
+                // staging and device space for the partition tables now, not when a
+                // growing sequence changes the shape mid-loop (pinned allocation stalls)
+                const size_t need = std::max<size_t>(64 * 1024, (size_t(plan.ctas) + 1) * 8 + 12 * size_t(plan.bh_count));
+                for (auto& tb : ctx->tabs) {
+                    if (tb.host_cap < need) {
+                        if (tb.host) cudaFreeHost(tb.host);
+                        tb.host = nullptr;
+                        tb.host_cap = 0;
+                        TD_CUDA(cudaMallocHost(&tb.host, need));
+                        tb.host_cap = need;
+                    }
+                    TD_CUDA(tb.buf.ensure(need));
+                }
+            }
         }
         if (ctx->cal_w.size() == size_t(plan.ctas)) {
             if (int rc = apply_partition(ctx, plan)) return rc;
@@ -518,6 +568,7 @@ float* mapped_host(td_context* ctx, float* host) {
 }
 
 int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int flags) {
+    if (int rc = note_table_use(ctx)) return rc;
     const size_t bytes = size_t(rows) * size_t(ctx->d) * sizeof(float);
     if (flags & TD_BF16_OUT) {
         TD_CUDA(ctx->out_bf16.ensure(size_t(rows) * size_t(ctx->d) * 2));
@@ -741,7 +792,11 @@ int td_destroy(td_context* ctx) {
     ctx->sm_map.release();
     ctx->claims.release();
     ctx->cal_q.release();
-    for (auto& tb : ctx->tabs) tb.buf.release();
+    for (auto& tb : ctx->tabs) {
+        tb.buf.release();
+        if (tb.host) cudaFreeHost(tb.host);
+        if (tb.used) cudaEventDestroy(tb.used);
+    }
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->xfer);
     delete ctx;
@@ -971,11 +1026,15 @@ int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host) {
     const size_t esz = td::dtype_bytes(ctx->dtype);
     const size_t tok = size_t(ctx->d) * esz, pitch = size_t(ctx->cap) * tok;
     const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
-    const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->k.p) + size_t(ctx->len) * tok, pitch, k, tok, tok, rows,
-                              kind, ctx->stream));
-    TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->v.p) + size_t(ctx->len) * tok, pitch, v, tok, tok, rows,
-                              kind, ctx->stream));
+    if (from_host) {
+        TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->k.p) + size_t(ctx->len) * tok, pitch, k, tok, tok, rows,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+        TD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->v.p) + size_t(ctx->len) * tok, pitch, v, tok, tok, rows,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    } else {  // a kernel: keeps the programmatic-launch chain of a decode loop
+        TD_CUDA(td::launch_kv_append(ctx->dtype, ctx->k.p, ctx->v.p, k, v, int64_t(rows), ctx->cap, ctx->len,
+                                     static_cast<int>(ctx->d), ctx->stream));
+    }
     ctx->len += 1;
     ctx->seq_len += 1;
     ctx->lens.back() += 1;
@@ -1197,6 +1256,7 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
                           host ? ctx->r_max : row_max, host ? ctx->r_lse : lse,
                           host ? ctx->r_out : out, (flags & TD_TIME_KERNELS) != 0)))
         return rc;
+    if ((rc = note_table_use(ctx))) return rc;
     if (host) {
         TD_CUDA(cudaMemcpyAsync(row_max, ctx->r_max, rows * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         TD_CUDA(cudaMemcpyAsync(lse, ctx->r_lse, rows * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));

@@ -143,6 +143,10 @@ cudaError_t launch_combine_partials(int P, const float* lse, const float* out, i
 cudaError_t launch_seeded_fill(int dtype, void* dst, uint64_t seed, double scale,
                                int64_t bh_count, int64_t seq, int64_t start, int64_t len,
                                int64_t d, cudaStream_t stream);
+// KV append from device memory: token rows kt/vt [rows][d] into position pos
+// of the [rows][cap][d] shard (programmatic launch, see td_kernels.cu).
+cudaError_t launch_kv_append(int dtype, void* k, void* v, const void* kt, const void* vt, int64_t rows,
+                             int64_t cap, int64_t pos, int d, cudaStream_t stream);
 // Energy formulation (energy.cpp:152-259), see td_kernels.cu.
 cudaError_t launch_energy_combine(int P, const float* rmax, const float* lse, int64_t rows, float* value,
                                   float* rmax_out, float* shifted, cudaStream_t stream);

@@ -2042,6 +2042,34 @@ cudaError_t launch_energy_logz(const float* rmax, const float* shifted, int64_t 
     return cudaGetLastError();
 }
 
+// ---- KV append: one new token per (b, kv-head) row ---------
+// A kernel rather than two strided copies so that it keeps the stream's
+// programmatic-launch chain: it starts under the previous step's K2 and the
+// next K1 starts under it. Row r of the shard receives the token at position
+// pos (rows are cap tokens apart).
+__global__ void k_kv_append(uint16_t* kc, uint16_t* vc, const uint16_t* kt, const uint16_t* vt, int64_t rows,
+                            int64_t pitch, int64_t pos, int words) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t n = rows * words;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / words, j = i - r * words;
+        const int64_t dst = r * pitch + pos * words + j;
+        kc[dst] = kt[i];
+        vc[dst] = vt[i];
+    }
+}
+
+cudaError_t launch_kv_append(int dtype, void* k, void* v, const void* kt, const void* vt, int64_t rows,
+                             int64_t cap, int64_t pos, int d, cudaStream_t st) {
+    const int words = d * dtype_bytes(dtype) / 2;  // 16-bit words per token row
+    const int64_t n = rows * words;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1024));
+    return launch_pdl(k_kv_append, grid < 1 ? 1 : grid, 256, 0, st, static_cast<uint16_t*>(k),
+                      static_cast<uint16_t*>(v), static_cast<const uint16_t*>(kt), static_cast<const uint16_t*>(vt),
+                      rows, cap * words, pos, words);
+}
+
 cudaError_t launch_seeded_fill(int dtype, void* dst, uint64_t seed, double scale,
                                int64_t bh_count, int64_t seq, int64_t start, int64_t len,
                                int64_t d, cudaStream_t st) {

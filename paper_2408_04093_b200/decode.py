@@ -483,6 +483,7 @@ class Worker:
         self.h = h
         self.device = device
         self._pending = []  # device tensors an enqueued td_kv_append still reads
+        self._xs = None     # torch handle of the worker's stream (created on first use)
         self.nranks, self.rank = 1, 0
         if comm is not None:
             nranks, rank, uid = comm
@@ -529,9 +530,15 @@ class Worker:
             lib().td_destroy(self.h)  # synchronizes the worker's streams
             self.h = None
         self._pending = []
+        self._xs = None
+
+    def _worker_stream(self):
+        if self._xs is None:
+            self._xs = _torch().cuda.ExternalStream(self.stream, device=self.device)
+        return self._xs
 
     def _sync_worker(self):
-        _torch().cuda.ExternalStream(self.stream).synchronize()
+        self._worker_stream().synchronize()
         self._pending.clear()
 
     def __del__(self):
@@ -579,12 +586,11 @@ class Worker:
             if k.numel() != self.b * self.n_kv * self.d or v.numel() != k.numel():
                 raise InvalidArgument(_capi.TD_EINVAL, "append_kv: token must be [b, n_kv, 1, d]")
             k, v = k.contiguous(), v.contiguous()
-            self._sync_in(k)
-            self._sync_in(v)
+            self._sync_in(k)  # k and v come from the same (current) stream
             check(lib().td_kv_append(self.h, k.data_ptr(), v.data_ptr(), 0 if k.is_cuda else 1))
             if k.is_cuda:  # the copy runs on the worker's stream: hold the sources until it is synced
                 self._pending.append((k, v))
-                if len(self._pending) > 64:
+                if len(self._pending) > 256:
                     self._sync_worker()
         else:
             check(lib().td_kv_append(self.h, None, None, 1))
@@ -632,8 +638,14 @@ class Worker:
         return s.value, n.value, nb.value
 
     def _sync_in(self, x):
+        """Order the worker's stream after the work already queued on torch's
+        current stream (which produced x): an event wait on the device, no host
+        block."""
         if x is not None and x.is_cuda:
-            _torch().cuda.current_stream().synchronize()
+            torch = _torch()
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(x.device))
+            self._worker_stream().wait_event(ev)
 
     def _decode(self, fn, q, scale, out, flags, *extra):
         torch = _torch()

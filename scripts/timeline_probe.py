@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--b", type=int, default=1)
     ap.add_argument("--nq", type=int, default=32)
     ap.add_argument("--nkv", type=int, default=8)
+    ap.add_argument("--append", action="store_true", help="append one token before every step")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -44,7 +45,13 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if args.append:
+        w.reserve_kv(args.steps + 8)
+        tok = td.seeded_tensor([args.b, args.nkv, 128], 9, 1.0, td.DType.Bf16)
+        torch.cuda.synchronize()
     for _ in range(args.steps):
+        if args.append:
+            w.append_kv(tok, tok)
         w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
     torch.cuda.synchronize()
     st = w.debug_stamps(6144)
