@@ -458,6 +458,7 @@ def main():
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
                     "matches_device_output": bool(ok)},
             "interconnect": interconnect(args, world, b, n_q, n_kv, n, d, esz, ms),
+            "calibration": dict(zip(("gain", "state"), w.calibration_info())),
             "phases_us": phases,
             "gpu_launches": kernels_per_step * args.steps,
             "kernels_per_step": kernels_per_step,

@@ -201,6 +201,12 @@ int td_energy_forward(td_context* ctx, const void* q, const void* src, int64_t n
 int td_energy_grad(td_context* ctx, const void* q, int64_t nq, const float* row_max,
                    const float* shifted, float* grad, int flags);
 
+/* The per-SM speed calibration of the split kernel's static partition (made on
+ * the first long decode of a context): gain = measured K1 time saved over the
+ * equal split (fraction); state -1 failed, 0 not run, 1 kept equal weights
+ * (gain too small), 2 weights in use. */
+int td_calibration_info(td_context* ctx, double* gain, int* state);
+
 /* Shard geometry of the placed cache. */
 int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes);
 /* Device pointers of the placed shard (for tests). */

@@ -25,7 +25,7 @@ EXPORTS = [
     "td_comm_info", "td_p2p_handle", "td_p2p_open", "td_p2p_status", "td_kv_place", "td_kv_generate", "td_kv_info", "td_kv_pointers",
     "td_kv_append", "td_kv_reserve",
     "td_energy_workspace_bytes", "td_energy_partial", "td_energy_combine", "td_energy_grad_combine",
-    "td_energy_forward", "td_energy_grad",
+    "td_energy_forward", "td_energy_grad", "td_calibration_info",
     "td_tree_decode", "td_ring_decode", "td_local_partial", "td_output_bf16", "td_kernel_time",
     "td_reset_kernel_timer", "td_phase_times", "td_debug_stamps", "td_last_launch_stats", "td_memory_bytes",
 ]
@@ -99,6 +99,7 @@ def lib() -> ctypes.CDLL:
     L.td_energy_grad_combine.argtypes = [ctypes.c_int] + [_vp] * 4 + [_i64, _i64, _vp, _vp]
     L.td_energy_forward.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.c_int]
     L.td_energy_grad.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, ctypes.c_int]
+    L.td_calibration_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
     L.td_tree_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_int, _vp, ctypes.c_int]
     L.td_ring_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, ctypes.c_int]
     L.td_local_partial.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, ctypes.c_int]

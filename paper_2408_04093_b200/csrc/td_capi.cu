@@ -192,6 +192,7 @@ struct td_context {
     // (blocks land on the same SMs launch after launch), measured once
     std::vector<float> cal_w;
     bool cal_failed = false;
+    double cal_gain = 0.0;      // measured K1 gain of the weights over the equal split
     DevBuf sm_map, claims;      // SM affinity of the calibrated CTA indices
     bool sm_map_ok = false;
     unsigned claim_epoch = 0;
@@ -341,79 +342,121 @@ int calibrate(td_context* ctx, int64_t n_q) {
         return set_err(TD_EINVAL, "calibration not applicable");
     p.row_stride = ctx->cap;
     const int G = p.ctas;
+    if (G > 1024) return set_err(TD_EINVAL, "calibration: too many CTAs");
     const int64_t rows = ctx->b * n_q;
     if (int rc = ensure_rows(ctx, rows, ctx->d)) return rc;
     TD_CUDA(ctx->cal_q.ensure(size_t(rows) * size_t(ctx->d) * 2));
     TD_CUDA(cudaMemsetAsync(ctx->cal_q.p, 0, size_t(rows) * size_t(ctx->d) * 2, ctx->stream));
     TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
-    std::vector<float> w(size_t(G), 1.f);
     std::vector<unsigned long long> st(6144);
-    for (int round = 0; round < 2; ++round) {
+    DevBuf tab;
+    // one static-split launch under weights w (per CTA index); stamps into st;
+    // returns the span first CTA start -> last CTA end (ns)
+    auto run = [&](const std::vector<float>& w, const int* sm_to_cta, unsigned epoch, std::vector<int64_t>& x,
+                   double& span) -> int {
         SplitPlan pr = p;
-        std::vector<int64_t> x(size_t(G) + 1);
+        x.assign(size_t(G) + 1, 0);
         std::vector<int> bh(3 * size_t(pr.bh_count));
         td::build_partition(pr, w.data(), x.data(), bh.data());
-        DevBuf tab;
         const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
         TD_CUDA(tab.ensure(xb + bb));
         TD_CUDA(cudaMemcpy(tab.p, x.data(), xb, cudaMemcpyHostToDevice));
         TD_CUDA(cudaMemcpy(static_cast<char*>(tab.p) + xb, bh.data(), bb, cudaMemcpyHostToDevice));
         pr.x_table = static_cast<const int64_t*>(tab.p);
         pr.bh_table = reinterpret_cast<const int*>(static_cast<const int64_t*>(tab.p) + G + 1);
+        pr.sm_to_cta = sm_to_cta;
+        pr.claims = static_cast<unsigned*>(ctx->claims.p);
+        pr.epoch = epoch;
         TD_CUDA(ctx->ws.ensure(pr.workspace_bytes()));
-        std::vector<double> dur(size_t(G), 0.0);
-        cudaError_t e = cudaSuccess;
-        for (int rep = 0; rep < 3 && e == cudaSuccess; ++rep) {
-            e = cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream);
-            td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
-            if (e == cudaSuccess)
-                e = td::launch_decode_partial(pr, ctx->cal_q.p, ctx->k.p, ctx->v.p, 1.0f, &ctx->tmk, &ctx->tmv,
-                                              ctx->ws.p, ctx->r_max, ctx->r_lse, ctx->r_out, ctx->stream);
-            td::set_debug_stamps(nullptr);
-            if (e == cudaSuccess)
-                e = cudaMemcpyAsync(st.data(), ctx->dbg.p, st.size() * sizeof(unsigned long long),
-                                    cudaMemcpyDeviceToHost, ctx->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-            if (rep == 0) continue;  // the first launch pays cold-start effects
-            for (int c = 0; c < G && c < 1024; ++c)
-                if (st[4097 + 2 * c] > st[4096 + 2 * c]) dur[size_t(c)] += double(st[4097 + 2 * c] - st[4096 + 2 * c]);
-        }
-        tab.release();
+        TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream));
+        TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xff, sizeof(unsigned long long), ctx->stream));
+        td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
+        const cudaError_t e = td::launch_decode_partial(pr, ctx->cal_q.p, ctx->k.p, ctx->v.p, 1.0f, &ctx->tmk,
+                                                        &ctx->tmv, ctx->ws.p, ctx->r_max, ctx->r_lse, ctx->r_out,
+                                                        ctx->stream);
+        td::set_debug_stamps(nullptr);
         TD_CUDA(e);
+        TD_CUDA(cudaMemcpyAsync(st.data(), ctx->dbg.p, st.size() * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        TD_CUDA(cudaStreamSynchronize(ctx->stream));
+        span = st[1] > st[0] ? double(st[1] - st[0]) : 0.0;
+        return TD_OK;
+    };
+    TD_CUDA(ctx->claims.ensure(size_t(G) * sizeof(unsigned)));
+    TD_CUDA(cudaMemset(ctx->claims.p, 0, size_t(G) * sizeof(unsigned)));
+    // 1. per-SM streaming speed: tiles / (end - start) of each CTA, indexed by the
+    // SM it ran on (the SM, not the block index, is what is fast or slow), over
+    // 3 rounds x 3 measured launches; each round re-weights the ranges
+    std::vector<double> sp_sum(1024, 0.0);
+    std::vector<int> sp_n(1024, 0);
+    std::vector<float> w(size_t(G), 1.f);
+    std::vector<int64_t> x;
+    std::vector<int> smid_of(size_t(G), -1);
+    double span = 0.0;
+    for (int round = 0; round < 3; ++round) {
+        for (int rep = 0; rep < 4; ++rep) {
+            if (int rc = run(w, nullptr, 0, x, span)) return rc;
+            if (rep == 0) continue;  // the first launch of a layout pays cold-start effects
+            for (int c = 0; c < G; ++c) {
+                const unsigned long long t0 = st[4096 + 2 * size_t(c)], t1 = st[4097 + 2 * size_t(c)];
+                const unsigned long long sm = st[2048 + size_t(c)];
+                const int64_t tiles = x[size_t(c) + 1] - x[size_t(c)];
+                if (t1 > t0 && tiles > 0 && sm < 1024) {
+                    sp_sum[size_t(sm)] += double(tiles) / double(t1 - t0);
+                    ++sp_n[size_t(sm)];
+                }
+                smid_of[size_t(c)] = sm < 1024 ? static_cast<int>(sm) : -1;
+            }
+        }
         double mean = 0.0;
         int n = 0;
-        std::vector<double> speed(size_t(G), 0.0);
         for (int c = 0; c < G; ++c) {
-            const int64_t tiles = x[size_t(c) + 1] - x[size_t(c)];
-            if (tiles > 0 && dur[size_t(c)] > 0) {
-                speed[size_t(c)] = double(tiles) / dur[size_t(c)];
-                mean += speed[size_t(c)];
+            const int sm = smid_of[size_t(c)];
+            if (sm >= 0 && sp_n[size_t(sm)] > 0) {
+                mean += sp_sum[size_t(sm)] / sp_n[size_t(sm)];
                 ++n;
             }
         }
         if (n == 0) return set_err(TD_ECUDA, "calibration: no stamps");
         mean /= n;
-        for (int c = 0; c < G; ++c)
-            w[size_t(c)] = speed[size_t(c)] > 0 ? static_cast<float>(std::min(1.5, std::max(0.5, speed[size_t(c)] / mean)))
-                                                 : w[size_t(c)];
+        for (int c = 0; c < G; ++c) {
+            const int sm = smid_of[size_t(c)];
+            if (sm >= 0 && sp_n[size_t(sm)] > 0)
+                w[size_t(c)] = static_cast<float>(std::min(1.5, std::max(0.5, sp_sum[size_t(sm)] / sp_n[size_t(sm)] / mean)));
+        }
     }
-    ctx->cal_w = w;
-    // SM affinity from the last round's stamps (dbg[2048 + c] = %smid of CTA c)
+    // 2. SM affinity: index c belongs to the SM it ran on in the last launch
     std::vector<int> m(1024, -1);
     bool ok = true;
     for (int c = 0; c < G && ok; ++c) {
-        const unsigned long long sm = st[2048 + size_t(c)];
-        if (c >= 1024 || sm >= 1024 || m[size_t(sm)] != -1) ok = false;
+        const int sm = smid_of[size_t(c)];
+        if (sm < 0 || m[size_t(sm)] != -1) ok = false;
         else m[size_t(sm)] = c;
     }
     ctx->sm_map_ok = false;
-    if (ok) {
-        TD_CUDA(ctx->sm_map.ensure(m.size() * sizeof(int)));
-        TD_CUDA(cudaMemcpy(ctx->sm_map.p, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice));
-        TD_CUDA(ctx->claims.ensure(size_t(G) * sizeof(unsigned)));
-        TD_CUDA(cudaMemset(ctx->claims.p, 0, size_t(G) * sizeof(unsigned)));
-        ctx->sm_map_ok = true;
+    if (!ok) return set_err(TD_ECUDA, "calibration: CTAs did not land one per SM");
+    TD_CUDA(ctx->sm_map.ensure(m.size() * sizeof(int)));
+    TD_CUDA(cudaMemcpy(ctx->sm_map.p, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice));
+    // 3. keep the weights only if they beat the equal split (median of 5 launches
+    // each, with the SM affinity the real launches use): a noisy calibration must
+    // never cost time
+    const int* smap = static_cast<const int*>(ctx->sm_map.p);
+    const std::vector<float> ones(size_t(G), 1.f);
+    std::vector<double> t_eq, t_cal;
+    unsigned epoch = 1;
+    for (int rep = 0; rep < 6; ++rep) {
+        if (int rc = run(ones, smap, epoch++, x, span)) return rc;
+        if (rep) t_eq.push_back(span);
+        if (int rc = run(w, smap, epoch++, x, span)) return rc;
+        if (rep) t_cal.push_back(span);
     }
+    std::sort(t_eq.begin(), t_eq.end());
+    std::sort(t_cal.begin(), t_cal.end());
+    TD_CUDA(cudaMemset(ctx->claims.p, 0, size_t(G) * sizeof(unsigned)));
+    tab.release();
+    ctx->cal_gain = t_eq.empty() ? 0.0 : (t_eq[t_eq.size() / 2] - t_cal[t_cal.size() / 2]) / t_eq[t_eq.size() / 2];
+    ctx->cal_w = ctx->cal_gain > 0.005 ? w : ones;  // equal weights: the affinity alone stays harmless
+    ctx->sm_map_ok = true;
     return TD_OK;
 }
 
@@ -1424,6 +1467,13 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
 int td_output_bf16(td_context* ctx, const void** out_bf16) {
     if (int rc = require_ctx(ctx)) return rc;
     *out_bf16 = ctx->out_bf16.p;
+    return TD_OK;
+}
+
+int td_calibration_info(td_context* ctx, double* gain, int* state) {
+    if (int rc = require_ctx(ctx)) return rc;
+    *gain = ctx->cal_gain;
+    *state = ctx->cal_failed ? -1 : (ctx->cal_w.empty() ? 0 : (ctx->cal_gain > 0.005 ? 2 : 1));
     return TD_OK;
 }
 

@@ -629,6 +629,13 @@ class Worker:
         self._sync_worker()
         return grad
 
+    def calibration_info(self):
+        """(gain, state): K1 time the per-SM calibration saves over the equal split
+        and whether its weights are in use (2), kept equal (1), not run (0) or failed (-1)."""
+        g, st = self._ct.c_double(), self._ct.c_int()
+        check(lib().td_calibration_info(self.h, self._ct.byref(g), self._ct.byref(st)))
+        return g.value, st.value
+
     def reserve_kv(self, tokens: int):
         check(lib().td_kv_reserve(self.h, int(tokens)))
 
