@@ -484,6 +484,7 @@ class Worker:
         self.device = device
         self._pending = []  # device tensors an enqueued td_kv_append still reads
         self._xs = None     # torch handle of the worker's stream (created on first use)
+        self._ev = None     # input-ordering event (created on first use)
         self.nranks, self.rank = 1, 0
         if comm is not None:
             nranks, rank, uid = comm
@@ -531,6 +532,7 @@ class Worker:
             self.h = None
         self._pending = []
         self._xs = None
+        self._ev = None
 
     def _worker_stream(self):
         if self._xs is None:
@@ -650,9 +652,10 @@ class Worker:
         block."""
         if x is not None and x.is_cuda:
             torch = _torch()
-            ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(x.device))
-            self._worker_stream().wait_event(ev)
+            if self._ev is None:  # one event, re-recorded: wait_event captures each recording
+                self._ev = torch.cuda.Event()
+            self._ev.record(torch.cuda.current_stream(x.device))
+            self._worker_stream().wait_event(self._ev)
 
     def _decode(self, fn, q, scale, out, flags, *extra):
         torch = _torch()
