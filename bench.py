@@ -193,6 +193,17 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def barrier(world):
     import torch
     torch.cuda.synchronize()
@@ -274,7 +285,7 @@ def run_reference_arm(args, wl, world, rank):
         "config": {"workload": args.workload, "seq_len": args.seq_len or n, "batch": b, "q_heads": n_q,
                    "kv_heads": n_kv, "head_dim": d, "shards": args.gpus, "algo": "tree"},
         "cpu_baseline": {"value": value, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
-                         "sample": info["sample"] + f"; host nproc={nproc}"},
+                         "sample": info["sample"] + f"; host nproc={nproc}, {cpu_model()}"},
         "e2e": {"value": value, "unit": "µs/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(time.time() - t0, 1),
     }
@@ -384,6 +395,9 @@ def main():
     k1_ms, k1_calls = w.kernel_time()
     kernels_per_step, kv_bytes_step, split_kernel = w.last_launch_stats()
     ms = max_over_ranks(ms_local, world)
+    lib_bytes = max_over_ranks(float(w.memory_bytes()), world)
+    free_b, total_b = torch.cuda.mem_get_info()
+    used_max = max_over_ranks(float(total_b - free_b), world)
     k1_ms_max = max_over_ranks(k1_ms, world)
 
     # ---- end-to-end through the public API with host buffers (pinned)
@@ -424,7 +438,10 @@ def main():
             heads = args.cpu_sample_heads or min(b * n_q, os.cpu_count() or 1)
             vals, info = reference_cpu(args, wl, 1, heads, os.cpu_count() or 1, steps=3)
             cpu = {"value": min(vals), "unit": "µs/token", "cores": info["cores"], "kind": "reference",
-                   "sample": info["sample"] + f"; host nproc={os.cpu_count()}"}
+                   "sample": info["sample"] + f"; host nproc={os.cpu_count()}, {cpu_model()}"}
+            # the same reference, one row on one thread (threads=p and 1)
+            vals1, info1 = reference_cpu(args, wl, 1, 1, 1, steps=2)
+            cpu["one_thread"] = {"value": min(vals1), "cores": 1, "sample": info1["sample"]}
         except Exception as e:  # the reference library may be absent on a foreign box
             cpu = {"value": None, "unit": "µs/token", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -442,6 +459,7 @@ def main():
                        "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": shard_len,
                        "algo": args.algo, "combine": args.combine if world > 1 and args.algo == "tree" else "none",
                        "scale": args.scale,
+                       "nccl_algo": os.environ.get("NCCL_ALGO", "auto") if world > 1 else None,
                        "l2": "flushed between steps" if flush else "inputs larger than L2 (KV shard > 4x126 MB)",
                        "parallelism": f"sp{world} (sequence-sharded KV)"},
             "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
@@ -458,6 +476,8 @@ def main():
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
                     "matches_device_output": bool(ok)},
             "interconnect": interconnect(args, world, b, n_q, n_kv, n, d, esz, ms),
+            "memory": {"library_bytes_max_rank": int(lib_bytes), "device_used_bytes_max_rank": int(used_max),
+                       "kv_bytes_per_rank": kv_per_rank},
             "calibration": dict(zip(("gain", "state"), w.calibration_info())),
             "phases_us": phases,
             "gpu_launches": kernels_per_step * args.steps,
