@@ -147,6 +147,10 @@ struct td_context {
     int dtype = td::kBF16;
     int64_t b = 0, n_kv = 0, seq_len = 0, d = 0, start = 0, len = 0;
     int64_t cap = 0;  // tokens per bh row allocated (>= len: room for td_kv_append)
+    // tokens of every row that no kernel still in flight may be writing: the whole
+    // cache after a synchronising placement, else the length the last decode's K1
+    // saw (appends write past it); SplitPlan::t_safe
+    int64_t kv_safe = 0;
     std::vector<int64_t> lens;  // every rank's shard length (chunk_extents, then appends on rank p-1)
     DevBuf k, v;
     CUtensorMap tmk{}, tmv{};
@@ -470,6 +474,7 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
                         static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det, generic_only))
         return set_err(TD_EINVAL, msg);
     plan.row_stride = stride;
+    plan.t_safe = stride > 0 ? std::min(ctx->kv_safe, t) : 0;  // the context's own cache only
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
         if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
             if (calibrate(ctx, n_q) != TD_OK) {
@@ -575,6 +580,7 @@ int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const voi
     }
     TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
                                       ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
+    if (kb == ctx->k.p && plan.row_stride > 0) ctx->kv_safe = t;  // later K1s run after this one's wait
     ctx->last_kernels += 2;  // K1 + K2
     ctx->last_kv_bytes += 2.0 * double(ctx->b) * double(ctx->n_kv) * double(t) * double(ctx->d) *
                           td::dtype_bytes(ctx->dtype);
@@ -964,6 +970,7 @@ static int kv_alloc(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t
     ctx->lens = chunk_extents(seq_len, ctx->nranks);
     ctx->kv_ok = false;
     ctx->tm_ok = false;
+    ctx->kv_safe = 0;
     return TD_OK;
 }
 
@@ -984,6 +991,7 @@ static int kv_finish(td_context* ctx) {
     }
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->kv_ok = true;
+    ctx->kv_safe = ctx->len;
     return TD_OK;
 }
 
@@ -1214,6 +1222,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         }
         TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                            ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
+        ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
         phase_mark(ctx);
         ctx->last_kernels = 2;  // K1 + K2x
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *

@@ -41,6 +41,12 @@ struct SplitPlan {
     // any row's pool and fold them into one of that row's fslots foreign states
     // ([bh_count][fslots]; 0 = off)
     int fslots = 0;
+    // tokens of every row that no kernel ahead of this launch on the stream may
+    // still be writing (0: none). k1_bf16 loads its first tiles below it before
+    // griddepcontrol.wait. Set only for the context's own cache (td_capi.cu
+    // kv_safe): everything up to the last decode's length, or all of it after
+    // a synchronising placement.
+    int64_t t_safe = 0;
     // calibrated static partition (device tables, optional; see
     // build_partition): CTA c owns static tiles [x_table[c], x_table[c+1])
     const int64_t* x_table = nullptr;

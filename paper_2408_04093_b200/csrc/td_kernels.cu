@@ -63,6 +63,8 @@ struct K1Args {
     const void* v;
     int64_t bh_count, t, tiles_per_bh, total_tiles;
     int64_t row_stride;  // tokens between consecutive bh rows in memory (>= t: append capacity)
+    int64_t t_safe;      // tokens of every row no kernel ahead of this grid may still be writing
+                         // (SplitPlan::t_safe): their tiles may be loaded before the PDL wait
     int d, n_q, n_kv, group, ctas, maxseg;
     float scale_log2;
     float* slot_m;  // [slots][group]
@@ -399,8 +401,18 @@ __global__ void __launch_bounds__(W * 32, 1)
         }
         __syncwarp();
     };
-    // this grid is itself a programmatic dependent (launch_pdl): q, K, V, the
-    // workspace and the pool counters only after the preceding kernel is done
+    // this grid is itself a programmatic dependent (launch_pdl): q, the
+    // workspace and the pool counters only after the preceding kernel is done.
+    // The first static tiles, when they lie wholly inside t_safe tokens (no
+    // kernel ahead may be writing them: an append only writes past the last
+    // decode's length), are requested before the wait, so HBM streams while
+    // the previous step's combine finishes.
+    int pre = 0;
+    for (; pre < S && a.t_safe > 0 && !a.early_trigger && s_next < x1; ++pre) {
+        const int64_t tb = s_next - (s_next / A) * A;
+        if ((tb + 1) * T > a.t_safe) break;
+        refill(pre);
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     unsigned long long t_go = 0;
     if (a.tl && threadIdx.x == 0) {
@@ -408,7 +420,7 @@ __global__ void __launch_bounds__(W * 32, 1)
         atomicMin(a.tl + 0, t_start);
         atomicMin(a.tl + 1, t_go);
     }
-    for (int s = 0; s < S; ++s) refill(s);
+    for (int s = pre; s < S; ++s) refill(s);
 
     const int hA = 2 * (lane & 3), hB = hA + 1;  // this lane's heads (N columns)
     const int eta = lane >> 2;                   // B-fragment head / C-fragment row
@@ -1485,6 +1497,8 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.bh_count = p.bh_count;
     a.t = p.t;
     a.row_stride = p.row_stride > 0 ? p.row_stride : p.t;
+    static const int prefetch = [] { const char* e = std::getenv("TD_K1_PREFETCH"); return e ? std::atoi(e) : 1; }();
+    a.t_safe = prefetch ? (p.t_safe < p.t ? p.t_safe : p.t) : 0;
     a.tiles_per_bh = p.tiles_per_bh;
     a.total_tiles = p.total_tiles;
     a.d = p.d;
