@@ -298,6 +298,42 @@ def test_worker_append_loop(td, oracle, dtype):
     w.close()
 
 
+def test_append_decode_loop_without_host_sync(td, oracle):
+    """A generation loop with no host synchronisation: device-source append
+    (kernel), then an async decode into its own output slot, 150 times. Each
+    appended key points along the group's first query (score ~15-30 against
+    ~0.3), so a tile read before its token landed -- K1 streams tiles below
+    the last decode's length before its PDL wait -- would move the output far
+    past the tolerance. Covers the capacity growth on the first append."""
+    import torch
+    b, n_q, n_kv, n, d, steps = 1, 32, 8, 700, 128, 150
+    scale = 1.0 / math.sqrt(d)
+    q, k, v = make_inputs(oracle, 41, b, n_q, n_kv, n + steps, d, BF16)
+    g = n_q // n_kv
+    qb = q.reshape(b, n_kv, g, d)[:, :, 0]  # [b, n_kv, d]
+    k = k.copy()
+    for s in range(steps):  # bf16-exact needles: q times a power of two (scores ~15 / ~30)
+        k[:, :, n + s] = qb * float(2 << (s % 2))
+    w = td.Worker(0)
+    w.place_kv(dev(np.ascontiguousarray(k[:, :, :n]), BF16), dev(np.ascontiguousarray(v[:, :, :n]), BF16))
+    qd = dev(q, BF16)
+    kn = dev(np.ascontiguousarray(np.moveaxis(k[:, :, n:], 2, 0)[:, :, :, None]), BF16)  # [steps, b, n_kv, 1, d]
+    vn = dev(np.ascontiguousarray(np.moveaxis(v[:, :, n:], 2, 0)[:, :, :, None]), BF16)
+    out = torch.empty(steps, b, n_q, d, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    for s in range(steps):
+        w.append_kv(kn[s], vn[s])
+        w.tree_decode_async(qd.data_ptr(), n_q, out[s].data_ptr(), scale)
+    w._sync_worker()
+    got = out.cpu().double().numpy()
+    for s in range(steps):
+        m = n + s + 1
+        want = oracle.tree_decode(q, np.ascontiguousarray(k[:, :, :m]), np.ascontiguousarray(v[:, :, :m]), 1, HIER,
+                                  scale, F64)
+        assert rel_err(got[s], want) <= TOL[BF16], (s, rel_err(got[s], want))
+    w.close()
+
+
 def test_worker_append_validation_and_output_buffers(td, oracle):
     """Append errors leave the cache unchanged; host outputs work pinned
     (zero-copy store) and pageable (D2H copy) alike."""
