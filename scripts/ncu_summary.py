@@ -70,6 +70,9 @@ def main():
                 rb = float(vals["dram__bytes_read.sum"][0].replace(",", "")) * UNIT_SCALE.get(vals["dram__bytes_read.sum"][1], 1)
                 wb = float(vals["dram__bytes_write.sum"][0].replace(",", "")) * UNIT_SCALE.get(vals["dram__bytes_write.sum"][1], 1)
                 split_bytes = rb + wb
+                us = float(vals["gpu__time_duration.sum"][0].replace(",", "")) * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(
+                    vals["gpu__time_duration.sum"][1], 1.0)
+                lines.append(f"| kernel-only DRAM read rate (read bytes / duration) | {rb / (us * 1e-6) / 1e9:.1f} | GB/s |")
             except (KeyError, ValueError):
                 pass
         lines.append("")
