@@ -1041,6 +1041,65 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
     const int col0 = lane * V;
     auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
     vec ov[BO][NC];
+    if (cv.nf == 0 && T >= 2 && T <= BO) {
+        // one batch of static candidates (the common case), branch-free: the o
+        // load of slot u reads candidate min(u, T - 1) -- slots past T repeat
+        // the last candidate with weight 0 -- at a fixed stride from candidate
+        // 1, so each load is one independent address op for the single warp
+        float ml1 = -CUDART_INF_F, ll1 = 0.f;
+        if (lane < T) {
+            const int off = lane == 0 ? b0 : b1 + (lane - 1) * st;
+            ml1 = __ldcg(a.cslot_m + off);
+            ll1 = __ldcg(a.cslot_l + off);
+        }
+        const float* p0 = a.cslot_o + size_t(b0) * D + col0;
+        const float* p1 = a.cslot_o + size_t(b1) * D + col0;
+        const int64_t sD = int64_t(st) * D;
+        bool colok[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) colok[c] = col0 + c * 32 * V < D;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (colok[c]) ov[0][c] = __ldcg(reinterpret_cast<const vec*>(p0 + c * 32 * V));
+#pragma unroll
+        for (int u = 1; u < BO; ++u) {
+            const float* src = p1 + int64_t(min(u, T - 1) - 1) * sD;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (colok[c]) ov[u][c] = __ldcg(reinterpret_cast<const vec*>(src + c * 32 * V));
+        }
+        float M = ml1;
+#pragma unroll
+        for (int o2 = 16; o2 >= 1; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+        const float e_l = ml1 == -CUDART_INF_F ? 0.f : fast_exp2(ml1 - M);
+        float L = e_l * ll1;
+#pragma unroll
+        for (int o2 = 16; o2 >= 1; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
+        float acc[NC][V];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[c][v] = 0.f;
+#pragma unroll
+        for (int u = 0; u < BO; ++u) {
+            const float e = __shfl_sync(0xffffffffu, e_l, u);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const float* o = reinterpret_cast<const float*>(&ov[u][c]);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[c][v] = fmaf(e, colok[c] ? o[v] : 0.f, acc[c][v]);
+            }
+        }
+        const bool empty = M == -CUDART_INF_F;
+        const float inv = empty ? 0.f : 1.f / L;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) res.v[c][v] = acc[c][v] * inv;
+        lse_o = empty ? -CUDART_INF_F : (M + log2f(L)) * kLn2;
+        rmax_o = empty ? -CUDART_INF_F : M * kLn2;
+        return;
+    }
     float ml = -CUDART_INF_F, ll = 0.f;  // lane i holds (m, l) of candidate i0 + i (BO <= 32)
     auto load = [&](int i0) {
         {
@@ -1165,6 +1224,11 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
         LaneRow<V, NC> res;
         Cover cv = r == w0 ? cv0 : cover_of(a, r / a.group);
         cv.nf = foreign_of(a, r / a.group);
+        if (ts && r == w0) {  // debug: one candidate load's round trip
+            const float pv = __ldcg(a.cslot_m + (cv.c_lo * a.maxseg + cv.seg_lo) * a.group);
+            if (pv == 1.2345e-30f) ts[5] = 1;
+            ts[1] = gtimer();
+        }
         merge_row_warp<V, NC, BO>(a, r, cv, res, l, m);
         store_row(t.out + orow * a.d, a.d, res);
         if (ts && r == w0) ts[2] = gtimer();

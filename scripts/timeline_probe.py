@@ -68,10 +68,11 @@ def main():
                       "step_period": steps, "k1_span": [round(r[2] - r[1], 2) for r in tl],
                       "tail": [round(r[3] - r[2], 2) for r in tl]}))
     if os.environ.get("TL_DUMP_CTAS"):  # the last step, per CTA index: (c, smid, past-wait, end)
-        g0 = min(st[4096 + 2 * c] for c in range(1024) if st[4096 + 2 * c])
+        nc = 452  # CTA slots [4096 + 2c] below the per-step rows at [5000 + 4i]
+        g0 = min(st[4096 + 2 * c] for c in range(nc) if st[4096 + 2 * c])
         print(json.dumps({"rank": local, "ctas": [(c, st[2048 + c], round((st[4096 + 2 * c] - g0) / 1000.0, 2),
                                                    round((st[4097 + 2 * c] - g0) / 1000.0, 2))
-                                                  for c in range(1024) if st[4097 + 2 * c]]}))
+                                                  for c in range(nc) if st[4097 + 2 * c]]}))
     w.close()
     if world > 1:
         dist.barrier()

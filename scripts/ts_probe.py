@@ -56,6 +56,7 @@ def main():
             summary["cta_end_q"] = [qt(ends, f) for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
         names = ["k2_entry", "pushed", "merged", "seen", "done"]
         if world == 1:
+            names[1] = "probe_load"
             names[3] = "k2_prewait"
         for k, name in enumerate(names):
             vals = [bl[k] for bl in blocks if bl[k]]
