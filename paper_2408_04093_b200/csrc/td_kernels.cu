@@ -176,6 +176,85 @@ __device__ void cta_merge(const K1Args& a, int c, float* sm) {
     }
 }
 
+// cta_merge with the loads of the merge batched: every thread loads its o
+// elements of all W states (EPT per thread per chunk) together with the
+// (m, l) pairs, before the weights are known, so the first chunk costs one
+// L2 round trip -- this is the epilogue of the grid's last CTA, on the step's
+// critical path. Needs W * maxseg * group <= blockDim.x (else cta_merge).
+template <int W, int D, int EPT>
+__device__ void cta_merge_batched(const K1Args& a, int c, float* sm) {
+    const int g = a.group, nsh = a.maxseg * g, nml = W * nsh, nt = blockDim.x;
+    if (nml > nt) {
+        cta_merge<W>(a, c, sm);
+        return;
+    }
+    float* sm_m = sm;
+    float* sm_l = sm + nml;
+    float* sm_e = sm + 2 * nml;
+    const int64_t base = int64_t(c) * nml;
+    const int n = nsh * D;
+    float ov[EPT][W];
+    auto load_chunk = [&](int e0) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int e = e0 + static_cast<int>(threadIdx.x) + k * nt;
+            if (e < n) {
+                const int i = e / D, j = e % D;
+#pragma unroll
+                for (int w = 0; w < W; ++w) ov[k][w] = a.slot_o[(base + int64_t(w) * nsh + i) * D + j];
+            }
+        }
+    };
+    auto use_chunk = [&](int e0) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int e = e0 + static_cast<int>(threadIdx.x) + k * nt;
+            if (e < n) {
+                const int i = e / D, j = e % D;
+                float O = 0.f;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    const float ew = sm_e[w * nsh + i];
+                    O += ew != 0.f ? ew * ov[k][w] : 0.f;  // never-flushed o may hold anything
+                }
+                a.cslot_o[(int64_t(c) * nsh + i) * D + j] = O;
+            }
+        }
+    };
+    float mv = -CUDART_INF_F, lv = 0.f;
+    if (static_cast<int>(threadIdx.x) < nml) {
+        mv = a.slot_m[base + threadIdx.x];
+        lv = a.slot_l[base + threadIdx.x];
+    }
+    load_chunk(0);
+    if (static_cast<int>(threadIdx.x) < nml) {
+        sm_m[threadIdx.x] = mv;
+        sm_l[threadIdx.x] = lv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nsh; i += nt) {
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < W; ++w) M = fmaxf(M, sm_m[w * nsh + i]);
+        float L = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const float m = sm_m[w * nsh + i];
+            const float e = (m == -CUDART_INF_F) ? 0.f : fast_exp2(m - M);
+            sm_e[w * nsh + i] = e;
+            L += e * sm_l[w * nsh + i];
+        }
+        a.cslot_m[int64_t(c) * nsh + i] = M;
+        a.cslot_l[int64_t(c) * nsh + i] = L;
+    }
+    __syncthreads();
+    use_chunk(0);
+    for (int e0 = EPT * nt; e0 < n; e0 += EPT * nt) {
+        load_chunk(e0);
+        use_chunk(e0);
+    }
+}
+
 // Logical CTA index: blockIdx, or -- with a calibrated partition -- the index
 // calibrated on this SM (SplitPlan::sm_to_cta), claimed for this launch; a CTA
 // whose SM already hosts one of this grid's CTAs takes the next free index.
@@ -630,8 +709,8 @@ __global__ void __launch_bounds__(W * 32, 1)
             }
         }
     __syncthreads();
-    if (phases == 2) cta_merge<2 * W>(a, c, reinterpret_cast<float*>(smem));
-    else cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    if (phases == 2) cta_merge_batched<2 * W, D, 8>(a, c, reinterpret_cast<float*>(smem));
+    else cta_merge_batched<W, D, 8>(a, c, reinterpret_cast<float*>(smem));
     if (a.tl && threadIdx.x == 0) {
         const unsigned long long t_end = gtimer();
         atomicMax(a.tl + 2, t_end);
