@@ -1,0 +1,26 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r72
+O=gpurun_out/r72
+timeout 1500 python -m pytest tests -q -m gpu -p timeout --timeout 800 > $O/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
+timeout 600 python bench.py > $O/b1.log 2>&1
+timeout 300 python bench.py --steps 100 --warmup 5 --seq-len 131072 --no-cpu-baseline > $O/b1_131k.log 2>&1
+timeout 600 python bench.py --workload cfg4 --steps 20 --warmup 3 --no-cpu-baseline > $O/b1_cfg4.log 2>&1
+port=29700
+for n in 2 4; do
+port=$((port+1))
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $port bench.py --gpus $n > $O/b$n.log 2>&1
+done
+port=$((port+1))
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $port bench.py --gpus 4 --steps 100 --seq-len 524288 > $O/b4_512k.log 2>&1
+port=$((port+1))
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $port bench.py --gpus 4 --combine nccl > $O/b4_nccl.log 2>&1
+port=$((port+1))
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $port bench.py --gpus 4 --workload cfg4 --steps 20 > $O/b4_cfg4.log 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref1.log 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $O/launches_1m.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_l1m.log 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_bf16|k2_combine" -s 30 -c 2 -o $O/prof_1m python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_f1m.log 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $O/launches_131k.csv python bench.py --steps 3 --warmup 3 --seq-len 131072 --no-cpu-baseline > $O/ncu_l131k.log 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_bf16|k2_combine" -s 30 -c 2 -o $O/prof_131k python bench.py --steps 2 --warmup 3 --seq-len 131072 --no-cpu-baseline > $O/ncu_f131k.log 2>&1
+echo done

@@ -64,6 +64,8 @@ def main():
     steps = [round(tl[i + 1][1] - tl[i][1], 2) for i in range(len(tl) - 1)]
     print(json.dumps({"rank": local, "world": world, "seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
                       "abs_k1_start_us": [round(r[0] / 1000.0, 2) for r in rows],
+                      "abs_k1_end_us": [round(r[2] / 1000.0, 2) for r in rows],
+                      "abs_k2_done_us": [round(r[3] / 1000.0, 2) for r in rows],
                       "k1_start_minus_prev_k2_done": gaps, "k1_past_wait_minus_prev_k2_done": waits,
                       "step_period": steps, "k1_span": [round(r[2] - r[1], 2) for r in tl],
                       "tail": [round(r[3] - r[2], 2) for r in tl]}))

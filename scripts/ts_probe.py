@@ -49,7 +49,8 @@ def main():
         starts = sorted((st[4096 + 2 * c] - t0) / 1000.0 for c in range(1024) if st[4096 + 2 * c])
         blocks = [st[8 + 8 * i: 8 + 8 * i + 8] for i in range(64) if st[8 + 8 * i] != 0]
         rel = lambda x: round((x - t0) / 1000.0, 2) if x else None
-        summary = {"k1_end": rel(st[1]), "pre_k1_stamp": rel(st[2]), "post_k2_stamp": rel(st[3])}
+        summary = {"k1_end": rel(st[1]), "pre_k1_stamp": rel(st[2]), "post_k2_stamp": rel(st[3]),
+                   "abs_k1_start_ns": int(t0), "abs_k1_end_ns": int(st[1])}
         if ends:
             qt = lambda xs, f: round(xs[min(len(xs) - 1, int(f * len(xs)))], 2)
             summary["cta_start_q"] = [qt(starts, f) for f in (0.0, 0.5, 1.0)]
@@ -63,6 +64,7 @@ def main():
             if vals:
                 summary[name + "_min"] = rel(min(vals))
                 summary[name + "_max"] = rel(max(vals))
+                summary["abs_" + name + "_max_ns"] = int(max(vals))
         if os.environ.get("TS_DUMP_CTAS"):
             summary["ctas"] = [(c, st[2048 + c], round((st[4097 + 2 * c] - t0) / 1000.0, 2))
                                for c in range(1024) if st[4097 + 2 * c]]
