@@ -1104,7 +1104,7 @@ struct LaneRow {
 // registers (a lane-parallel pass + shuffles only when S > BO).
 template <int V, int NC, int BO>
 __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const Cover& cv, LaneRow<V, NC>& res,
-                                               float& lse_o, float& rmax_o) {
+                                               float& lse_o, float& rmax_o, int colb = 0) {
     using vec = typename std::conditional<V == 4, float4, float>::type;
     static_assert(BO <= 32, "one candidate (m, l) per lane");
     const int lane = threadIdx.x & 31;
@@ -1117,7 +1117,7 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
     const int st = a.maxseg * g;
     const int b0 = static_cast<int>(cs_of(0) * g + h), b1 = static_cast<int>(cs_of(1) * g + h);
     const int fb = static_cast<int>((r / g) * a.fslots * g + h);
-    const int col0 = lane * V;
+    const int col0 = colb + lane * V;  // colb: first column of this warp's share of the row
     auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
     vec ov[BO][NC];
     if (cv.nf == 0 && T >= 2 && T <= BO) {
@@ -1248,12 +1248,12 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
 }
 
 template <int V, int NC>
-__device__ __forceinline__ void store_row(float* dst, int D, const LaneRow<V, NC>& res) {
+__device__ __forceinline__ void store_row(float* dst, int D, const LaneRow<V, NC>& res, int colb = 0) {
     using vec = typename std::conditional<V == 4, float4, float>::type;
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        const int col = (c * 32 + lane) * V;
+        const int col = colb + (c * 32 + lane) * V;
         if (col < D) *reinterpret_cast<vec*>(dst + col) = *reinterpret_cast<const vec*>(res.v[c]);
     }
 }
@@ -1320,6 +1320,43 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
 }
 
+// K2 with each row split by columns over Q warps (d = 32 Q, one float per
+// lane): a warp loads one 128-byte line per candidate instead of Q, so the
+// merge's loads of a row spread over Q SMs. Same results as k2_combine (the
+// per-column arithmetic is identical).
+template <int Q>
+__global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
+    const int64_t rows = a.bh_count * a.group, units = rows * Q;
+    const int64_t u0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const Cover cv0 = u0 < units ? cover_of(a, (u0 / Q) / a.group) : Cover{};  // host-written tables only
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pool_tiles > 0)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
+             i += int64_t(gridDim.x) * blockDim.x) {
+            a.pool_next[i] = 0u;
+            if (a.fcnt_next) a.fcnt_next[i] = 0u;
+        }
+    const Tail& t = a.tail;
+    for (int64_t u = u0; u < units; u += nw) {
+        const int64_t r = u / Q;
+        const int colb = static_cast<int>(u % Q) * 32;
+        const int64_t orow = out_row_of(a, r);
+        float l, m;
+        LaneRow<1, 1> res;
+        Cover cv = u == u0 ? cv0 : cover_of(a, r / a.group);
+        cv.nf = foreign_of(a, r / a.group);
+        merge_row_warp<1, 1, 32>(a, r, cv, res, l, m, colb);
+        store_row(t.out + orow * a.d, a.d, res, colb);
+        if (t.mode == kTailPartial && colb == 0 && (threadIdx.x & 31) == 0) {
+            t.lse[orow] = l;
+            t.row_max[orow] = m;
+        }
+    }
+    if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
+}
+
 // =========================================================================
 // K2x: K2 fused with the one-shot NVLink exchange (kTailExchange), LL
 // protocol: every 8-byte word of the exchange buffer is (value, epoch), so a
@@ -1363,14 +1400,14 @@ __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
 }
 
 
-template <int V, int NC, int BO>
+template <int V, int NC, int BO, int Q>
 __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
-    const int64_t rows = a.bh_count * a.group;
+    const int64_t rows = a.bh_count * a.group, units = rows * Q;  // Q warps per row (column split)
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    const Cover cv0 = w0 < rows ? cover_of(a, w0 / a.group) : Cover{};
+    const Cover cv0 = w0 < units ? cover_of(a, (w0 / Q) / a.group) : Cover{};
     const Xchg& x = a.tail.x;
     constexpr int PMAX = 8;  // peers held in registers (the exchange spans one NVLink domain)
     uint2* pp[PMAX];         // peer buffers, read before the wait (host-written)
@@ -1391,24 +1428,26 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
     unsigned long long* ts = (a.dbg && w0 < 512 && lane == 0) ? a.dbg + 8 + 8 * w0 : nullptr;
     if (ts) ts[0] = gtimer();
-    for (int64_t r = w0; r < rows; r += nw) {  // merge + push
+    for (int64_t u = w0; u < units; u += nw) {  // merge + push
+        const int64_t r = u / Q;
+        const int colb = static_cast<int>(u % Q) * (32 * V * NC);
         const int64_t orow = out_row_of(a, r);
         float l, m;
         LaneRow<V, NC> res;
-        Cover cv = r == w0 ? cv0 : cover_of(a, r / a.group);
+        Cover cv = u == w0 ? cv0 : cover_of(a, r / a.group);
         cv.nf = foreign_of(a, r / a.group);
-        merge_row_warp<V, NC, BO>(a, r, cv, res, l, m);
-        if (ts && r == w0) ts[2] = gtimer();
+        merge_row_warp<V, NC, BO>(a, r, cv, res, l, m, colb);
+        if (ts && u == w0) ts[2] = gtimer();
         const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
         auto push = [&](uint2* dst) {  // LL words of this row into slot `rank` of one buffer
 #pragma unroll
             for (int c = 0; c < NC; ++c)
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const int col = (c * 32 + lane) * V + v;
+                    const int col = colb + (c * 32 + lane) * V + v;
                     if (col < D) st_ll(dst + col, res.v[c][v], x.epoch);
                 }
-            if (lane == 0) st_ll(dst + D, l, x.epoch);
+            if (lane == 0 && colb == 0) st_ll(dst + D, l, x.epoch);
         };
         if (x.pull) {
             push(peers[x.rank] + off);  // own buffer only: the peers read it over NVLink
@@ -1420,7 +1459,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
         }
     }
     if (ts) ts[1] = gtimer();
-    for (int64_t r = w0; r < rows; r += nw) {  // exact combine of the p partials
+    for (int64_t u = w0; u < units; u += nw) {  // exact combine of the p partials
+        const int64_t r = u / Q;
+        const int colb = static_cast<int>(u % Q) * (32 * V * NC);
         const int64_t orow = out_row_of(a, r);
         // source k's words: push -- slot k of the own buffer; pull -- slot k of k's buffer
         const int64_t roff = int64_t(par) * x.p * stride + orow * (D + 1);
@@ -1440,7 +1481,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
                 for (int c = 0; c < NC; ++c)
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
-                        const int col = (c * 32 + lane) * V + v;
+                        const int col = colb + (c * 32 + lane) * V + v;
                         if (col < D) wo[k][c][v] = ld_word(slot + col);
                     }
             }
@@ -1452,7 +1493,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
                 for (int c = 0; c < NC; ++c)
 #pragma unroll
                     for (int v = 0; v < V; ++v)
-                        if ((c * 32 + lane) * V + v < D) all &= wo[k][c][v].y == x.epoch;
+                        if (colb + (c * 32 + lane) * V + v < D) all &= wo[k][c][v].y == x.epoch;
             }
             if (__all_sync(0xffffffffu, all)) break;
             if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
@@ -1460,7 +1501,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
                 break;
             }
         }
-        if (ts && r == w0) ts[3] = gtimer();
+        if (ts && u == w0) ts[3] = gtimer();
         float shift = -CUDART_INF_F, den = 0.f;
 #pragma unroll
         for (int k = 0; k < PMAX; ++k)
@@ -1492,7 +1533,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
             for (int c = 0; c < NC; ++c)
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const int col = (c * 32 + lane) * V + v;
+                    const int col = colb + (c * 32 + lane) * V + v;
                     if (col < D) num[c][v] += wgt * ld_ll(slot + col, x.epoch, x.error);
                 }
         }
@@ -1501,7 +1542,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
         for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const int col = (c * 32 + lane) * V + v;
+                const int col = colb + (c * 32 + lane) * V + v;
                 if (col < D) dst[col] = num[c][v] / den;
             }
     }
@@ -1982,9 +2023,9 @@ cudaError_t launch_k2_t(const K1Args& a, int64_t blocks, int warps, bool exchang
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = exchange ? prefer_max_smem(k2_exchange<V, NC, BO>) : prefer_max_smem(k2_combine<V, NC, BO>);
+    cudaError_t e = exchange ? prefer_max_smem(k2_exchange<V, NC, BO, 1>) : prefer_max_smem(k2_combine<V, NC, BO>);
     if (e != cudaSuccess) return e;
-    return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange<V, NC, BO>, a)
+    return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange<V, NC, BO, 1>, a)
                     : cudaLaunchKernelEx(&cfg, k2_combine<V, NC, BO>, a);
 }
 
@@ -2005,6 +2046,23 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
     int64_t blocks = (rows + warps - 1) / warps;
     if (blocks > limit) blocks = limit;
 #define TD_K2(VV, NN, BB) launch_k2_t<VV, NN, BB>(a, blocks, warps, exchange, st)
+    static const int cols = [] { const char* e = std::getenv("TD_K2_COLS"); return e ? std::atoi(e) : 4; }();
+    if (cols == 4 && a.d == 128 && force_w == 0 && rows * 4 <= limit && !a.dbg) {
+        const int64_t b4 = rows * 4;  // one (row, column quarter) per single-warp block
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(b4 < 1 ? 1 : b4));
+        cfg.blockDim = dim3(32);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = exchange ? prefer_max_smem(k2_exchange<1, 1, 32, 4>) : prefer_max_smem(k2_combine_cols<4>);
+        if (e != cudaSuccess) return e;
+        return exchange ? cudaLaunchKernelEx(&cfg, k2_exchange<1, 1, 32, 4>, a)
+                        : cudaLaunchKernelEx(&cfg, k2_combine_cols<4>, a);
+    }
     if (a.d % 4 == 0 && a.d <= 128) return TD_K2(4, 1, 32);
     if (a.d % 4 == 0) return TD_K2(4, 2, 16);
     return TD_K2(1, 8, 8);
