@@ -44,8 +44,12 @@ typedef enum {
 
 typedef enum { TD_F64 = 0, TD_F32 = 1, TD_BF16 = 2 } td_dtype;
 
-/* treedec::ReduceStrategy (reduce.hpp:10). On the GPU the collective is one
- * NCCL allreduce over NVLink; the strategy selects NCCL's algorithm hint. */
+/* treedec::ReduceStrategy (reduce.hpp:10). It is validated and names the
+ * reduction schedule whose round counts the host mirrors report
+ * (DecodeResult::collectives, reduce.cpp:60-139). The GPU collective itself is
+ * one NCCL allreduce per step (NCCL picks its algorithm; NCCL_ALGO steers it
+ * process-wide) or the one-shot exchange (TD_P2P): the result is the same
+ * exact combine whichever schedule is named. */
 typedef enum { TD_TREE_BINARY = 0, TD_RING_ALLREDUCE = 1, TD_HIERARCHICAL = 2 } td_strategy;
 
 /* flags for td_tree_decode / td_ring_decode */
@@ -137,7 +141,11 @@ int td_comm_info(td_context* ctx, int* nranks, int* rank);
  * the caller (rank order, nranks * 64 bytes) and every rank opens its peers'.
  * td_tree_decode with TD_P2P then pushes each rank's partial into every
  * peer's HBM and combines the p partials locally (one exchange, no NCCL).
- * td_p2p_status reports a peer that never arrived (1) since the last call. */
+ * A peer that never delivers within ~2 s makes the step fail: td_tree_decode
+ * returns TD_ECUDA at its next synchronising point (TD_HOST_IO calls: the
+ * same call; device calls: the next call, or td_p2p_status, which waits for
+ * the stream and reports 1). The exchange must then be re-opened on every
+ * rank (td_p2p_handle + td_p2p_open) before TD_P2P is used again. */
 int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char handle[64]);
 int td_p2p_open(td_context* ctx, const unsigned char* handles);
 int td_p2p_status(td_context* ctx, int* error);

@@ -7,7 +7,7 @@ is the host-side mirror of the reference interface over that C-ABI.
 """
 from ._capi import DomainError, InvalidArgument, TreeDecError  # noqa: F401
 from .decode import (  # noqa: F401
-    CostAccount, DecodeAlgo, DecodeResult, DType, EnergyEval, ReduceStrategy, ShardedKVCache, SoftmaxPartial,
+    CostAccount, DecodeAlgo, DecodeResult, allreduce_rounds, tree_collectives, DType, EnergyEval, ReduceStrategy, ShardedKVCache, SoftmaxPartial,
     Topology, energy, energy_forward_parallel, energy_grad_parallel, energy_partial,
     Worker, attention_chunk_partial, chunk_extents, combine_pair, combine_partials, comm_volume_formula,
     comm_volume_formula_seq, decode_tolerance_abs, finalize, partial_to_numerator, peak_memory_formula,

@@ -182,9 +182,15 @@ struct td_context {
     int64_t x_max_rows = 0, x_d = 0;
     std::vector<void*> x_opened;      // IPC mappings to close
     DevBuf x_ptrs;                    // device array: peers[p]
-    DevBuf x_err;
+    int* x_err = nullptr;             // exchange timeout flag, mapped pinned host memory (K2x stores 1)
     unsigned x_epoch = 0;
     bool x_ready = false;
+
+    // debug instrumentation of the current call (debug_begin), copied into every plan
+    unsigned long long* cur_dbg = nullptr;
+    unsigned long long* cur_tl = nullptr;
+    unsigned long long* cur_tl_cta = nullptr;
+    bool shared_device = false;       // another context of this process runs on the same GPU (td_group)
 
     DevBuf dbg;  // TD_DEBUG_TS stamps
     int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
@@ -293,12 +299,17 @@ int apply_partition(td_context* ctx, SplitPlan& plan) {
             return TD_OK;
         }
     }
+    std::vector<int64_t> x(size_t(plan.ctas) + 1);
+    std::vector<int> bh(3 * size_t(plan.bh_count));
+    SplitPlan weighted = plan;
+    td::build_partition(weighted, ctx->cal_w.data(), x.data(), bh.data());
+    // the weighted ranges may cover more (batch, head) rows per CTA than the
+    // kernels' per-warp segment masks hold: keep the equal split then
+    if (weighted.maxseg > td::kMaxSegments) return TD_OK;
+    plan.maxseg = weighted.maxseg;
     const int idx = ctx->tab_next;
     auto& tb = ctx->tabs[idx];
     ctx->tab_next = (ctx->tab_next + 1) % 4;
-    std::vector<int64_t> x(size_t(plan.ctas) + 1);
-    std::vector<int> bh(3 * size_t(plan.bh_count));
-    td::build_partition(plan, ctx->cal_w.data(), x.data(), bh.data());
     const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
     // no stream drain when the sequence grows (a new shape every 32 appended tokens):
     // wait only for the last launch that read this entry, then upload from pinned
@@ -362,6 +373,7 @@ int calibrate(td_context* ctx, int64_t n_q) {
         x.assign(size_t(G) + 1, 0);
         std::vector<int> bh(3 * size_t(pr.bh_count));
         td::build_partition(pr, w.data(), x.data(), bh.data());
+        if (pr.maxseg > td::kMaxSegments) return set_err(TD_EINVAL, "calibration: weighted ranges span too many rows");
         const size_t xb = x.size() * sizeof(int64_t), bb = bh.size() * sizeof(int);
         TD_CUDA(tab.ensure(xb + bb));
         TD_CUDA(cudaMemcpy(tab.p, x.data(), xb, cudaMemcpyHostToDevice));
@@ -374,12 +386,10 @@ int calibrate(td_context* ctx, int64_t n_q) {
         TD_CUDA(ctx->ws.ensure(pr.workspace_bytes()));
         TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream));
         TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xff, sizeof(unsigned long long), ctx->stream));
-        td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
-        const cudaError_t e = td::launch_decode_partial(pr, ctx->cal_q.p, ctx->k.p, ctx->v.p, 1.0f, &ctx->tmk,
-                                                        &ctx->tmv, ctx->ws.p, ctx->r_max, ctx->r_lse, ctx->r_out,
-                                                        ctx->stream);
-        td::set_debug_stamps(nullptr);
-        TD_CUDA(e);
+        pr.dbg = static_cast<unsigned long long*>(ctx->dbg.p);
+        pr.tl = pr.tl_cta = nullptr;
+        TD_CUDA(td::launch_decode_partial(pr, ctx->cal_q.p, ctx->k.p, ctx->v.p, 1.0f, &ctx->tmk, &ctx->tmv,
+                                          ctx->ws.p, ctx->r_max, ctx->r_lse, ctx->r_out, ctx->stream));
         TD_CUDA(cudaMemcpyAsync(st.data(), ctx->dbg.p, st.size() * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
         TD_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -475,8 +485,12 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
         return set_err(TD_EINVAL, msg);
     plan.row_stride = stride;
     plan.t_safe = stride > 0 ? std::min(ctx->kv_safe, t) : 0;  // the context's own cache only
+    plan.dbg = ctx->cur_dbg;
+    plan.tl = ctx->cur_tl;
+    plan.tl_cta = ctx->cur_tl_cta;
+    plan.pdl = !ctx->shared_device;
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
-        if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok) {
+        if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok && !ctx->shared_device) {
             if (calibrate(ctx, n_q) != TD_OK) {
                 ctx->cal_failed = true;  // keep the equal split
             } else {
@@ -614,6 +628,18 @@ float* mapped_host(td_context* ctx, float* host) {
     ctx->mapped_for = host;
     ctx->mapped_dev = dev;
     return dev;
+}
+
+// A K2x spin that timed out (a peer never delivered this step's words) stores
+// 1 into the mapped flag; the step's output is then garbage. Reported as an
+// error, after which the exchange must be re-opened on every rank
+// (td_p2p_handle / td_p2p_open) so that the epochs agree again.
+int exchange_failed(td_context* ctx) {
+    if (!ctx->x_err || !*reinterpret_cast<volatile int*>(ctx->x_err)) return TD_OK;
+    *reinterpret_cast<volatile int*>(ctx->x_err) = 0;
+    ctx->x_ready = false;
+    return set_err(TD_ECUDA, "tree_decode: NVLink exchange timed out (a peer never delivered its partial); "
+                             "re-open the exchange with td_p2p_handle / td_p2p_open");
 }
 
 int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int flags) {
@@ -755,17 +781,16 @@ int td_energy_grad_combine(int P, const float* lse, const float* out, const floa
 int td_combine_partials(int P, const float* lse, const float* out, int64_t rows, int64_t d,
                         float* result, void* stream) {
     if (P < 1) return set_err(TD_EINVAL, "combine_partials: no parts");
-    int* bad = nullptr;
-    TD_CUDA(cudaMalloc(&bad, sizeof(int)));
+    // the empty-row verdict: one mapped pinned flag per host thread (portable across
+    // devices), allocated once; the call synchronises to raise like the reference
+    thread_local int* bad = nullptr;
+    if (!bad) TD_CUDA(cudaHostAlloc(&bad, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    volatile int* flag = bad;
+    *flag = 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaMemsetAsync(bad, 0, sizeof(int), st);
-    cudaError_t e = td::launch_combine_partials(P, lse, out, rows, static_cast<int>(d), result, bad, st);
-    int hbad = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(bad);
-    TD_CUDA(e);
-    if (hbad) return set_err(TD_EINVAL, "combine_partials: no keys attended");
+    TD_CUDA(td::launch_combine_partials(P, lse, out, rows, static_cast<int>(d), result, bad, st));
+    TD_CUDA(cudaStreamSynchronize(st));
+    if (*flag) return set_err(TD_EINVAL, "combine_partials: no keys attended");
     return TD_OK;
 }
 
@@ -834,7 +859,7 @@ int td_destroy(td_context* ctx) {
     for (void* ptr : ctx->x_opened) cudaIpcCloseMemHandle(ptr);
     ctx->xbuf.release();
     ctx->x_ptrs.release();
-    ctx->x_err.release();
+    if (ctx->x_err) cudaFreeHost(ctx->x_err);
     ctx->ctr.release();
     ctx->dbg.release();
     ctx->tlbuf.release();
@@ -902,8 +927,8 @@ int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char ha
     ctx->xbuf.release();
     TD_CUDA(ctx->xbuf.ensure(data));
     TD_CUDA(cudaMemset(ctx->xbuf.p, 0, data));
-    TD_CUDA(ctx->x_err.ensure(sizeof(int)));
-    TD_CUDA(cudaMemset(ctx->x_err.p, 0, sizeof(int)));
+    if (!ctx->x_err) TD_CUDA(cudaHostAlloc(&ctx->x_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    *reinterpret_cast<volatile int*>(ctx->x_err) = 0;
     ctx->x_max_rows = max_rows;
     ctx->x_d = d;
     ctx->x_epoch = 0;
@@ -941,10 +966,14 @@ int td_p2p_open(td_context* ctx, const unsigned char* handles) {
 int td_p2p_status(td_context* ctx, int* error) {
     if (int rc = require_ctx(ctx)) return rc;
     *error = 0;
-    if (!ctx->x_err.p) return TD_OK;
+    if (!ctx->x_err) return TD_OK;
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
-    TD_CUDA(cudaMemcpy(error, ctx->x_err.p, sizeof(int), cudaMemcpyDeviceToHost));
-    TD_CUDA(cudaMemset(ctx->x_err.p, 0, sizeof(int)));
+    volatile int* f = ctx->x_err;
+    *error = *f;
+    if (*error) {  // the ranks' epochs can no longer be trusted to agree: re-open to resume
+        *f = 0;
+        ctx->x_ready = false;
+    }
     return TD_OK;
 }
 
@@ -1124,10 +1153,8 @@ int td_kv_pointers(td_context* ctx, void** k, void** v) {
 // without any extra operation on the stream (see scripts/timeline_probe.py).
 static int timeline_step(td_context* ctx) {
     static const bool on = [] { const char* e = std::getenv("TD_DEBUG_TIMELINE"); return e && std::atoi(e) != 0; }();
-    if (!on) {
-        td::set_timeline(nullptr);
-        return TD_OK;
-    }
+    ctx->cur_tl = ctx->cur_tl_cta = nullptr;
+    if (!on) return TD_OK;
     if (ctx->tl_count < 0) {
         std::vector<unsigned long long> init(6144 - 5000);
         for (size_t i = 0; i < init.size(); ++i) init[i] = (i % 4) < 2 ? ~0ull : 0ull;
@@ -1137,22 +1164,20 @@ static int timeline_step(td_context* ctx) {
         ctx->tl_count = 0;
     }
     TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
-    td::set_timeline(static_cast<unsigned long long*>(ctx->tlbuf.p) + 4 * (ctx->tl_count % 286),
-                     static_cast<unsigned long long*>(ctx->dbg.p));
+    ctx->cur_tl = static_cast<unsigned long long*>(ctx->tlbuf.p) + 4 * (ctx->tl_count % 286);
+    ctx->cur_tl_cta = static_cast<unsigned long long*>(ctx->dbg.p);
     ++ctx->tl_count;
     return TD_OK;
 }
 
 static int debug_begin(td_context* ctx, int flags) {
+    ctx->cur_dbg = nullptr;
     if (int rc = timeline_step(ctx)) return rc;
-    if (!(flags & TD_DEBUG_TS)) {
-        td::set_debug_stamps(nullptr);
-        return TD_OK;
-    }
+    if (!(flags & TD_DEBUG_TS)) return TD_OK;
     TD_CUDA(ctx->dbg.ensure(6144 * sizeof(unsigned long long)));
     TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0, 6144 * sizeof(unsigned long long), ctx->stream));
     TD_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xff, sizeof(unsigned long long), ctx->stream));
-    td::set_debug_stamps(static_cast<unsigned long long*>(ctx->dbg.p));
+    ctx->cur_dbg = static_cast<unsigned long long*>(ctx->dbg.p);
     return TD_OK;
 }
 
@@ -1195,14 +1220,15 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         if (!ctx->x_ready) return set_err(TD_ESTATE, "tree_decode: TD_P2P without td_p2p_open");
         if (rows > ctx->x_max_rows || d != ctx->x_d)
             return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
+        if (int rc = exchange_failed(ctx)) return rc;  // an earlier asynchronous step timed out
         td::XchgArgs xa;
         xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
         xa.p = ctx->nranks;
         xa.rank = ctx->rank;
-        xa.epoch = ++ctx->x_epoch;
+        xa.epoch = ctx->x_epoch + 1;  // committed only once the launch is in: all ranks stay in step
         xa.max_rows = ctx->x_max_rows;
         xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
-        xa.error = static_cast<int*>(ctx->x_err.p);
+        xa.error = ctx->x_err;
         static const int pull = [] { const char* e = std::getenv("TD_XCHG_PULL"); return e ? std::atoi(e) : 0; }();
         xa.pull = pull;
         const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
@@ -1222,13 +1248,15 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         }
         TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                            ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
+        ctx->x_epoch = xa.epoch;
         ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
         phase_mark(ctx);
         ctx->last_kernels = 2;  // K1 + K2x
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
                              td::dtype_bytes(ctx->dtype);
         ctx->last_split_kernel = plan.kernel;
-        return deliver_out(ctx, xdst, rows, out, flags);
+        if (int rc = deliver_out(ctx, xdst, rows, out, flags)) return rc;
+        return (flags & TD_HOST_IO) ? exchange_failed(ctx) : TD_OK;  // synchronised: this step's verdict
     }
     if (ctx->nranks == 1) {
         // p = 1: the shard partial is the result (shift = lse, w = 1): one kernel,
@@ -1292,6 +1320,7 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
                      float* lse, float* out, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
     ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
+    if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "local_partial: no KV shard placed");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "local_partial: q/kv head mismatch");
     ctx->last_kernels = 0;
@@ -1325,8 +1354,8 @@ int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, 
 int td_energy_forward(td_context* ctx, const void* q, const void* src, int64_t nq, float* value,
                       float* row_max, float* shifted, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
-    (void)flags;
     ctx->det = g_deterministic != 0;
+    if (int rc = debug_begin(ctx, flags & ~TD_DEBUG_TS)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "energy_forward: no KV shard placed");
     if (nq < 1) return set_err(TD_EINVAL, "energy_forward: need nq >= 1");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "energy_forward: more workers than keys");
@@ -1355,8 +1384,8 @@ int td_energy_forward(td_context* ctx, const void* q, const void* src, int64_t n
 int td_energy_grad(td_context* ctx, const void* q, int64_t nq, const float* row_max, const float* shifted,
                    float* grad, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
-    (void)flags;
     ctx->det = g_deterministic != 0;
+    if (int rc = debug_begin(ctx, flags & ~TD_DEBUG_TS)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "energy_grad: no KV shard placed");
     if (nq < 1) return set_err(TD_EINVAL, "energy_grad: need nq >= 1");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "energy_grad: more workers than keys");
@@ -1381,6 +1410,7 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
                    int flags) {
     if (int rc = require_ctx(ctx)) return rc;
     ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
+    if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "ring_decode: no KV shard placed");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "ring_decode: more workers than keys");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "ring_decode: q/kv head mismatch");

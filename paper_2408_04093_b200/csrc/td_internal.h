@@ -12,6 +12,10 @@ namespace td {
 
 enum DType { kF64 = 0, kF32 = 1, kBF16 = 2 };
 
+// K1 tracks the (batch, head) rows a CTA's range touches in per-warp bit masks:
+// a split plan (equal or speed-weighted) may span at most this many per CTA.
+constexpr int kMaxSegments = 32;
+
 inline int dtype_bytes(int dt) { return dt == kBF16 ? 2 : (dt == kF32 ? 4 : 8); }
 
 // Split-KV work decomposition of one shard (K1). The shard holds bh_count
@@ -58,6 +62,16 @@ struct SplitPlan {
     const int* sm_to_cta = nullptr;
     unsigned* claims = nullptr;
     unsigned epoch = 0;
+    // debug instrumentation of this launch (owned by the calling context, null = off):
+    // TD_DEBUG_TS stamps [0] min K1 CTA start, [1] max K1 CTA end, [8 + 8*blk + k] K2
+    // block stages, [2048 + c] / [4096 + 2c] per-CTA SM and times; TD_DEBUG_TIMELINE
+    // per-step slot of 4 stamps (K1Args::tl) and per-CTA stamps (tl_cta)
+    unsigned long long* dbg = nullptr;
+    unsigned long long* tl = nullptr;
+    unsigned long long* tl_cta = nullptr;
+    // launch K1 as a programmatic dependent of the preceding kernel (off when several
+    // contexts share one GPU and a peer's K1 must get SMs while this one's exchange waits)
+    bool pdl = true;
     int64_t slots() const { return int64_t(ctas) * slot_warps * maxseg; }
     // workspace: slot_m, slot_l [slots][group]; slot_o [slots][group][d] (fp32),
     // then the per-CTA merged states [ctas * maxseg][group] (+ [..][d])
@@ -69,11 +83,6 @@ struct SplitPlan {
     size_t counters_bytes() const { return sizeof(unsigned) * 4 * size_t(bh_count > 0 ? bh_count : 1); }
 };
 
-// TD_DEBUG_TS: kernels write %globaltimer stamps into buf (nullptr = off):
-// [0] min K1 CTA start, [1] max K1 CTA end, [8 + 8*blk + k] K2 block stages.
-void set_debug_stamps(unsigned long long* buf);
-// TD_DEBUG_TIMELINE: per-step slot of 4 stamps (nullptr = off), see K1Args::tl.
-void set_timeline(unsigned long long* slot, unsigned long long* cta = nullptr);
 // TD_DEBUG_TS: a one-thread kernel writing %globaltimer to *p (front-end gaps).
 cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
 

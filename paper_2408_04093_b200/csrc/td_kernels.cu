@@ -1392,7 +1392,7 @@ __device__ __forceinline__ float ld_ll(const uint2* p, unsigned e, int* err) {
         asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(f) : "l"(p) : "memory");
         if (f == e) break;
         if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
-            atomicExch(err, 1);
+            *reinterpret_cast<volatile int*>(err) = 1;  // mapped host memory: a plain store
             break;
         }
     }
@@ -1497,7 +1497,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
             }
             if (__all_sync(0xffffffffu, all)) break;
             if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
-                atomicExch(x.error, 1);
+                *reinterpret_cast<volatile int*>(x.error) = 1;  // mapped host memory: a plain store
                 break;
             }
         }
@@ -1606,7 +1606,7 @@ __global__ void k_combine_partials(int P, const float* lse, const float* out, in
     float shift = -CUDART_INF_F;
     for (int p = 0; p < P; ++p) shift = fmaxf(shift, lse[p * rows + r]);
     if (shift == -CUDART_INF_F) {
-        if (threadIdx.x == 0) atomicExch(bad_row, 1);
+        if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(bad_row) = 1;  // mapped host flag
         for (int j = threadIdx.x; j < d; j += blockDim.x) result[r * d + j] = 0.f;
         return;
     }
@@ -1661,16 +1661,12 @@ size_t bf16_smem() {
 }
 size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 * 4 + 128; }
 
-unsigned long long* g_dbg = nullptr;  // set by set_debug_stamps
-unsigned long long* g_tl = nullptr;   // set by set_timeline
-unsigned long long* g_tl_cta = nullptr;
-
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
     K1Args a{};
-    a.dbg = g_dbg;
-    a.tl = g_tl;
-    a.tl_cta = g_tl_cta;
+    a.dbg = p.dbg;
+    a.tl = p.tl;
+    a.tl_cta = p.tl_cta;
     static const int early = [] { const char* e = std::getenv("TD_K1_EARLY_TRIGGER"); return e ? std::atoi(e) : 0; }();
     a.early_trigger = early;
     static const int rev = [] { const char* e = std::getenv("TD_DEBUG_REVERSE"); return e ? std::atoi(e) : 0; }();
@@ -1769,12 +1765,6 @@ cudaError_t prefer_max_smem(K kernel) {
 
 }  // namespace
 
-void set_debug_stamps(unsigned long long* buf) { g_dbg = buf; }
-void set_timeline(unsigned long long* slot, unsigned long long* cta) {
-    g_tl = slot;
-    g_tl_cta = cta;
-}
-
 __global__ void k_stamp(unsigned long long* p) { *p = gtimer(); }
 cudaError_t launch_stamp(unsigned long long* p, cudaStream_t st) {
     prefer_max_smem(k_stamp);
@@ -1864,7 +1854,7 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     const int64_t per_cta = (p.total_tiles + p.ctas - 1) / p.ctas;
     const int64_t tpb = p.tiles_per_bh > 0 ? p.tiles_per_bh : 1;
     p.maxseg = static_cast<int>((per_cta + tpb - 1) / tpb + 1);
-    if (p.maxseg > 32) {
+    if (p.maxseg > kMaxSegments) {
         msg = "decode: too many (batch, head) rows per CTA for a split plan";
         return false;
     }
@@ -1938,8 +1928,9 @@ namespace {
 // that kernel drains and wait in griddepcontrol.wait before touching any input,
 // so the ~3-5 us kernel-to-kernel launch gap leaves the critical path.
 template <typename Kern, typename... Args>
-cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
-    static const bool on = [] { const char* e = std::getenv("TD_K1_PDL"); return !e || std::atoi(e) != 0; }();
+cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, bool allow, Args... args) {
+    static const bool env_on = [] { const char* e = std::getenv("TD_K1_PDL"); return !e || std::atoi(e) != 0; }();
+    const bool on = env_on && allow;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(static_cast<unsigned>(block));
@@ -1966,7 +1957,7 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
         auto kern = k1_bf16<DD, kBf16Tile, bf16_warps(DD), bf16_stages(DD)>;                \
         const size_t sm = bf16_smem<DD>();                                                  \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;                              \
-        if ((e = launch_pdl(kern, p.ctas, bf16_warps(DD) * 32, sm, st, a, *tmk, *tmv)) != cudaSuccess) return e; \
+        if ((e = launch_pdl(kern, p.ctas, bf16_warps(DD) * 32, sm, st, p.pdl, a, *tmk, *tmv)) != cudaSuccess) return e; \
         break;                                                                              \
     }
             TD_LAUNCH_BF16(64)
@@ -1982,7 +1973,7 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
     case GG: {                                                              \
         auto kern = k1_f32<kF32Tile, kF32Warps, kF32Stages, GG>;            \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;              \
-        if ((e = launch_pdl(kern, p.ctas, kF32Warps * 32, sm, st, a)) != cudaSuccess) return e; \
+        if ((e = launch_pdl(kern, p.ctas, kF32Warps * 32, sm, st, p.pdl, a)) != cudaSuccess) return e; \
         break;                                                              \
     }
             TD_LAUNCH_F32(1)
@@ -1994,10 +1985,10 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
         size_t sm = sizeof(float) * 3 * kGenWarps * p.maxseg * p.group;
         if (p.dtype == kBF16) {
             if ((e = set_smem(k1_generic<__nv_bfloat16>, sm)) != cudaSuccess) return e;
-            if ((e = launch_pdl(k1_generic<__nv_bfloat16>, p.ctas, kGenWarps * 32, sm, st, a)) != cudaSuccess) return e;
+            if ((e = launch_pdl(k1_generic<__nv_bfloat16>, p.ctas, kGenWarps * 32, sm, st, p.pdl, a)) != cudaSuccess) return e;
         } else {
             if ((e = set_smem(k1_generic<float>, sm)) != cudaSuccess) return e;
-            if ((e = launch_pdl(k1_generic<float>, p.ctas, kGenWarps * 32, sm, st, a)) != cudaSuccess) return e;
+            if ((e = launch_pdl(k1_generic<float>, p.ctas, kGenWarps * 32, sm, st, p.pdl, a)) != cudaSuccess) return e;
         }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -2280,7 +2271,7 @@ cudaError_t launch_kv_append(int dtype, void* k, void* v, const void* kt, const 
     const int words = d * dtype_bytes(dtype) / 2;  // 16-bit words per token row
     const int64_t n = rows * words;
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1024));
-    return launch_pdl(k_kv_append, grid < 1 ? 1 : grid, 256, 0, st, static_cast<uint16_t*>(k),
+    return launch_pdl(k_kv_append, grid < 1 ? 1 : grid, 256, 0, st, true, static_cast<uint16_t*>(k),
                       static_cast<uint16_t*>(v), static_cast<const uint16_t*>(kt), static_cast<const uint16_t*>(vt),
                       rows, cap * words, pos, words);
 }

@@ -128,6 +128,28 @@ def comm_volume_formula_seq(algo: DecodeAlgo, b: int, seq_len: int, d: int, n_h:
     return comm_volume_formula(algo, b, 0.0, d, n_h, p)
 
 
+def _ceil_log2(p: int) -> int:  # reduce.cpp:24-27
+    return 0 if p <= 1 else (p - 1).bit_length()
+
+
+def allreduce_rounds(strategy: ReduceStrategy, nodes: int, gpus_per_node: int) -> tuple[int, int]:
+    """(reduce rounds, total rounds) of allreduce_schedule (reduce.cpp:60-139):
+    TreeBinary ceil(log2 p) + its broadcast, Ring (p-1) + (p-1), Hierarchical
+    (g-1) intra + ceil(log2 nodes) inter, mirrored. Every strategy moves
+    2(p-1) transfers in total; only the round count differs."""
+    if nodes < 1 or gpus_per_node < 1:
+        raise InvalidArgument(_capi.TD_EINVAL, "allreduce_schedule: bad topology")
+    p = nodes * gpus_per_node
+    strategy = ReduceStrategy(strategy)
+    if strategy == ReduceStrategy.TreeBinary:
+        r = _ceil_log2(p)
+        return r, 2 * r
+    if strategy == ReduceStrategy.Ring:
+        return p - 1, 2 * (p - 1)
+    r = (gpus_per_node - 1) + _ceil_log2(nodes)
+    return r, 2 * r
+
+
 def ring_schedule(p: int) -> list[list[tuple[int, int, int]]]:
     """Per round r: (worker, chunk held, chunk received) -- decode.cpp:213-238."""
     return [[(w, (w - r) % p, (w - 1 - r) % p) for w in range(p)] for r in range(p - 1)]
@@ -154,16 +176,27 @@ class CostAccount:  # cluster.hpp:197-212, reporting conventions of decode.cpp:4
         return self.wire_elems_intra + self.wire_elems_inter
 
 
-def tree_cost(b: int, n_q: int, n_kv: int, seq_len: int, d_h: int, p: int) -> CostAccount:
+def tree_cost(b: int, n_q: int, n_kv: int, seq_len: int, d_h: int, p: int,
+              strategy: ReduceStrategy = ReduceStrategy.Hierarchical, topo: Topology | None = None) -> CostAccount:
     """Counters of one tree decode step (decode.cpp:110-177): convention volume
-    2(p-1)/p (b d + 2 b n_h); wire = 2(p-1) (b d + 2 b n_h) for the 2(p-1)-round
-    single-node schedules; peak = Mem_tree with GQA-corrected KV (n_kv heads)."""
+    2(p-1)/p (b d + 2 b n_h); wire = 2(p-1) (b d + 2 b n_h) (every allreduce
+    schedule moves 2(p-1) transfers of each payload); rounds = two collectives
+    of the strategy's schedule; peak = Mem_tree with GQA-corrected KV (n_kv heads)."""
     d = n_q * d_h
     t = math.ceil(seq_len / p)
+    topo = topo or topology_for_workers(p)
     vol = comm_volume_formula_seq(DecodeAlgo.Tree, b, seq_len, d, n_q, p)
     wire = 2 * (p - 1) * (b * d + 2 * b * n_q)
+    rounds = 2 * allreduce_rounds(strategy, topo.nodes, topo.gpus_per_node)[1]
     peak = 2 * b * t * n_kv * d_h + 2 * b * d + 2 * b * n_q
-    return CostAccount(vol, 0.0, wire, 0, 0, peak)
+    return CostAccount(vol, 0.0, wire, 0, rounds, peak)
+
+
+def tree_collectives(strategy: ReduceStrategy, topo: Topology) -> list[tuple[int, int]]:
+    """DecodeResult.collectives of tree_decode (decode.cpp:140-142, 161-162):
+    (reduce rounds, broadcast rounds) of the max and of the fused sum allreduce."""
+    red, tot = allreduce_rounds(strategy, topo.nodes, topo.gpus_per_node)
+    return [(red, tot - red)] * 2
 
 
 def ring_cost(b: int, n_q: int, n_kv: int, seq_len: int, d_h: int, p: int) -> CostAccount:
@@ -443,7 +476,9 @@ def tree_decode(q, cache: ShardedKVCache, topo: Topology, strategy: ReduceStrate
     b, n_q, d = q3.shape
     n_kv = cache.k_chunks[0].shape[1]
     p = cache.workers()
-    return DecodeResult(out, tree_cost(b, n_q, n_kv, cache.seq_len, d, p), [(p - 1, p - 1)] * 2)
+    strategy = ReduceStrategy(strategy)
+    return DecodeResult(out, tree_cost(b, n_q, n_kv, cache.seq_len, d, p, strategy, topo),
+                        tree_collectives(strategy, topo))
 
 
 def ring_decode(q, cache: ShardedKVCache, topo: Topology, scale: float = 1.0) -> DecodeResult:
@@ -575,6 +610,9 @@ class Worker:
             if ext != ln:
                 raise InvalidArgument(_capi.TD_EINVAL, "place_kv: shard length does not match chunk_extents")
         k, v = k.contiguous(), v.contiguous()
+        if k.is_cuda != v.is_cuda:
+            raise InvalidArgument(_capi.TD_EINVAL, "place_kv: k and v must both be on the host or on the device")
+        self._sync_in(k)  # the device copy runs on the worker's stream: after k / v's producers
         check(lib().td_kv_place(self.h, int(dtype_of(k)), b, n_kv, seq_len, d, start, ln, k.data_ptr(),
                                 v.data_ptr(), 0 if k.is_cuda else 1))
         self._meta(dtype_of(k), b, n_kv, seq_len, d)
@@ -676,6 +714,9 @@ class Worker:
         check(rc)
         if not host:
             self._sync_worker()
+            if flags & _capi.TD_P2P and self.p2p_status():
+                raise _capi.TreeDecError(_capi.TD_ECUDA, "tree_decode: NVLink exchange timed out (a peer never "
+                                                         "delivered its partial); call enable_p2p again on every rank")
         return out
 
     def tree_decode(self, q, scale: float = 1.0, strategy: ReduceStrategy = ReduceStrategy.Hierarchical,

@@ -78,11 +78,13 @@ def test_counters_match_reference(oracle, reference):
     for p in (1, 2, 4, 8):
         with reference.prepare(q, k, v, p, F64) as pr:
             # counters of a single row call: n_h = 1
-            _, _, ct = pr.decode(0, HIER)
-            tc = td.tree_cost(1, 1, 1, n, d_h, p)
-            assert ct[0] == pytest.approx(tc.elems_sent_total())
-            assert ct[1] == tc.wire_elems_total()
-            assert ct[2] == tc.peak_elems_per_worker
+            for strategy in (0, 1, 2):
+                _, _, ct = pr.decode(0, strategy)
+                tc = td.tree_cost(1, 1, 1, n, d_h, p, td.ReduceStrategy(strategy))
+                assert ct[0] == pytest.approx(tc.elems_sent_total())
+                assert ct[1] == tc.wire_elems_total()
+                assert ct[2] == tc.peak_elems_per_worker
+                assert ct[3] == tc.rounds
             _, _, cr = pr.decode(1, HIER)
             rc = td.ring_cost(1, 1, 1, n, d_h, p)
             assert cr[0] == pytest.approx(rc.elems_sent_total())
@@ -108,3 +110,14 @@ def test_llama_shape_accounting():
     assert tc.elems_sent_total() == pytest.approx(2 * 7 / 8 * (32 * 128 + 2 * 32))
     rc = td.ring_cost(b, n_q, n_kv, n, d, p)
     assert rc.wire_elems_total() == 2 * n_kv * d * n * 7
+
+
+def test_allreduce_rounds_match_reference_schedules(oracle):
+    """allreduce_rounds / tree_collectives equal allreduce_schedule's round counts
+    (reduce.cpp:60-139) for every strategy and topology."""
+    for strategy in (0, 1, 2):
+        for nodes, gpus in ((1, 1), (1, 2), (1, 3), (1, 4), (1, 7), (1, 8), (2, 8), (3, 8), (4, 4)):
+            want = oracle.schedule_rounds(strategy, nodes, gpus)
+            assert td.allreduce_rounds(td.ReduceStrategy(strategy), nodes, gpus) == want
+            red, tot = want
+            assert td.tree_collectives(td.ReduceStrategy(strategy), td.Topology(nodes, gpus)) == [(red, tot - red)] * 2
