@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=None)
     ap.add_argument("--phases", action="store_true", help="add a per-phase breakdown (phases_us)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed output")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="N > 1: skip the ring pass-KV and paper-literal NCCL comparison records")
+    ap.add_argument("--compare-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -230,6 +234,52 @@ def align_streams(world, stream):
     stream.wait_event(ev)
 
 
+def bench_config(args, wl, world, combine, flush):
+    """The config dict of a bench line (both arms: the driver matches them key by key)."""
+    desc, b, n_q, n_kv, n, d, dt = wl
+    n = args.seq_len or n
+    return {"workload": args.workload, "desc": desc, "seq_len": n, "batch": b, "q_heads": n_q,
+            "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": math.ceil(n / world),
+            "algo": args.algo, "combine": combine, "scale": args.scale,
+            "nccl_algo": os.environ.get("NCCL_ALGO", "auto") if world > 1 else None,
+            "l2": "flushed between steps (read-only sweep of 256 MB, timed apart and subtracted)" if flush
+            else "inputs larger than L2 (KV shard > 4x126 MB)",
+            "parallelism": f"sp{world} (sequence-sharded KV)"}
+
+
+def parity_leg(args, wl, q_dev, out_dev, world):
+    """THE CHECKER (rank 0, after timing): the timed run's device output against
+    the oracle -- the reference algorithm in Float64 on the same bf16 / f32
+    inputs (oracle/full.py) -- on every row when b * n_q <= 64, else one query
+    row per (batch, kv-head) pair, rotating through the group."""
+    import numpy as np
+
+    from oracle.full import full_decode, rel_err_rows
+    from oracle.oracle import BF16, F32, Oracle
+    _, b, n_q, n_kv, n, d, dt = wl
+    n = args.seq_len or n
+    t0 = time.time()
+    orc = Oracle()
+    seed = orc.mix64(0, n)
+    dtc = BF16 if dt == "bf16" else F32
+    qh = orc.seeded(orc.mix64(seed, 1), b * n_q * d, dtc).reshape(b, n_q, d)
+    if not np.array_equal(q_dev.double().cpu().numpy(), qh):
+        return {"max_rel_err": None, "ok": False, "note": "device query differs from the reference generator"}
+    g = n_q // n_kv
+    if b * n_q <= 64:
+        rows = None
+    else:
+        rows = [(ib, kvh * g + (ib + kvh) % g) for ib in range(b) for kvh in range(n_kv)]
+    want = full_decode(orc, qh, n_kv, n, orc.mix64(seed, 2), orc.mix64(seed, 3), dtc, args.scale, rows=rows)
+    err = rel_err_rows(out_dev.double().cpu().numpy(), want)
+    tol = 1e-3 if dt == "bf16" else 1e-5
+    return {"max_rel_err": err, "tol": tol, "ok": bool(err <= tol), "rows_checked": len(want),
+            "rows_total": b * n_q, "kv_rows_covered": len({(ib, h // g) for ib, h in want}),
+            "oracle": "reference decode in Float64 on the same dtype-rounded inputs (oracle/treedec_oracle.c, "
+                      "per (batch, kv-head) row, token-range partials + combine_partials)",
+            "seconds": round(time.time() - t0, 1)}
+
+
 # ---------------------------------------------------------------- CPU reference (oracle/_ref)
 def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
     """Times the reference's own tree_decode (compiled from /root/reference by
@@ -258,7 +308,7 @@ def reference_cpu(args, wl, n_gpus, sample_heads, nthreads, steps=1, warmup=0):
         for i in range(warmup + steps):
             _, secs, _ = pr.decode(0, HIER, args.scale, parallel=n_gpus > 1, nthreads=nthreads)
             if i >= warmup:
-                vals.append(secs / sample_heads * rows * 1e6 / b)  # us per decoded token
+                vals.append(secs / sample_heads * rows * 1e6)  # us per decode step (= per token of each sequence)
     cores = nthreads * (n_gpus if n_gpus > 1 else 1)
     return vals, {
         "sample": f"{sample_heads} query row(s) over one kv head at N={n}, p={n_gpus} worker(s), {nthreads} row "
@@ -280,10 +330,11 @@ def run_reference_arm(args, wl, world, rank):
     value = sum(vals) / len(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "µs/token", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * b / 1000.0, "higher_is_better": False,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value / 1000.0, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": dt, "data": "synthetic (reference generator)",
-        "config": {"workload": args.workload, "seq_len": args.seq_len or n, "batch": b, "q_heads": n_q,
-                   "kv_heads": n_kv, "head_dim": d, "shards": args.gpus, "algo": "tree"},
+        "config": bench_config(args, wl, args.gpus, combine=("p2p" if args.gpus > 1 else "none"),
+                               flush=2 * b * n_kv * math.ceil((args.seq_len or n) / args.gpus) * d
+                               * (2 if dt == "bf16" else 4) < 4 * L2_BYTES),
         "cpu_baseline": {"value": value, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
                          "sample": info["sample"] + f"; host nproc={nproc}, {cpu_model()}"},
         "e2e": {"value": value, "unit": "µs/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -331,7 +382,13 @@ def main():
     stream_ptr = w.stream
     stream = torch.cuda.ExternalStream(stream_ptr)
     flush = shard_bytes < 4 * L2_BYTES
-    scratch = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if flush else None
+    # L2 flush by a read-only sweep of 256 MB (> 2 x L2): it leaves clean lines, so
+    # the decode that follows pays no write-back of a flush's dirty lines
+    scratch = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda") if flush else None
+    flush_sink = torch.empty(1, dtype=torch.float32, device="cuda") if flush else None
+
+    def flush_l2():
+        torch.sum(scratch, dim=0, out=flush_sink)
     decode = w.tree_decode_async if args.algo == "tree" else w.ring_decode_async
     flags_timed = _capi.TD_TIME_KERNELS
     base_flags = 0
@@ -375,7 +432,7 @@ def main():
             if flush:
                 fl[i][0].record(stream)
                 with torch.cuda.stream(stream):
-                    scratch.fill_(i & 0xFF)
+                    flush_l2()
                 fl[i][1].record(stream)
             step(0)
         ev_b.record(stream)
@@ -387,9 +444,10 @@ def main():
         for i in range(args.steps):
             if flush:
                 with torch.cuda.stream(stream):
-                    scratch.fill_(i & 0xFF)
+                    flush_l2()
             step(flags_timed)
         barrier(world)
+    out_timed = out.clone()  # the timed run's output (checked against the oracle below)
     flush_ms = sum(a.elapsed_time(bb) for a, bb in fl) if flush else 0.0
     ms_local = (ev_a.elapsed_time(ev_b) - flush_ms) / args.steps
     k1_ms, k1_calls = w.kernel_time()
@@ -409,7 +467,7 @@ def main():
     for i in range(e2e_steps):
         if flush:
             with torch.cuda.stream(stream):
-                scratch.fill_(i & 0xFF)
+                flush_l2()
             stream.synchronize()
         t0 = time.perf_counter()
         decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO | base_flags)
@@ -431,6 +489,62 @@ def main():
         barrier(world)
         phases = [round(max_over_ranks(x, world) * 1000.0, 2) for x in w.phase_times()]
 
+    # ---- N > 1: the paper-literal NCCL combine and the ring pass-KV schedule on the
+    # same cache, fewer steps (the reference's run_sweep times tree and ring for
+    # every cell, bench.cpp:83-112)
+    compare = None
+    if world > 1 and args.algo == "tree" and not args.no_compare:
+        def timed_loop(fn, steps):
+            for _ in range(2):
+                fn(0)
+            barrier(world)
+            align_streams(world, stream)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            ea.record(stream)
+            for i in range(steps):
+                if flush:
+                    fe[i][0].record(stream)
+                    with torch.cuda.stream(stream):
+                        flush_l2()
+                    fe[i][1].record(stream)
+                fn(0)
+            eb.record(stream)
+            barrier(world)
+            f_ms = sum(x.elapsed_time(y) for x, y in fe) if flush else 0.0
+            return max_over_ranks((ea.elapsed_time(eb) - f_ms) / steps, world)
+
+        ks = max(3, args.compare_steps)
+        nccl_ms = timed_loop(lambda fl: w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, fl), ks)
+        w.reset_kernel_timer()
+        align_streams(world, stream)
+        for _ in range(ks):
+            w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, _capi.TD_TIME_PHASES)
+        barrier(world)
+        nccl_phases = [round(max_over_ranks(x, world) * 1000.0, 2) for x in w.phase_times()]
+        ring_ms = timed_loop(lambda fl: w.ring_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, fl), ks)
+        compare = {
+            "steps": ks,
+            "tree_us": ms * 1000.0, "tree_combine": args.combine,
+            "nccl_us": nccl_ms * 1000.0,
+            "nccl_phases_us": dict(zip(("K1", "K2", "allreduce_max", "K3", "allreduce_sum", "K4"), nccl_phases)),
+            "ring_us": ring_ms * 1000.0,
+            "tree_over_ring": ring_ms / ms,
+            "note": "same cache and query; nccl = K1, K2, ncclAllReduce(max), K3, ncclAllReduce(sum), K4 "
+                    "(decode.cpp:129-173 literally); ring = p-1 NCCL send/recv rotations of the KV shards with "
+                    "the partial of the chunk in hand overlapped (decode.cpp:186-251); tree_over_ring = "
+                    "ring_us / tree_us",
+        }
+
+    # ---- parity of the timed output (rank 0; the checker, not the product)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_leg(args, wl, q, out_timed, world)
+        except Exception as e:  # the oracle library may be absent on a foreign box
+            parity = {"max_rel_err": None, "ok": False, "note": f"unavailable: {e}"}
+    barrier(world)
+
     # ---- CPU reference baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -450,18 +564,15 @@ def main():
         peak, peak_kind = load_peaks()
         kv_per_rank = 2 * b * n_kv * math.ceil(n / world) * d * esz
         achieved = kv_per_rank / (k1_ms_max * 1e-3) / 1e9 if k1_ms_max > 0 else None
+        # latency per decoded token = the step: each of the b sequences gets its
+        # next token when the step ends (b = 1 at the default workload)
         line = {
-            "metric": METRIC, "value": ms * 1000.0 / b, "unit": "µs/token", "n_gpus": world,
+            "metric": METRIC, "value": ms * 1000.0, "unit": "µs/token", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": dt,
             "data": "synthetic (reference SplitMix64 generator, generated on device)",
-            "config": {"workload": args.workload, "desc": desc, "seq_len": n, "batch": b, "q_heads": n_q,
-                       "kv_heads": n_kv, "head_dim": d, "shards": world, "shard_tokens": shard_len,
-                       "algo": args.algo, "combine": args.combine if world > 1 and args.algo == "tree" else "none",
-                       "scale": args.scale,
-                       "nccl_algo": os.environ.get("NCCL_ALGO", "auto") if world > 1 else None,
-                       "l2": "flushed between steps" if flush else "inputs larger than L2 (KV shard > 4x126 MB)",
-                       "parallelism": f"sp{world} (sequence-sharded KV)"},
+            "config": bench_config(args, wl, world,
+                                   args.combine if world > 1 and args.algo == "tree" else "none", flush),
             "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
@@ -472,7 +583,13 @@ def main():
                          "step_frac": kv_per_rank / (ms * 1e-3) / 1e9 / peak,
                          "read_ceiling": read_ceiling(kv_per_rank)},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_ms * 1000.0 / b, "unit": "µs/token",
+            "parity": parity,
+            "compare": compare,
+            "ring_us": compare["ring_us"] if compare else None,
+            "nccl_us": compare["nccl_us"] if compare else None,
+            "tree_over_ring": compare["tree_over_ring"] if compare else None,
+            "sequences_per_s": b / (ms * 1e-3),
+            "e2e": {"value": e2e_ms * 1000.0, "unit": "µs/token",
                     "h2d_bytes_per_step": q.numel() * esz, "d2h_bytes_per_step": out.numel() * 4,
                     "matches_device_output": bool(ok)},
             "interconnect": interconnect(args, world, b, n_q, n_kv, n, d, esz, ms),

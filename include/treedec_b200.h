@@ -269,6 +269,32 @@ int td_last_launch_stats(td_context* ctx, int* kernels, double* kv_bytes, int* s
 /* Peak device bytes held by the context (KV shard, ring buffers, workspaces). */
 int td_memory_bytes(td_context* ctx, size_t* bytes);
 
+/* ---------------------------------------------------------------------
+ * Worker group: the reference's p in-process workers (decode.hpp:70-72,
+ * parallel_workers threads at decode.cpp:37-41) in ONE process. Worker w is a
+ * td_context on device devs[w * ndev / workers] (contiguous placement,
+ * cluster.hpp:18-24) with nranks = workers, rank = w; several workers may
+ * share a GPU. Place each worker's shard through its context
+ * (td_group_context + td_kv_place / td_kv_generate), open the exchange once
+ * (td_group_p2p_open: every worker's exchange buffer, peers addressed as
+ * device pointers over NVLink or in the same HBM -- no IPC, no NCCL), then
+ * td_group_tree_decode runs K1 + K2x on every worker from one host thread:
+ * the one-shot exact combine (allreduce(max) + rescale + allreduce(sum) +
+ * divide, decode.cpp:129-173). Device q / out live on worker 0's device and
+ * are ordered on worker 0's stream (td_stream of worker 0); TD_HOST_IO takes
+ * host buffers and returns after every worker's step, reporting an exchange
+ * timeout as TD_ECUDA. Workers sharing a GPU launch K1 without the
+ * programmatic early launch (a waiting grid would hold the SMs a peer's K1
+ * needs) and skip the per-SM calibration (the SMs are shared).
+ * ------------------------------------------------------------------- */
+typedef struct td_group td_group;
+int td_group_create(int ndev, const int* devs, int workers, td_group** group);
+int td_group_destroy(td_group* group);
+int td_group_context(td_group* group, int worker, td_context** ctx);
+int td_group_p2p_open(td_group* group, int64_t max_rows, int64_t d);
+int td_group_tree_decode(td_group* group, const void* q, int64_t n_q, double scale, int strategy, float* out,
+                         int flags);
+
 #ifdef __cplusplus
 }
 #endif

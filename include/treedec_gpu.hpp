@@ -8,12 +8,18 @@
 // return a treedec::DecodeResult; status codes come back as the reference's
 // exception types (invalid_argument / domain_error / runtime_error).
 //
-// In one process the p workers of the ShardedKVCache run on one GPU, each
-// worker's chunk placed in HBM and reduced with the split-KV kernel
-// (td_local_partial); the max-allreduce / rescale / sum-allreduce / divide
-// of the p partials is the single-device combine kernel
-// (td_combine_partials). Across GPUs the same call sequence runs one
-// process per GPU with td_comm_init + td_tree_decode.
+// tree_decode runs the p workers of the ShardedKVCache as a td_group: worker w
+// is a context on GPU w * ndev / p of the visible GPUs (contiguous placement,
+// cluster.hpp:18-24; several workers share a GPU when p exceeds the GPU
+// count), its chunk placed in that GPU's HBM, and every worker runs the
+// split-KV kernel and the one-shot exchange combine (allreduce(max) / rescale
+// / allreduce(sum) / divide, decode.cpp:129-173) with its peers addressed as
+// device pointers. The group is created once per worker count and reused
+// (calls are serialised by a mutex, so the functions stay callable from any
+// thread like the reference's). ring_decode folds the per-worker partials
+// with combine_pair in the reference order on one cached context. Across
+// processes the same kernels run one process per GPU with td_comm_init +
+// td_tree_decode.
 //
 // Inputs must be Float32 or Bf16 tensors (the GPU computes in fp32 on those
 // grids); Float64 tensors raise invalid_argument. The output is stored
@@ -24,6 +30,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -93,7 +100,7 @@ inline int code_of(DType dt) {
 }
 
 // Places worker w's chunk (k/v [b, n_h, t, d]) and returns its fp32 partial.
-inline void chunk_partial(Context& ctx, const Tensor& q, const Tensor& k, const Tensor& v,
+inline void chunk_partial(td_context* ctx, const Tensor& q, const Tensor& k, const Tensor& v,
                           std::int64_t seq_len, std::int64_t start, double scale, float* rm,
                           float* lse, float* out_dev) {
     const int dt = code_of(q.dtype());
@@ -101,20 +108,64 @@ inline void chunk_partial(Context& ctx, const Tensor& q, const Tensor& k, const 
     const std::int64_t n_q = q.extent(1);
     if (dt == TD_BF16) {
         const auto kb = to_bf16(k.data()), vb = to_bf16(v.data()), qb = to_bf16(q.data());
-        check(td_kv_place(ctx.h, dt, b, n_kv, seq_len, d, start, t, kb.data(), vb.data(), 1));
+        check(td_kv_place(ctx, dt, b, n_kv, seq_len, d, start, t, kb.data(), vb.data(), 1));
         std::vector<float> hrm(b * n_q), hl(b * n_q), ho(b * n_q * d);
-        check(td_local_partial(ctx.h, qb.data(), n_q, scale, hrm.data(), hl.data(), ho.data(), TD_HOST_IO));
+        check(td_local_partial(ctx, qb.data(), n_q, scale, hrm.data(), hl.data(), ho.data(), TD_HOST_IO));
         cuda(cudaMemcpy(rm, hrm.data(), hrm.size() * 4, cudaMemcpyHostToDevice), "copy");
         cuda(cudaMemcpy(lse, hl.data(), hl.size() * 4, cudaMemcpyHostToDevice), "copy");
         cuda(cudaMemcpy(out_dev, ho.data(), ho.size() * 4, cudaMemcpyHostToDevice), "copy");
     } else {
         const auto kf = to_f32(k.data()), vf = to_f32(v.data()), qf = to_f32(q.data());
-        check(td_kv_place(ctx.h, dt, b, n_kv, seq_len, d, start, t, kf.data(), vf.data(), 1));
+        check(td_kv_place(ctx, dt, b, n_kv, seq_len, d, start, t, kf.data(), vf.data(), 1));
         std::vector<float> hrm(b * n_q), hl(b * n_q), ho(b * n_q * d);
-        check(td_local_partial(ctx.h, qf.data(), n_q, scale, hrm.data(), hl.data(), ho.data(), TD_HOST_IO));
+        check(td_local_partial(ctx, qf.data(), n_q, scale, hrm.data(), hl.data(), ho.data(), TD_HOST_IO));
         cuda(cudaMemcpy(rm, hrm.data(), hrm.size() * 4, cudaMemcpyHostToDevice), "copy");
         cuda(cudaMemcpy(lse, hl.data(), hl.size() * 4, cudaMemcpyHostToDevice), "copy");
         cuda(cudaMemcpy(out_dev, ho.data(), ho.size() * 4, cudaMemcpyHostToDevice), "copy");
+    }
+}
+
+// The process-wide worker group of tree_decode (re-created when the worker
+// count changes) and the single context of ring_decode. Never destroyed: the
+// CUDA runtime may already be torn down when static destructors run.
+struct Cached {
+    std::mutex mu;
+    td_group* group = nullptr;
+    int workers = 0;
+    std::int64_t x_rows = 0, x_d = 0;
+    td_context* ring = nullptr;
+};
+inline Cached& cached() {
+    static Cached* c = new Cached;
+    return *c;
+}
+
+inline td_group* group_for(Cached& c, int p) {
+    if (c.group && c.workers == p) return c.group;
+    if (c.group) td_group_destroy(c.group);
+    c.group = nullptr;
+    c.workers = 0;
+    c.x_rows = c.x_d = 0;
+    int n = 0;
+    cuda(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (n < 1) throw std::runtime_error("treedec::gpu: no CUDA device");
+    std::vector<int> devs(static_cast<std::size_t>(std::min(n, p)));
+    for (std::size_t i = 0; i < devs.size(); ++i) devs[i] = static_cast<int>(i);
+    check(td_group_create(static_cast<int>(devs.size()), devs.data(), p, &c.group));
+    c.workers = p;
+    return c.group;
+}
+
+// Worker w's chunk of the cache into its context's HBM (host upload).
+inline void place_chunk(td_context* ctx, const Tensor& k, const Tensor& v, std::int64_t seq_len, std::int64_t start) {
+    const int dt = code_of(k.dtype());
+    const std::int64_t b = k.extent(0), n_kv = k.extent(1), t = k.extent(2), d = k.extent(3);
+    if (dt == TD_BF16) {
+        const auto kb = to_bf16(k.data()), vb = to_bf16(v.data());
+        check(td_kv_place(ctx, dt, b, n_kv, seq_len, d, start, t, kb.data(), vb.data(), 1));
+    } else {
+        const auto kf = to_f32(k.data()), vf = to_f32(v.data());
+        check(td_kv_place(ctx, dt, b, n_kv, seq_len, d, start, t, kf.data(), vf.data(), 1));
     }
 }
 
@@ -135,19 +186,34 @@ inline DecodeResult tree_decode(const Tensor& q, const ShardedKVCache& cache, co
     detail::require(q, cache, topo, "tree_decode");
     const int p = cache.workers();
     const std::int64_t b = q.extent(0), n_h = q.extent(1), d_h = q.extent(3), rows = b * n_h;
-    detail::Context ctx(0);
-    detail::DeviceArray<float> rm(std::size_t(p) * rows), lse(std::size_t(p) * rows),
-        out(std::size_t(p) * rows * d_h), res(std::size_t(rows) * d_h);
-    std::int64_t start = 0;
-    for (int w = 0; w < p; ++w) {
-        const Tensor& k = cache.k_chunks[std::size_t(w)];
-        detail::chunk_partial(ctx, q, k, cache.v_chunks[std::size_t(w)], cache.seq_len, start, scale,
-                              rm.p + w * rows, lse.p + w * rows, out.p + w * rows * d_h);
-        start += k.extent(2);
-    }
-    detail::check(td_combine_partials(p, lse.p, out.p, rows, d_h, res.p, nullptr));
+    const int dt = detail::code_of(q.dtype());
     std::vector<float> host(std::size_t(rows) * d_h);
-    detail::cuda(cudaMemcpy(host.data(), res.p, host.size() * 4, cudaMemcpyDeviceToHost), "copy");
+    {
+        detail::Cached& c = detail::cached();
+        std::lock_guard<std::mutex> lock(c.mu);
+        td_group* g = detail::group_for(c, p);
+        std::int64_t start = 0;
+        for (int w = 0; w < p; ++w) {
+            td_context* ctx = nullptr;
+            detail::check(td_group_context(g, w, &ctx));
+            const Tensor& k = cache.k_chunks[std::size_t(w)];
+            detail::place_chunk(ctx, k, cache.v_chunks[std::size_t(w)], cache.seq_len, start);
+            start += k.extent(2);
+        }
+        if (c.x_rows < rows || c.x_d != d_h) {
+            detail::check(td_group_p2p_open(g, rows, d_h));
+            c.x_rows = rows;
+            c.x_d = d_h;
+        }
+        const int strategy = static_cast<int>(allreduce_strategy);
+        if (dt == TD_BF16) {
+            const auto qb = detail::to_bf16(q.data());
+            detail::check(td_group_tree_decode(g, qb.data(), n_h, scale, strategy, host.data(), TD_HOST_IO));
+        } else {
+            const auto qf = detail::to_f32(q.data());
+            detail::check(td_group_tree_decode(g, qf.data(), n_h, scale, strategy, host.data(), TD_HOST_IO));
+        }
+    }
     DecodeResult r;
     r.output = Tensor({b, n_h, 1, d_h}, std::vector<double>(host.begin(), host.end()), q.dtype());
     const ReductionSchedule s = allreduce_schedule(allreduce_strategy, topo.nodes, topo.gpus_per_node);
@@ -169,23 +235,28 @@ inline DecodeResult ring_decode(const Tensor& q, const ShardedKVCache& cache, co
     detail::require(q, cache, topo, "ring_decode");
     const int p = cache.workers();
     const std::int64_t b = q.extent(0), n_h = q.extent(1), d_h = q.extent(3), rows = b * n_h;
-    detail::Context ctx(0);
-    detail::DeviceArray<float> rm(std::size_t(p) * rows), lse(std::size_t(p) * rows),
-        out(std::size_t(p) * rows * d_h);
-    std::int64_t start = 0;
-    for (int w = 0; w < p; ++w) {
-        const Tensor& k = cache.k_chunks[std::size_t(w)];
-        detail::chunk_partial(ctx, q, k, cache.v_chunks[std::size_t(w)], cache.seq_len, start, scale,
-                              rm.p + w * rows, lse.p + w * rows, out.p + w * rows * d_h);
-        start += k.extent(2);
-    }
-    for (int r = 0; r + 1 < p; ++r) {  // root = parts[0]; fold parts[(p-1-r) mod p]
-        const int inc = ((p - 1 - r) % p + p) % p;
-        detail::check(td_combine_pair(rm.p, lse.p, out.p, rm.p + inc * rows, lse.p + inc * rows,
-                                      out.p + inc * rows * d_h, rows, d_h, nullptr));
-    }
     std::vector<float> host(std::size_t(rows) * d_h);
-    detail::cuda(cudaMemcpy(host.data(), out.p, host.size() * 4, cudaMemcpyDeviceToHost), "copy");
+    {
+        detail::Cached& c = detail::cached();
+        std::lock_guard<std::mutex> lock(c.mu);
+        if (!c.ring) detail::check(td_create(0, &c.ring));
+        detail::cuda(cudaSetDevice(0), "cudaSetDevice");
+        detail::DeviceArray<float> rm(std::size_t(p) * rows), lse(std::size_t(p) * rows),
+            out(std::size_t(p) * rows * d_h);
+        std::int64_t start = 0;
+        for (int w = 0; w < p; ++w) {
+            const Tensor& k = cache.k_chunks[std::size_t(w)];
+            detail::chunk_partial(c.ring, q, k, cache.v_chunks[std::size_t(w)], cache.seq_len, start, scale,
+                                  rm.p + w * rows, lse.p + w * rows, out.p + w * rows * d_h);
+            start += k.extent(2);
+        }
+        for (int r = 0; r + 1 < p; ++r) {  // root = parts[0]; fold parts[(p-1-r) mod p]
+            const int inc = ((p - 1 - r) % p + p) % p;
+            detail::check(td_combine_pair(rm.p, lse.p, out.p, rm.p + inc * rows, lse.p + inc * rows,
+                                          out.p + inc * rows * d_h, rows, d_h, nullptr));
+        }
+        detail::cuda(cudaMemcpy(host.data(), out.p, host.size() * 4, cudaMemcpyDeviceToHost), "copy");
+    }
     DecodeResult r;
     r.output = Tensor({b, n_h, 1, d_h}, std::vector<double>(host.begin(), host.end()), q.dtype());
     r.cost.rounds = static_cast<std::uint64_t>(p - 1);

@@ -9,7 +9,7 @@ from ._capi import DomainError, InvalidArgument, TreeDecError  # noqa: F401
 from .decode import (  # noqa: F401
     CostAccount, DecodeAlgo, DecodeResult, allreduce_rounds, tree_collectives, DType, EnergyEval, ReduceStrategy, ShardedKVCache, SoftmaxPartial,
     Topology, energy, energy_forward_parallel, energy_grad_parallel, energy_partial,
-    Worker, attention_chunk_partial, chunk_extents, combine_pair, combine_partials, comm_volume_formula,
+    Worker, WorkerGroup, attention_chunk_partial, chunk_extents, combine_pair, combine_partials, comm_volume_formula,
     comm_volume_formula_seq, decode_tolerance_abs, finalize, partial_to_numerator, peak_memory_formula,
     ring_cost, ring_decode, ring_fold_order, ring_schedule, seeded_tensor, set_deterministic, shard_kv, shard_range, tree_cost,
     tree_decode, topology_for_workers,

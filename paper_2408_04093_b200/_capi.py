@@ -28,6 +28,7 @@ EXPORTS = [
     "td_energy_forward", "td_energy_grad", "td_calibration_info",
     "td_tree_decode", "td_ring_decode", "td_local_partial", "td_output_bf16", "td_kernel_time",
     "td_reset_kernel_timer", "td_phase_times", "td_debug_stamps", "td_last_launch_stats", "td_memory_bytes",
+    "td_group_create", "td_group_destroy", "td_group_context", "td_group_p2p_open", "td_group_tree_decode",
 ]
 
 
@@ -112,6 +113,11 @@ def lib() -> ctypes.CDLL:
     L.td_last_launch_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int)]
     L.td_memory_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_size_t)]
+    L.td_group_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(_vp)]
+    L.td_group_destroy.argtypes = [_vp]
+    L.td_group_context.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.td_group_p2p_open.argtypes = [_vp, _i64, _i64]
+    L.td_group_tree_decode.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_int, _vp, ctypes.c_int]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int or name not in ("td_last_error",):

@@ -916,8 +916,11 @@ int td_comm_info(td_context* ctx, int* nranks, int* rank) {
     return TD_OK;
 }
 
-int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char handle[64]) {
-    if (int rc = require_ctx(ctx)) return rc;
+}  // extern "C"
+
+// The exchange buffer of one rank, zeroed (epoch 0 matches no step), and its
+// timeout flag; the peers' pointers are set by td_p2p_open / td_group_p2p_open.
+static int xbuf_alloc(td_context* ctx, int64_t max_rows, int64_t d) {
     if (max_rows < 1 || d < 1 || d > 256) return set_err(TD_EINVAL, "p2p: bad max_rows / head_dim");
     for (void* ptr : ctx->x_opened) cudaIpcCloseMemHandle(ptr);
     ctx->x_opened.clear();
@@ -932,6 +935,14 @@ int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char ha
     ctx->x_max_rows = max_rows;
     ctx->x_d = d;
     ctx->x_epoch = 0;
+    return TD_OK;
+}
+
+extern "C" {
+
+int td_p2p_handle(td_context* ctx, int64_t max_rows, int64_t d, unsigned char handle[64]) {
+    if (int rc = require_ctx(ctx)) return rc;
+    if (int rc = xbuf_alloc(ctx, max_rows, d)) return rc;
     cudaIpcMemHandle_t h;
     TD_CUDA(cudaIpcGetMemHandle(&h, ctx->xbuf.p));
     static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
@@ -1194,8 +1205,22 @@ int td_debug_stamps(td_context* ctx, unsigned long long* out, int n) {
     return TD_OK;
 }
 
-int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
-                   float* out, int flags) {
+}  // extern "C"
+
+namespace {
+
+// The part of tree_decode before any launch: validation, per-row buffers, the
+// split plan (calibrating the partition on a context's first long decode) and
+// the query on the device. `q_on_device` overrides the staging of q (td_group
+// stages it itself).
+struct TreeCall {
+    SplitPlan plan;
+    const void* qd = nullptr;
+    int64_t rows = 0;
+};
+
+int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int flags, TreeCall& tc,
+               const void* q_on_device = nullptr) {
     if (int rc = require_ctx(ctx)) return rc;
     ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
     if (int rc = debug_begin(ctx, flags)) return rc;
@@ -1205,57 +1230,79 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "tree_decode: q/kv head mismatch");
     ctx->last_kernels = 0;
     ctx->last_kv_bytes = 0.0;
-    const int64_t rows = ctx->b * n_q;
-    const int64_t d = ctx->d;
-    if (int rc = ensure_rows(ctx, rows, d)) return rc;
-    SplitPlan plan;
-    if (int rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap)) return rc;
+    tc.rows = ctx->b * n_q;
+    if (int rc = ensure_rows(ctx, tc.rows, ctx->d)) return rc;
+    if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap)) return rc;
     int rc = TD_OK;
-    const void* qd = stage_q(ctx, q, n_q, flags, &rc);
+    tc.qd = q_on_device ? q_on_device : stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
     phase_begin(ctx, flags);
     phase_mark(ctx);
+    return TD_OK;
+}
+
+// K1 + K2x: split-KV partial, then one exchange + exact combine into xdst
+// (device memory or a mapped host buffer); no synchronisation.
+int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xdst, int flags) {
+    const SplitPlan& plan = tc.plan;
+    const int64_t d = ctx->d;
+    if (!ctx->x_ready) return set_err(TD_ESTATE, "tree_decode: TD_P2P without td_p2p_open");
+    if (tc.rows > ctx->x_max_rows || d != ctx->x_d)
+        return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
+    if (int rc = exchange_failed(ctx)) return rc;  // an earlier asynchronous step timed out
+    td::XchgArgs xa;
+    xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
+    xa.p = ctx->nranks;
+    xa.rank = ctx->rank;
+    xa.epoch = ctx->x_epoch + 1;  // committed only once the launch is in: all ranks stay in step
+    xa.max_rows = ctx->x_max_rows;
+    xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
+    xa.error = ctx->x_err;
+    static const int pull = [] { const char* e = std::getenv("TD_XCHG_PULL"); return e ? std::atoi(e) : 0; }();
+    xa.pull = pull;
+    const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
+    const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (flags & TD_TIME_KERNELS) {
+        cudaEvent_t* pr = next_timer(ctx);
+        e0 = pr[0];
+        e1 = pr[1];
+    } else if (ctx->cur_phase) {
+        e1 = (*ctx->cur_phase)[ctx->cur_mark++];
+    }
+    TD_CUDA(td::launch_decode_exchange(plan, tc.qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
+                                       ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
+    ctx->x_epoch = xa.epoch;
+    ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
+    phase_mark(ctx);
+    ctx->last_kernels = 2;  // K1 + K2x
+    ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
+                         td::dtype_bytes(ctx->dtype);
+    ctx->last_split_kernel = plan.kernel;
+    return TD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, int strategy,
+                   float* out, int flags) {
+    TreeCall tc;
+    if (int rc = tree_begin(ctx, q, n_q, strategy, flags, tc)) return rc;
+    const SplitPlan& plan = tc.plan;
+    const void* qd = tc.qd;
+    const int64_t rows = tc.rows;
+    const int64_t d = ctx->d;
+    int rc = TD_OK;
     if ((flags & TD_P2P) && ctx->nranks > 1) {
-        // K1 + K2x: split-KV partial, then one exchange + exact combine
-        if (!ctx->x_ready) return set_err(TD_ESTATE, "tree_decode: TD_P2P without td_p2p_open");
-        if (rows > ctx->x_max_rows || d != ctx->x_d)
-            return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
-        if (int rc = exchange_failed(ctx)) return rc;  // an earlier asynchronous step timed out
-        td::XchgArgs xa;
-        xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
-        xa.p = ctx->nranks;
-        xa.rank = ctx->rank;
-        xa.epoch = ctx->x_epoch + 1;  // committed only once the launch is in: all ranks stay in step
-        xa.max_rows = ctx->x_max_rows;
-        xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
-        xa.error = ctx->x_err;
-        static const int pull = [] { const char* e = std::getenv("TD_XCHG_PULL"); return e ? std::atoi(e) : 0; }();
-        xa.pull = pull;
-        const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
-        const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (flags & TD_TIME_KERNELS) {
-            cudaEvent_t* pr = next_timer(ctx);
-            e0 = pr[0];
-            e1 = pr[1];
-        } else if (ctx->cur_phase) {
-            e1 = (*ctx->cur_phase)[ctx->cur_mark++];
-        }
         float* xdst = out;
         if (flags & TD_HOST_IO) {
             float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
             xdst = m ? m : ctx->out;
         }
-        TD_CUDA(td::launch_decode_exchange(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
-                                           ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
-        ctx->x_epoch = xa.epoch;
-        ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
-        phase_mark(ctx);
-        ctx->last_kernels = 2;  // K1 + K2x
-        ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
-                             td::dtype_bytes(ctx->dtype);
-        ctx->last_split_kernel = plan.kernel;
-        if (int rc = deliver_out(ctx, xdst, rows, out, flags)) return rc;
+        if (int rc2 = launch_tree_p2p(ctx, tc, scale, xdst, flags)) return rc2;
+        if (int rc2 = deliver_out(ctx, xdst, rows, out, flags)) return rc2;
         return (flags & TD_HOST_IO) ? exchange_failed(ctx) : TD_OK;  // synchronised: this step's verdict
     }
     if (ctx->nranks == 1) {
@@ -1581,6 +1628,171 @@ int td_memory_bytes(td_context* ctx, size_t* bytes) {
         for (auto& x : rb) s += x.cap;
     *bytes = s;
     return TD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- single-process worker group
+// The reference runs its p workers in one process (decode.hpp:70-72; one
+// std::thread per worker with parallel_workers, decode.cpp:37-41). A td_group
+// is that: one context per worker, worker w on device devs[w * ndev / p]
+// (contiguous placement, cluster.hpp:18-24), the exchange buffers of the
+// one-shot combine addressed as plain device pointers (peer access over
+// NVLink, or the same HBM when workers share a GPU) instead of CUDA IPC, and
+// one host thread issuing every worker's launches asynchronously.
+struct td_group {
+    std::vector<td_context*> w;
+    std::vector<int> dev;
+    cudaEvent_t entry = nullptr;  // on worker 0's device: start of a call (orders the others after it)
+};
+
+extern "C" {
+
+int td_group_create(int ndev, const int* devs, int workers, td_group** out) {
+    if (!out) return set_err(TD_EINVAL, "td_group_create: null output");
+    *out = nullptr;
+    if (ndev < 1 || !devs || workers < 1) return set_err(TD_EINVAL, "td_group_create: need ndev >= 1 and workers >= 1");
+    int n = 0;
+    TD_CUDA(cudaGetDeviceCount(&n));
+    for (int i = 0; i < ndev; ++i)
+        if (devs[i] < 0 || devs[i] >= n) return set_err(TD_EINVAL, "td_group_create: no such device");
+    auto* g = new td_group;
+    auto fail = [&](int rc) {
+        td_group_destroy(g);
+        return rc;
+    };
+    for (int w = 0; w < workers; ++w) {
+        const int dv = devs[int64_t(w) * ndev / workers];
+        td_context* ctx = nullptr;
+        if (int rc = td_create(dv, &ctx)) return fail(rc);
+        ctx->nranks = workers;
+        ctx->rank = w;
+        g->w.push_back(ctx);
+        g->dev.push_back(dv);
+    }
+    for (int w = 0; w < workers; ++w)
+        for (int u = 0; u < workers; ++u)
+            if (u != w && g->dev[size_t(u)] == g->dev[size_t(w)]) g->w[size_t(w)]->shared_device = true;
+    // peer access between every pair of distinct devices (K2x stores into peers' HBM)
+    for (int a = 0; a < workers; ++a)
+        for (int b = 0; b < workers; ++b) {
+            const int da = g->dev[size_t(a)], db = g->dev[size_t(b)];
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) return fail(set_err(TD_ECUDA, "td_group_create: no peer access between the devices"));
+            cudaSetDevice(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(set_err(TD_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e)));
+            cudaGetLastError();
+        }
+    cudaSetDevice(g->dev[0]);
+    if (cudaEventCreateWithFlags(&g->entry, cudaEventDisableTiming) != cudaSuccess)
+        return fail(set_err(TD_ECUDA, "td_group_create: event"));
+    *out = g;
+    return TD_OK;
+}
+
+int td_group_destroy(td_group* g) {
+    if (!g) return TD_OK;
+    for (td_context* ctx : g->w) td_destroy(ctx);
+    if (g->entry) {
+        cudaSetDevice(g->dev[0]);
+        cudaEventDestroy(g->entry);
+    }
+    delete g;
+    return TD_OK;
+}
+
+int td_group_context(td_group* g, int worker, td_context** ctx) {
+    if (!g || !ctx || worker < 0 || worker >= int(g->w.size()))
+        return set_err(TD_EINVAL, "td_group_context: no such worker");
+    *ctx = g->w[size_t(worker)];
+    return TD_OK;
+}
+
+int td_group_p2p_open(td_group* g, int64_t max_rows, int64_t d) {
+    if (!g) return set_err(TD_EINVAL, "null td_group");
+    std::vector<void*> base;
+    for (td_context* ctx : g->w) {
+        if (int rc = require_ctx(ctx)) return rc;
+        if (int rc = xbuf_alloc(ctx, max_rows, d)) return rc;
+        base.push_back(ctx->xbuf.p);
+    }
+    for (td_context* ctx : g->w) {
+        if (int rc = require_ctx(ctx)) return rc;
+        TD_CUDA(ctx->x_ptrs.ensure(base.size() * sizeof(void*)));
+        TD_CUDA(cudaMemcpy(ctx->x_ptrs.p, base.data(), base.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        ctx->x_ready = true;
+    }
+    return TD_OK;
+}
+
+int td_group_tree_decode(td_group* g, const void* q, int64_t n_q, double scale, int strategy, float* out,
+                         int flags) {
+    if (!g) return set_err(TD_EINVAL, "null td_group");
+    if (flags & (TD_BF16_OUT | TD_TIME_PHASES | TD_DEBUG_TS))
+        return set_err(TD_EINVAL, "td_group_tree_decode: TD_BF16_OUT / TD_TIME_PHASES / TD_DEBUG_TS are per-context flags");
+    const int p = int(g->w.size());
+    const bool host = (flags & TD_HOST_IO) != 0;
+    td_context* c0 = g->w[0];
+    if (int rc = require_ctx(c0)) return rc;
+    // every worker's work is ordered after what the caller queued on worker 0's stream (a device q)
+    TD_CUDA(cudaEventRecord(g->entry, c0->stream));
+    for (int w = 1; w < p; ++w) {
+        if (int rc = require_ctx(g->w[size_t(w)])) return rc;
+        TD_CUDA(cudaStreamWaitEvent(g->w[size_t(w)]->stream, g->entry, 0));
+    }
+    if (p == 1) return td_tree_decode(c0, q, n_q, scale, strategy, out, flags);
+    // 1. plans (and a first long decode's calibration) for every worker before any
+    //    exchange is in flight; q onto every worker's device
+    std::vector<TreeCall> tc(static_cast<size_t>(p));
+    for (int w = 0; w < p; ++w) {
+        td_context* ctx = g->w[size_t(w)];
+        const void* qd = nullptr;
+        if (!host) {
+            if (g->dev[size_t(w)] == g->dev[0]) {
+                qd = q;
+            } else {
+                if (int rc = require_ctx(ctx)) return rc;
+                if (!ctx->kv_ok) return set_err(TD_ESTATE, "tree_decode: no KV shard placed");
+                const size_t bytes = size_t(ctx->b) * size_t(n_q) * size_t(ctx->d) * td::dtype_bytes(ctx->dtype);
+                TD_CUDA(ctx->q_dev.ensure(bytes));
+                TD_CUDA(cudaMemcpyPeerAsync(ctx->q_dev.p, g->dev[size_t(w)], q, g->dev[0], bytes, ctx->stream));
+                qd = ctx->q_dev.p;
+            }
+        }
+        if (int rc = tree_begin(ctx, q, n_q, strategy, flags, tc[size_t(w)], qd)) return rc;
+        if (ctx->b != c0->b || ctx->n_kv != c0->n_kv || ctx->d != c0->d || ctx->seq_len != c0->seq_len)
+            return set_err(TD_EINVAL, "tree_decode: the workers' shards are not one cache");
+    }
+    // 2. K1 + K2x on every worker, back to back; worker 0 writes the caller's output
+    float* dst0 = out;
+    if (host) {
+        require_ctx(c0);
+        float* m = mapped_host(c0, out);
+        dst0 = m ? m : c0->out;
+    }
+    for (int w = 0; w < p; ++w) {
+        td_context* ctx = g->w[size_t(w)];
+        require_ctx(ctx);
+        if (int rc = launch_tree_p2p(ctx, tc[size_t(w)], scale, w == 0 ? dst0 : ctx->out, flags)) return rc;
+        if (int rc = note_table_use(ctx)) return rc;
+    }
+    if (!host) return TD_OK;
+    require_ctx(c0);
+    if (dst0 != c0->mapped_dev || c0->mapped_for != out)
+        TD_CUDA(cudaMemcpyAsync(out, dst0, size_t(tc[0].rows) * size_t(c0->d) * sizeof(float), cudaMemcpyDeviceToHost,
+                                c0->stream));
+    int rc = TD_OK;
+    for (int w = 0; w < p; ++w) {  // every worker's step is over: report any exchange timeout
+        td_context* ctx = g->w[size_t(w)];
+        require_ctx(ctx);
+        TD_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (int e = exchange_failed(ctx)) rc = e;
+    }
+    return rc;
 }
 
 }  // extern "C"

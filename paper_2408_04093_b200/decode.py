@@ -502,6 +502,76 @@ def decode_tolerance_abs(dtype: DType, ref_max_abs: float) -> float:  # decode.c
     return 1e-10
 
 
+# ---------------------------------------------------------------- p workers in one process
+class WorkerGroup:
+    """The reference's p in-process workers (decode.hpp:70-72; one thread per
+    worker under parallel_workers, decode.cpp:37-41) in ONE process: worker w is
+    a Worker on device devices[w * len(devices) // p] (contiguous placement,
+    cluster.hpp:18-24), several workers may share a GPU. Place shards through
+    ``group.workers[w]`` (generate_kv / place_kv), call ``enable_p2p`` once, then
+    ``tree_decode`` runs K1 + the one-shot exchange combine (K2x) on every
+    worker, the peers' exchange buffers addressed as plain device pointers."""
+
+    def __init__(self, workers: int, devices=None):
+        import ctypes
+        torch = _torch()
+        if devices is None:
+            devices = list(range(max(1, min(workers, torch.cuda.device_count()))))
+        arr = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        check(lib().td_group_create(len(devices), arr, workers, ctypes.byref(h)))
+        self.h = h
+        self.devices = list(devices)
+        self.workers = []
+        for w in range(workers):
+            c = ctypes.c_void_p()
+            check(lib().td_group_context(h, w, ctypes.byref(c)))
+            self.workers.append(Worker._from_group(c, devices[w * len(devices) // workers]))
+
+    def enable_p2p(self, max_rows: int, d: int):
+        check(lib().td_group_p2p_open(self.h, max_rows, d))
+
+    def tree_decode(self, q, scale: float = 1.0, strategy: ReduceStrategy = ReduceStrategy.Hierarchical,
+                    out=None, flags: int = 0):
+        """Algorithm 3 over the group's workers (decode.cpp:100-184) with the
+        one-shot combine; q and out on the host or on worker 0's device."""
+        torch = _torch()
+        w0 = self.workers[0]
+        q = q.reshape(q.shape[0], q.shape[1], q.shape[-1]).contiguous()
+        host = not q.is_cuda
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device="cpu" if host else q.device, pin_memory=host)
+        if host:
+            flags |= _capi.TD_HOST_IO
+        w0._sync_in(q)
+        check(lib().td_group_tree_decode(self.h, q.data_ptr(), q.shape[1], float(scale), int(strategy),
+                                         out.data_ptr(), flags))
+        if not host:
+            w0._sync_worker()
+            for w in self.workers[1:]:
+                w._sync_worker()
+            if any(w.p2p_status() for w in self.workers):
+                raise _capi.TreeDecError(_capi.TD_ECUDA, "tree_decode: exchange timed out; call enable_p2p again")
+        return out
+
+    def tree_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0,
+                          strategy: int = 2):
+        check(lib().td_group_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags))
+
+    def close(self):
+        if getattr(self, "h", None):
+            for w in self.workers:
+                w.h = None
+            lib().td_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ---------------------------------------------------------------- one rank of the multi-GPU path
 class Worker:
     """One GPU (one process) holding one contiguous KV shard.
@@ -516,6 +586,7 @@ class Worker:
         h = ctypes.c_void_p()
         check(lib().td_create(device, ctypes.byref(h)))
         self.h = h
+        self._owned = True  # False: a worker of a WorkerGroup (the group destroys it)
         self.device = device
         self._pending = []  # device tensors an enqueued td_kv_append still reads
         self._xs = None     # torch handle of the worker's stream (created on first use)
@@ -561,9 +632,26 @@ class Worker:
         check(lib().td_p2p_status(self.h, self._ct.byref(e)))
         return e.value
 
+    @classmethod
+    def _from_group(cls, handle, device: int):
+        import ctypes
+        w = cls.__new__(cls)
+        w._ct = ctypes
+        w.h = handle
+        w._owned = False
+        w.device = device
+        w._pending, w._xs, w._ev = [], None, None
+        n, r = ctypes.c_int(), ctypes.c_int()
+        check(lib().td_comm_info(handle, ctypes.byref(n), ctypes.byref(r)))
+        w.nranks, w.rank = n.value, r.value
+        w.n_kv = w.d = w.b = w.seq_len = None
+        w.dtype = None
+        return w
+
     def close(self):
         if getattr(self, "h", None):
-            lib().td_destroy(self.h)  # synchronizes the worker's streams
+            if getattr(self, "_owned", True):
+                lib().td_destroy(self.h)  # synchronizes the worker's streams
             self.h = None
         self._pending = []
         self._xs = None

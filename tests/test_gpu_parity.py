@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from conftest import make_inputs, rel_err
+from oracle.full import full_decode, rel_err_rows
 from oracle.oracle import BF16, F32, F64, HIER
 
 pytestmark = pytest.mark.gpu
@@ -252,12 +253,8 @@ def test_worker_generate_and_decode(td, oracle, dtype, n_q, n_kv, n):
     w.generate_kv(td.DType(dtype), 1, n_kv, n, 128, oracle.mix64(seed, 2), oracle.mix64(seed, 3))
     q = oracle.seeded(oracle.mix64(seed, 1), n_q * 128, dtype).reshape(1, n_q, 128)
     out = w.tree_decode(dev(q, dtype))
-    # oracle on the first kv head's query group only (bounded CPU work)
-    g = n_q // n_kv
-    k0 = oracle.seeded(oracle.mix64(seed, 2), n * 128, dtype).reshape(1, 1, n, 128)
-    v0 = oracle.seeded(oracle.mix64(seed, 3), n * 128, dtype).reshape(1, 1, n, 128)
-    want = oracle.tree_decode(np.ascontiguousarray(q[:, :g]), k0, v0, 1, HIER, 1.0, F64, nthreads=8)
-    assert rel_err(host(out[:, :g]), want) <= TOL[dtype]
+    want = full_decode(oracle, q, n_kv, n, oracle.mix64(seed, 2), oracle.mix64(seed, 3), dtype)  # every row
+    assert rel_err_rows(host(out), want) <= TOL[dtype]
     # host buffers through the same call (the e2e path)
     out_h = w.tree_decode(torch.from_numpy(np.ascontiguousarray(q)).to(dev(q, dtype).dtype))
     assert rel_err(out_h.double().numpy(), host(out)) <= 5e-6  # default mode: ~1e-7..1e-6 between calls
@@ -366,13 +363,10 @@ def test_long_shard_default_path(td, oracle):
     w.generate_kv(td.DType(BF16), 1, n_kv, n, 128, oracle.mix64(seed, 2), oracle.mix64(seed, 3))
     q = oracle.seeded(oracle.mix64(seed, 1), n_q * 128, BF16).reshape(1, n_q, 128)
     outs = [w.tree_decode(dev(q, BF16)) for _ in range(3)]
-    g = n_q // n_kv
-    k0 = oracle.seeded(oracle.mix64(seed, 2), n * 128, BF16).reshape(1, 1, n, 128)
-    v0 = oracle.seeded(oracle.mix64(seed, 3), n * 128, BF16).reshape(1, 1, n, 128)
-    want = oracle.tree_decode(np.ascontiguousarray(q[:, :g]), k0, v0, 1, HIER, 1.0, F64, nthreads=16)
-    for o in outs:
-        assert rel_err(host(o[:, :g]), want) <= TOL[BF16]
     w.close()
+    want = full_decode(oracle, q, n_kv, n, oracle.mix64(seed, 2), oracle.mix64(seed, 3), BF16)  # every row
+    for o in outs:
+        assert rel_err_rows(host(o), want) <= TOL[BF16]
 
 
 def test_cross_row_stealing_parity(lib):
