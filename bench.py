@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-compare", action="store_true",
                     help="N > 1: skip the ring pass-KV and paper-literal NCCL comparison records")
     ap.add_argument("--compare-steps", type=int, default=10)
+    ap.add_argument("--deterministic", action="store_true",
+                    help="static split only (bitwise-reproducible results, td_set_deterministic)")
     return ap.parse_args()
 
 
@@ -244,7 +246,8 @@ def bench_config(args, wl, world, combine, flush):
             "nccl_algo": os.environ.get("NCCL_ALGO", "auto") if world > 1 else None,
             "l2": "flushed between steps (read-only sweep of 256 MB, timed apart and subtracted)" if flush
             else "inputs larger than L2 (KV shard > 4x126 MB)",
-            "parallelism": f"sp{world} (sequence-sharded KV)"}
+            "parallelism": f"sp{world} (sequence-sharded KV)",
+            "deterministic": bool(getattr(args, "deterministic", False))}
 
 
 def parity_leg(args, wl, q_dev, out_dev, world):
@@ -374,6 +377,8 @@ def main():
         return z ^ (z >> 31)
 
     seed = mix64(0, n)
+    if args.deterministic:
+        td.set_deterministic(True)
     w = td.Worker.from_torch_distributed(local) if world > 1 else td.Worker(local)
     w.generate_kv(dtype, b, n_kv, n, d, mix64(seed, 2), mix64(seed, 3))
     start, shard_len, shard_bytes = w.kv_info()
@@ -385,7 +390,7 @@ def main():
     # L2 flush by a read-only sweep of 256 MB (> 2 x L2): it leaves clean lines, so
     # the decode that follows pays no write-back of a flush's dirty lines
     scratch = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda") if flush else None
-    flush_sink = torch.empty(1, dtype=torch.float32, device="cuda") if flush else None
+    flush_sink = torch.empty((), dtype=torch.float32, device="cuda") if flush else None
 
     def flush_l2():
         torch.sum(scratch, dim=0, out=flush_sink)
@@ -470,7 +475,7 @@ def main():
                 flush_l2()
             stream.synchronize()
         t0 = time.perf_counter()
-        decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO | base_flags)
+        decode(q_host.data_ptr(), n_q, out_host.data_ptr(), args.scale, _capi.TD_HOST_IO | _capi.TD_PINNED_IO | base_flags)
         e2e_times.append(time.perf_counter() - t0)
     e2e_ms = max_over_ranks(1000.0 * sum(e2e_times) / len(e2e_times), world)
     # same result through the host path; the dynamic tile pool regroups the

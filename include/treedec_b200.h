@@ -61,10 +61,16 @@ enum {
     TD_P2P = 16,         /* tree decode: one-shot NVLink exchange instead of the
                             two NCCL allreduces (needs td_p2p_open)              */
     TD_DEBUG_TS = 32,    /* kernels record %globaltimer stamps (td_debug_stamps) */
-    TD_DETERMINISTIC = 64 /* static split only: bitwise-reproducible results (the
-                             default also hands the last ~15% of each (batch,
-                             kv-head) row out dynamically; results then agree to
-                             ~1e-7 between calls, the grouping of tiles varies) */
+    TD_DETERMINISTIC = 64, /* static split only: bitwise-reproducible results (the
+                              default also hands the last ~15% of each (batch,
+                              kv-head) row out dynamically; results then agree to
+                              ~1e-7 between calls, the grouping of tiles varies) */
+    TD_PINNED_IO = 128    /* with TD_HOST_IO: out is a pinned host buffer (cudaHostAlloc
+                             / cudaHostRegister). The combine kernel writes it in place
+                             and signals completion through pinned host memory; the
+                             call returns when the host sees that signal (no stream
+                             synchronisation). Ignored where it cannot apply (the
+                             NCCL path, TD_BF16_OUT). */
 };
 
 typedef struct td_context td_context;

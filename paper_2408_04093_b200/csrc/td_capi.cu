@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -64,6 +65,13 @@ struct NcclApi {
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     ncclResult_t (*GetVersion)(int*) = nullptr;
+    // symmetric memory (NCCL >= 2.27, optional): registered windows let NCCL run its
+    // low-latency symmetric kernels for the two small allreduces
+    ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+    ncclResult_t (*MemFree)(void*) = nullptr;
+    ncclResult_t (*WindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+    ncclResult_t (*WindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+    bool symmetric() const { return MemAlloc && MemFree && WindowRegister && WindowDeregister; }
 };
 
 NcclApi& nccl() {
@@ -91,6 +99,13 @@ NcclApi& nccl() {
         sym(a.GetErrorString, "ncclGetErrorString");
         sym(a.GetVersion, "ncclGetVersion");
         a.ok = all;
+        auto opt = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+        };
+        opt(a.MemAlloc, "ncclMemAlloc");
+        opt(a.MemFree, "ncclMemFree");
+        opt(a.WindowRegister, "ncclCommWindowRegister");
+        opt(a.WindowDeregister, "ncclCommWindowDeregister");
         if (!all) a.err = "libnccl.so.2 lacks a required symbol";
         return a;
     }();
@@ -192,6 +207,13 @@ struct td_context {
     unsigned long long* cur_tl_cta = nullptr;
     bool shared_device = false;       // another context of this process runs on the same GPU (td_group)
 
+    // TD_PINNED_IO fast path: the K2 warp counter (device) and the completion
+    // word (mapped pinned host memory)
+    DevBuf sig;
+    unsigned* done_host = nullptr;
+    unsigned done_epoch = 0;
+    int host_ptr_ok = -1;             // pinned host pointers usable by kernels as is (UVA), probed once
+
     DevBuf dbg;  // TD_DEBUG_TS stamps
     int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
     float* mapped_for = nullptr;   // this call's host output buffer and its device alias (or null)
@@ -220,6 +242,13 @@ struct td_context {
     unsigned tabs_touched = 0;        // entries selected since the last note_table_use
 
     bool det = false;  // this call: static split only (TD_DETERMINISTIC)
+    // paper-literal NCCL combine: [lse | shift | n, d] of the step in one
+    // ncclMemAlloc block registered as a symmetric window (collective, once per size)
+    void* win_buf = nullptr;
+    size_t win_bytes = 0;
+    ncclWindow_t win = nullptr;
+    int win_state = 0;  // 0 untried, 1 registered, -1 unavailable (plain buffers)
+
     DevBuf ctr;        // K1 dynamic-pool counters (SplitPlan::counters)
     int64_t ctr_bh = -1;
     int kpar = 0;      // parity of the next launch
@@ -531,10 +560,16 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
             ctx->kpar = 0;
         }
         plan.counters = static_cast<unsigned*>(ctx->ctr.p);
-        plan.parity = ctx->kpar;
-        ctx->kpar ^= 1;
+        plan.parity = ctx->kpar;  // advanced by launched() once the launch is in
     }
     return TD_OK;
+}
+
+// After a K1 launch of `plan` on the context's own counters: the next launch uses
+// the other parity (the one this launch's K2 zeroes). A call that fails before
+// launching leaves the parity alone, so the counters at rest stay zero.
+void launched(td_context* ctx, const SplitPlan& plan) {
+    if (plan.pool_tiles > 0 && plan.counters == ctx->ctr.p) ctx->kpar = plan.parity ^ 1;
 }
 
 void phase_begin(td_context* ctx, int flags) {
@@ -594,6 +629,7 @@ int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const voi
     }
     TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
                                       ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
+    launched(ctx, plan);
     if (kb == ctx->k.p && plan.row_stride > 0) ctx->kv_safe = t;  // later K1s run after this one's wait
     ctx->last_kernels += 2;  // K1 + K2
     ctx->last_kv_bytes += 2.0 * double(ctx->b) * double(ctx->n_kv) * double(t) * double(ctx->d) *
@@ -607,8 +643,7 @@ const void* stage_q(td_context* ctx, const void* q, int64_t n_q, int flags, int*
     if (!(flags & TD_HOST_IO)) return q;
     const size_t bytes = size_t(ctx->b) * size_t(n_q) * size_t(ctx->d) * td::dtype_bytes(ctx->dtype);
     cudaError_t e = ctx->q_dev.ensure(bytes);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(ctx->q_dev.p, q, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->q_dev.p, q, bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) {
         *rc = set_err(TD_ECUDA, std::string("q upload: ") + cudaGetErrorString(e));
         return nullptr;
@@ -640,6 +675,36 @@ int exchange_failed(td_context* ctx) {
     ctx->x_ready = false;
     return set_err(TD_ECUDA, "tree_decode: NVLink exchange timed out (a peer never delivered its partial); "
                              "re-open the exchange with td_p2p_handle / td_p2p_open");
+}
+
+// The NCCL combine's buffers [lse rows | shift rows | n rows*d, d rows] inside a
+// symmetric window (every rank reaches this with the same shape: the decode is
+// collective). Returns null when symmetric memory is unavailable or switched off
+// (TD_NCCL_SYMMETRIC=0): the plain per-row buffers are used then.
+float* nccl_window(td_context* ctx, int64_t rows, int64_t d) {
+    static const bool on = [] { const char* e = std::getenv("TD_NCCL_SYMMETRIC"); return !e || std::atoi(e) != 0; }();
+    if (!on || !ctx->comm || !nccl().symmetric() || ctx->win_state < 0) return nullptr;
+    auto pad = [](size_t n) { return (n + 63) / 64 * 64; };
+    const size_t need = (2 * pad(size_t(rows)) + pad(size_t(rows) * size_t(d + 1))) * sizeof(float);
+    if (ctx->win_state == 1 && need <= ctx->win_bytes) return static_cast<float*>(ctx->win_buf);
+    if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
+    if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
+    ctx->win = nullptr;
+    ctx->win_buf = nullptr;
+    ctx->win_bytes = 0;
+    const size_t bytes = (need + 4095) / 4096 * 4096;
+    if (nccl().MemAlloc(&ctx->win_buf, bytes) != ncclSuccess ||
+        nccl().WindowRegister(ctx->comm, ctx->win_buf, bytes, &ctx->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+        if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
+        ctx->win_buf = nullptr;
+        ctx->win = nullptr;
+        ctx->win_state = -1;
+        cudaGetLastError();
+        return nullptr;
+    }
+    ctx->win_bytes = bytes;
+    ctx->win_state = 1;
+    return static_cast<float*>(ctx->win_buf);
 }
 
 int deliver_out(td_context* ctx, const float* src, int64_t rows, float* out, int flags) {
@@ -841,6 +906,8 @@ int td_destroy(td_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->xfer);
+    if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
+    if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     ctx->k.release();
     ctx->v.release();
@@ -860,6 +927,8 @@ int td_destroy(td_context* ctx) {
     ctx->xbuf.release();
     ctx->x_ptrs.release();
     if (ctx->x_err) cudaFreeHost(ctx->x_err);
+    if (ctx->done_host) cudaFreeHost(ctx->done_host);
+    ctx->sig.release();
     ctx->ctr.release();
     ctx->dbg.release();
     ctx->tlbuf.release();
@@ -895,6 +964,12 @@ int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[1
     if (int rc = require_ctx(ctx)) return rc;
     if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(TD_EINVAL, "td_comm_init: bad rank");
     if (ctx->comm) {
+        if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
+        if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
+        ctx->win = nullptr;
+        ctx->win_buf = nullptr;
+        ctx->win_bytes = 0;
+        ctx->win_state = 0;
         nccl().CommDestroy(ctx->comm);
         ctx->comm = nullptr;
     }
@@ -1217,7 +1292,63 @@ struct TreeCall {
     SplitPlan plan;
     const void* qd = nullptr;
     int64_t rows = 0;
+    bool fast = false;  // TD_PINNED_IO fast path taken (tree_begin)
 };
+
+// TD_PINNED_IO with TD_HOST_IO: out is a pinned host buffer the combine kernel
+// writes in place (with UVA a pinned buffer's device address is its host
+// address) and then signals through pinned host memory. Taken when the last
+// kernel of the step is a signalling K2 / K2x (not the NCCL path's K4) and the
+// output needs no bf16 copy.
+bool pinned_fast_path(td_context* ctx, int flags, const SplitPlan& plan) {
+    static const bool on = [] { const char* e = std::getenv("TD_PINNED_FAST"); return !e || std::atoi(e) != 0; }();
+    if (!on || (flags & (TD_HOST_IO | TD_PINNED_IO)) != (TD_HOST_IO | TD_PINNED_IO) ||
+        (flags & (TD_BF16_OUT | TD_DEBUG_TS)))
+        return false;
+    if (flags & TD_TIME_PHASES) return false;
+    (void)plan;
+    if (ctx->nranks > 1 && !(flags & TD_P2P)) return false;  // the NCCL path ends in K4, not in a signalling K2
+    if (ctx->host_ptr_ok < 0) {
+        int uva = 0, reg = 0;
+        cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, ctx->device);
+        cudaDeviceGetAttribute(&reg, cudaDevAttrCanUseHostPointerForRegisteredMem, ctx->device);
+        ctx->host_ptr_ok = uva && reg;
+    }
+    return ctx->host_ptr_ok == 1;
+}
+
+int ensure_signals(td_context* ctx) {
+    if (!ctx->sig.p) {
+        TD_CUDA(ctx->sig.ensure(sizeof(unsigned)));
+        TD_CUDA(cudaMemset(ctx->sig.p, 0, sizeof(unsigned)));
+    }
+    if (!ctx->done_host) {
+        void* h = nullptr;
+        TD_CUDA(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(h, 0, 64);
+        ctx->done_host = static_cast<unsigned*>(h);
+    }
+    return TD_OK;
+}
+
+// Waits for the combine kernel's completion word (a spin on pinned host memory
+// the GPU writes over PCIe: no stream synchronisation on the step). The stream
+// is queried now and then so a failed launch surfaces as an error.
+int wait_done(td_context* ctx, unsigned epoch) {
+    static const bool spin = [] { const char* e = std::getenv("TD_PINNED_SPIN"); return !e || std::atoi(e) != 0; }();
+    if (!spin) TD_CUDA(cudaStreamSynchronize(ctx->stream));  // A/B switch: the runtime's wait instead
+    volatile unsigned* f = ctx->done_host;
+    for (unsigned spins = 1; *f != epoch; ++spins) {
+        if ((spins & 1023u) == 0) {
+            const cudaError_t e = cudaStreamQuery(ctx->stream);
+            if (e == cudaSuccess && *f != epoch)
+                return set_err(TD_ECUDA, "tree_decode: the combine kernel finished without its completion word");
+            if (e != cudaSuccess && e != cudaErrorNotReady)
+                return set_err(TD_ECUDA, std::string("tree_decode: ") + cudaGetErrorString(e));
+        }
+    }
+    return TD_OK;
+}
 
 int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int flags, TreeCall& tc,
                const void* q_on_device = nullptr) {
@@ -1234,6 +1365,16 @@ int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int fl
     if (int rc = ensure_rows(ctx, tc.rows, ctx->d)) return rc;
     if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap)) return rc;
     int rc = TD_OK;
+    if (!q_on_device && pinned_fast_path(ctx, flags, tc.plan)) {
+        // the output goes straight into the caller's pinned buffer and the combine
+        // kernel signals completion through pinned host memory (no stream sync)
+        SplitPlan& pl = tc.plan;
+        if (int rc2 = ensure_signals(ctx)) return rc2;
+        pl.done_ctr = static_cast<unsigned*>(ctx->sig.p);
+        pl.done_flag = ctx->done_host;
+        pl.done_epoch = ++ctx->done_epoch == 0 ? ++ctx->done_epoch : ctx->done_epoch;
+        tc.fast = true;
+    }
     tc.qd = q_on_device ? q_on_device : stage_q(ctx, q, n_q, flags, &rc);
     if (rc) return rc;
     phase_begin(ctx, flags);
@@ -1272,6 +1413,7 @@ int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xd
     }
     TD_CUDA(td::launch_decode_exchange(plan, tc.qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                        ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
+    launched(ctx, plan);
     ctx->x_epoch = xa.epoch;
     ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
     phase_mark(ctx);
@@ -1297,19 +1439,24 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     int rc = TD_OK;
     if ((flags & TD_P2P) && ctx->nranks > 1) {
         float* xdst = out;
-        if (flags & TD_HOST_IO) {
+        if ((flags & TD_HOST_IO) && !tc.fast) {
             float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
             xdst = m ? m : ctx->out;
         }
         if (int rc2 = launch_tree_p2p(ctx, tc, scale, xdst, flags)) return rc2;
-        if (int rc2 = deliver_out(ctx, xdst, rows, out, flags)) return rc2;
+        if (tc.fast) {
+            if (int rc2 = note_table_use(ctx)) return rc2;
+            if (int rc2 = wait_done(ctx, plan.done_epoch)) return rc2;
+        } else if (int rc2 = deliver_out(ctx, xdst, rows, out, flags)) {
+            return rc2;
+        }
         return (flags & TD_HOST_IO) ? exchange_failed(ctx) : TD_OK;  // synchronised: this step's verdict
     }
     if (ctx->nranks == 1) {
         // p = 1: the shard partial is the result (shift = lse, w = 1): one kernel,
         // written straight into the caller's buffer when it is on the device
         float* dst = out;
-        if (flags & TD_HOST_IO) {
+        if ((flags & TD_HOST_IO) && !tc.fast) {
             float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
             dst = m ? m : ctx->out;
         }
@@ -1325,37 +1472,46 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         if (dbg) TD_CUDA(td::launch_stamp(dbg + 2, ctx->stream));
         TD_CUDA(td::launch_decode_final(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
                                         ctx->ws.p, dst, ctx->stream, e0, e1));
+        launched(ctx, plan);
         if (dbg) TD_CUDA(td::launch_stamp(dbg + 3, ctx->stream));
         phase_mark(ctx);
         ctx->last_kernels = 2;  // K1 + K2
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
                              td::dtype_bytes(ctx->dtype);
         ctx->last_split_kernel = plan.kernel;
-        return deliver_out(ctx, dst, rows, out, flags);
+        if (!tc.fast) return deliver_out(ctx, dst, rows, out, flags);
+        if (int rc2 = note_table_use(ctx)) return rc2;
+        return wait_done(ctx, plan.done_epoch);
+    }
+    // the allreduced buffers: in a symmetric NCCL window when available
+    float *lse = ctx->lse, *shift = ctx->shift, *nd = ctx->nd;
+    if (ctx->nranks > 1) {
+        if (float* w = nccl_window(ctx, rows, d)) {
+            const int64_t pr = (rows + 63) / 64 * 64;
+            lse = w;
+            shift = w + pr;
+            nd = w + 2 * pr;
+        }
     }
     // 1. local partial (out, lse) of this shard
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
-                          ctx->row_max, ctx->lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0,
+                          ctx->row_max, lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0,
                           ctx->cur_phase ? ctx : nullptr)))
         return rc;
     phase_mark(ctx);
     const float* result = ctx->out_local;
     if (ctx->nranks > 1) {
         // 2. allreduce(max) over lse -> common shift (decode.cpp:129-139)
-        TD_NCCL(nccl().AllReduce(ctx->lse, ctx->shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm,
-                              ctx->stream));
+        TD_NCCL(nccl().AllReduce(lse, shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm, ctx->stream));
         phase_mark(ctx);
         // 3. n = o e^(lse-m), d = e^(lse-m) (decode.cpp:150-153)
-        TD_CUDA(td::launch_to_numerator(ctx->lse, ctx->out_local, ctx->shift, rows,
-                                        static_cast<int>(d), ctx->nd, ctx->stream));
+        TD_CUDA(td::launch_to_numerator(lse, ctx->out_local, shift, rows, static_cast<int>(d), nd, ctx->stream));
         phase_mark(ctx);
         // 4. one fused sum-allreduce over [n|d] (decode.cpp:154-160); fp32 wire
-        TD_NCCL(nccl().AllReduce(ctx->nd, ctx->nd, size_t(rows * d + rows), ncclFloat32, ncclSum,
-                              ctx->comm, ctx->stream));
+        TD_NCCL(nccl().AllReduce(nd, nd, size_t(rows * d + rows), ncclFloat32, ncclSum, ctx->comm, ctx->stream));
         phase_mark(ctx);
         // 5. out = n / d (decode.cpp:165-173)
-        TD_CUDA(td::launch_finalize(ctx->nd, rows, static_cast<int>(d), ctx->out, nullptr,
-                                    ctx->stream));
+        TD_CUDA(td::launch_finalize(nd, rows, static_cast<int>(d), ctx->out, nullptr, ctx->stream));
         phase_mark(ctx);
         ctx->last_kernels += 2;
         result = ctx->out;
@@ -1734,6 +1890,7 @@ int td_group_tree_decode(td_group* g, const void* q, int64_t n_q, double scale, 
     if (!g) return set_err(TD_EINVAL, "null td_group");
     if (flags & (TD_BF16_OUT | TD_TIME_PHASES | TD_DEBUG_TS))
         return set_err(TD_EINVAL, "td_group_tree_decode: TD_BF16_OUT / TD_TIME_PHASES / TD_DEBUG_TS are per-context flags");
+    flags &= ~TD_PINNED_IO;  // the group stages q and collects the output itself
     const int p = int(g->w.size());
     const bool host = (flags & TD_HOST_IO) != 0;
     td_context* c0 = g->w[0];

@@ -69,6 +69,11 @@ struct SplitPlan {
     unsigned long long* dbg = nullptr;
     unsigned long long* tl = nullptr;
     unsigned long long* tl_cta = nullptr;
+    // TD_PINNED_IO: the combine kernel's last warp stores done_epoch into the
+    // mapped host word done_flag (done_ctr counts its warps), which the caller polls
+    unsigned* done_ctr = nullptr;
+    unsigned* done_flag = nullptr;
+    unsigned done_epoch = 0;
     // launch K1 as a programmatic dependent of the preceding kernel (off when several
     // contexts share one GPU and a peer's K1 must get SMs while this one's exchange waits)
     bool pdl = true;

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -106,6 +107,10 @@ struct K1Args {
     unsigned* claims;
     unsigned epoch;
     int early_trigger;        // debug: PDL trigger at K1 entry instead of after the main loop
+    // TD_PINNED_IO (SplitPlan): completion signalled to the host by K2's last warp
+    unsigned* done_ctr;
+    unsigned* done_flag;
+    unsigned done_epoch;
     Tail tail;
 };
 
@@ -121,6 +126,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ int64_t div_nn(int64_t n, int64_t d) {
     if (((n | d) >> 32) == 0) return static_cast<int64_t>(static_cast<uint32_t>(n) / static_cast<uint32_t>(d));
     return n / d;
+}
+
+// TD_PINNED_IO: after a K2 warp's last output store (to mapped host memory),
+// count the warp; the grid's last warp stores the step's epoch into the mapped
+// host word the caller polls. Each warp releases its stores at gpu scope before
+// it counts (the threadfence-reduction pattern); the last warp, having
+// observed every count, fences at system scope once before the flag, which by
+// cumulativity orders every warp's output before the flag for the host.
+__device__ __forceinline__ void signal_done(const K1Args& a) {
+    if (!a.done_flag) return;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence();
+        const unsigned warps = gridDim.x * (blockDim.x >> 5);
+        if (atomicAdd(a.done_ctr, 1u) == warps - 1) {
+            *a.done_ctr = 0u;  // the next launch is stream-ordered after this one
+            __threadfence_system();
+            st_release_sys(a.done_flag, a.done_epoch);
+        }
+    }
 }
 
 __device__ __forceinline__ int64_t cta_begin(int64_t total, int c, int ctas) {
@@ -499,7 +524,6 @@ __global__ void __launch_bounds__(W * 32, 1)
         atomicMin(a.tl + 0, t_start);
         atomicMin(a.tl + 1, t_go);
     }
-    for (int s = pre; s < S; ++s) refill(s);
 
     const int hA = 2 * (lane & 3), hB = hA + 1;  // this lane's heads (N columns)
     const int eta = lane >> 2;                   // B-fragment head / C-fragment row
@@ -510,11 +534,12 @@ __global__ void __launch_bounds__(W * 32, 1)
     float o[MD][4];
     float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
     uint32_t qf[KS][2];
-    int64_t cur_bh = -1;
+    int64_t cur_bh = -1, q_bh = -1;
     int cur_rec = -1;
     uint64_t flushed = 0;
 
     auto load_q = [&](int64_t bh) {
+        q_bh = bh;
         const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
         const bool ok = eta < a.group;
         const uint16_t* qrow = static_cast<const uint16_t*>(a.q) +
@@ -522,8 +547,8 @@ __global__ void __launch_bounds__(W * 32, 1)
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
             const int col = ks * 16 + 2 * (lane & 3);
-            qf[ks][0] = ok ? *reinterpret_cast<const uint32_t*>(qrow + col) : 0u;
-            qf[ks][1] = ok ? *reinterpret_cast<const uint32_t*>(qrow + col + 8) : 0u;
+            qf[ks][0] = ok ? __ldcg(reinterpret_cast<const unsigned*>(qrow + col)) : 0u;
+            qf[ks][1] = ok ? __ldcg(reinterpret_cast<const unsigned*>(qrow + col + 8)) : 0u;
         }
     };
     auto reset = [&]() {
@@ -574,6 +599,10 @@ __global__ void __launch_bounds__(W * 32, 1)
         }
     };
 
+    // the first static tile's q before the rest of the first tiles are requested:
+    // its load is then not queued behind this CTA's burst of TMA reads
+    if (x1 > x0 + warp) load_q((x0 + warp) / A);
+    for (int s = pre; s < S; ++s) refill(s);
     reset();
     for (int64_t kk = 0;; ++kk) {
         const int s = static_cast<int>(kk % S);
@@ -587,7 +616,7 @@ __global__ void __launch_bounds__(W * 32, 1)
                 flush(cur_bh, cur_rec);
                 reset();
             }
-            if (bh != cur_bh) load_q(bh);
+            if (bh != q_bh) load_q(bh);
             cur_bh = bh;
             cur_rec = rec;
         }
@@ -786,9 +815,6 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         bulk_load(kd, kg + row * D, bytes, &bars[warp][s], pol);
         bulk_load(kd + TILE_BYTES, vg + row * D, bytes, &bars[warp][s], pol);
     };
-    if (lane == 0)
-        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
-
     float qv[G][4], o[G][4], m[G], l[G];
     int64_t cur_bh = -1;
     uint32_t flushed = 0;
@@ -796,8 +822,8 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         const int64_t b = bh / a.n_kv, kvh = bh % a.n_kv;
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-            const float4 qq = reinterpret_cast<const float4*>(
-                static_cast<const float*>(a.q) + ((b * a.n_q) + kvh * G + h) * int64_t(D))[lane];
+            const float4 qq = __ldcg(reinterpret_cast<const float4*>(
+                static_cast<const float*>(a.q) + ((b * a.n_q) + kvh * G + h) * int64_t(D)) + lane);
             qv[h][0] = qq.x * a.scale_log2;
             qv[h][1] = qq.y * a.scale_log2;
             qv[h][2] = qq.z * a.scale_log2;
@@ -830,6 +856,14 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     };
 
     reset();
+    // the first tile's q before this warp's bulk copies: its load is then not
+    // queued behind the CTA's burst of KV reads (it misses L2 after a flush)
+    if (nmine > 0) {
+        cur_bh = (x0 + warp) / a.tiles_per_bh;
+        load_q(cur_bh);
+    }
+    if (lane == 0)
+        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
     for (int64_t kk = 0; kk < nmine; ++kk) {
         const int s = static_cast<int>(kk % S);
         const uint32_t phase = static_cast<uint32_t>((kk / S) & 1);
@@ -1318,6 +1352,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine(const K1Args a) {
     }
     if (ts) ts[4] = gtimer();
     if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
+    signal_done(a);
 }
 
 // K2 with each row split by columns over Q warps (d = 32 Q, one float per
@@ -1355,6 +1390,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
         }
     }
     if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
+    signal_done(a);
 }
 
 // =========================================================================
@@ -1548,6 +1584,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     }
     if (ts) ts[4] = gtimer();
     if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
+    signal_done(a);
 }
 
 // =========================================================================
@@ -1707,6 +1744,9 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.claims = p.claims;
     a.epoch = p.epoch;
     a.bh_table = p.bh_table;
+    a.done_ctr = p.done_ctr;
+    a.done_flag = p.done_flag;
+    a.done_epoch = p.done_epoch;
     if (p.pool_tiles > 0) {
         unsigned* cnt = p.counters;  // [2 parities][bh_count] pool, then [2][bh_count] foreign
         a.pool_ctr = cnt + p.parity * p.bh_count;

@@ -797,6 +797,8 @@ class Worker:
                                                    "on the same side (host / device) as q")
         if host:
             flags |= _capi.TD_HOST_IO
+            if out.is_pinned():
+                flags |= _capi.TD_PINNED_IO  # the combine kernel writes out in place and signals the host
         self._sync_in(q)
         rc = fn(self.h, q.data_ptr(), n_q, float(scale), *extra, out.data_ptr(), flags)
         check(rc)
