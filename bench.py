@@ -65,8 +65,8 @@ def parse():
     ap.add_argument("--no-compare", action="store_true",
                     help="N > 1: skip the ring pass-KV and paper-literal NCCL comparison records")
     ap.add_argument("--compare-steps", type=int, default=10)
-    ap.add_argument("--deterministic", action="store_true",
-                    help="static split only (bitwise-reproducible results, td_set_deterministic)")
+    ap.add_argument("--dynamic", action="store_true",
+                    help="dynamic tile pool (TD_DYNAMIC; the default static split is bitwise reproducible)")
     return ap.parse_args()
 
 
@@ -247,7 +247,7 @@ def bench_config(args, wl, world, combine, flush):
             "l2": "flushed between steps (read-only sweep of 256 MB, timed apart and subtracted)" if flush
             else "inputs larger than L2 (KV shard > 4x126 MB)",
             "parallelism": f"sp{world} (sequence-sharded KV)",
-            "deterministic": bool(getattr(args, "deterministic", False))}
+            "deterministic": not getattr(args, "dynamic", False)}
 
 
 def parity_leg(args, wl, q_dev, out_dev, world):
@@ -377,8 +377,8 @@ def main():
         return z ^ (z >> 31)
 
     seed = mix64(0, n)
-    if args.deterministic:
-        td.set_deterministic(True)
+    if args.dynamic:
+        td.set_deterministic(False)
     w = td.Worker.from_torch_distributed(local) if world > 1 else td.Worker(local)
     w.generate_kv(dtype, b, n_kv, n, d, mix64(seed, 2), mix64(seed, 3))
     start, shard_len, shard_bytes = w.kv_info()

@@ -61,16 +61,21 @@ enum {
     TD_P2P = 16,         /* tree decode: one-shot NVLink exchange instead of the
                             two NCCL allreduces (needs td_p2p_open)              */
     TD_DEBUG_TS = 32,    /* kernels record %globaltimer stamps (td_debug_stamps) */
-    TD_DETERMINISTIC = 64, /* static split only: bitwise-reproducible results (the
-                              default also hands the last ~15% of each (batch,
-                              kv-head) row out dynamically; results then agree to
-                              ~1e-7 between calls, the grouping of tiles varies) */
-    TD_PINNED_IO = 128    /* with TD_HOST_IO: out is a pinned host buffer (cudaHostAlloc
+    TD_DETERMINISTIC = 64, /* static split (the default, see td_set_deterministic):
+                              every CTA streams a fixed, calibrated range, so the
+                              grouping of the sums and the result are bitwise
+                              identical from call to call on a context */
+    TD_PINNED_IO = 128,   /* with TD_HOST_IO: out is a pinned host buffer (cudaHostAlloc
                              / cudaHostRegister). The combine kernel writes it in place
                              and signals completion through pinned host memory; the
                              call returns when the host sees that signal (no stream
                              synchronisation). Ignored where it cannot apply (the
                              NCCL path, TD_BF16_OUT). */
+    TD_DYNAMIC = 256      /* this call: hand the last ~15% of each (batch, kv-head)
+                             row out at run time to the SMs that stream fastest
+                             (and let idle warps take other rows' chunks on long
+                             shards). Up to ~2.5% faster on some shapes; results
+                             then agree to ~1e-7, not bitwise, between calls. */
 };
 
 typedef struct td_context td_context;
@@ -89,9 +94,10 @@ const char* td_last_error(void);
 int td_seeded_fill(int dtype, void* dst, uint64_t seed, double scale, int64_t bh_count,
                    int64_t seq, int64_t start, int64_t len, int64_t d, void* stream);
 
-/* Process-wide TD_DETERMINISTIC for every call (including the stateless
- * td_decode_partial): bitwise-reproducible results, the reference's
- * determinism property (test_decode.cpp:185-202). */
+/* Process-wide default of every call (including the stateless
+ * td_decode_partial): on (1, the default) = the static split, bitwise-
+ * reproducible results like the reference's (test_decode.cpp:185-202);
+ * off (0) = the dynamic pool of TD_DYNAMIC for every call. */
 int td_set_deterministic(int on);
 
 /* Workspace bytes td_decode_partial needs for this shard shape. */

@@ -26,7 +26,16 @@ using td::SplitPlan;
 namespace {
 
 thread_local std::string g_err;
-int g_deterministic = 0;  // td_set_deterministic
+int g_deterministic = 1;  // td_set_deterministic: static split by default (bitwise reproducible)
+
+// Static split (bitwise reproducible) unless the call or the process asks for the
+// dynamic pool: TD_DETERMINISTIC forces it on, TD_DYNAMIC off, else the
+// process setting (td_set_deterministic, on by default).
+bool call_deterministic(int flags) {
+    if (flags & TD_DETERMINISTIC) return true;
+    if (flags & TD_DYNAMIC) return false;
+    return g_deterministic != 0;
+}
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -1353,7 +1362,7 @@ int wait_done(td_context* ctx, unsigned epoch) {
 int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int flags, TreeCall& tc,
                const void* q_on_device = nullptr) {
     if (int rc = require_ctx(ctx)) return rc;
-    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
+    ctx->det = call_deterministic(flags);
     if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "tree_decode: no KV shard placed");
     if (strategy < 0 || strategy > 2) return set_err(TD_EINVAL, "tree_decode: unknown strategy");
@@ -1522,7 +1531,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
 int td_local_partial(td_context* ctx, const void* q, int64_t n_q, double scale, float* row_max,
                      float* lse, float* out, int flags) {
     if (int rc = require_ctx(ctx)) return rc;
-    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
+    ctx->det = call_deterministic(flags);
     if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "local_partial: no KV shard placed");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "local_partial: q/kv head mismatch");
@@ -1612,7 +1621,7 @@ int td_energy_grad(td_context* ctx, const void* q, int64_t nq, const float* row_
 int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, float* out,
                    int flags) {
     if (int rc = require_ctx(ctx)) return rc;
-    ctx->det = (flags & TD_DETERMINISTIC) != 0 || g_deterministic != 0;
+    ctx->det = call_deterministic(flags);
     if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "ring_decode: no KV shard placed");
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "ring_decode: more workers than keys");

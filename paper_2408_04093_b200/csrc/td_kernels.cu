@@ -1684,7 +1684,17 @@ __global__ void k6_seeded_fill(int dtype, void* dst, uint64_t seed, double half_
 namespace {
 
 constexpr int kBf16Tile = 32;
-constexpr int kF32Tile = 32, kF32Warps = 3, kF32Stages = 2;
+constexpr int kF32Tile = 32;
+// k1_f32 geometry (warps x stages of 32-token K+V tiles, 192 KB of stages):
+// TD_F32_CFG = 0 (3 x 2, default), 1 (2 x 3), 2 (6 x 1), 3 (1 x 6)
+int f32_cfg() {
+    static const int c = [] { const char* e = std::getenv("TD_F32_CFG"); return e ? std::atoi(e) & 3 : 0; }();
+    return c;
+}
+int f32_warps() {
+    static constexpr int w[4] = {3, 2, 6, 1};
+    return w[f32_cfg()];
+}
 constexpr int kGenTile = 32, kGenWarps = 4;
 constexpr int kSmemBudget = 192 * 1024;  // per CTA, one CTA per SM
 
@@ -1696,7 +1706,7 @@ template <int D>
 size_t bf16_smem() {
     return size_t(bf16_warps(D)) * bf16_stages(D) * bf16_stage_bytes(D) + 1024;
 }
-size_t f32_smem() { return size_t(kF32Warps) * kF32Stages * 2 * kF32Tile * 128 * 4 + 128; }
+size_t f32_smem() { return size_t(6) * 2 * kF32Tile * 128 * 4 + 128; }
 
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
@@ -1848,7 +1858,7 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     } else if (f32_ok) {
         p.kernel = 2;
         p.tile = kF32Tile;
-        p.warps = kF32Warps;
+        p.warps = f32_warps();
     } else {
         p.kernel = 0;
         p.tile = kGenTile;
@@ -2009,16 +2019,25 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
     } else if (p.kernel == 2) {
         const size_t sm = f32_smem();
         switch (p.group) {
-#define TD_LAUNCH_F32(GG)                                                   \
-    case GG: {                                                              \
-        auto kern = k1_f32<kF32Tile, kF32Warps, kF32Stages, GG>;            \
+#define TD_LAUNCH_F32_WS(GG, WW, SS)                                        \
+    {                                                                       \
+        auto kern = k1_f32<kF32Tile, WW, SS, GG>;                           \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;              \
-        if ((e = launch_pdl(kern, p.ctas, kF32Warps * 32, sm, st, p.pdl, a)) != cudaSuccess) return e; \
-        break;                                                              \
+        if ((e = launch_pdl(kern, p.ctas, WW * 32, sm, st, p.pdl, a)) != cudaSuccess) return e; \
     }
+#define TD_LAUNCH_F32(GG)                                                   \
+    case GG:                                                                \
+        switch (f32_cfg()) {                                                \
+        case 1: TD_LAUNCH_F32_WS(GG, 2, 3) break;                           \
+        case 2: TD_LAUNCH_F32_WS(GG, 6, 1) break;                           \
+        case 3: TD_LAUNCH_F32_WS(GG, 1, 6) break;                           \
+        default: TD_LAUNCH_F32_WS(GG, 3, 2) break;                          \
+        }                                                                   \
+        break;
             TD_LAUNCH_F32(1)
             TD_LAUNCH_F32(2)
 #undef TD_LAUNCH_F32
+#undef TD_LAUNCH_F32_WS
         default: return cudaErrorInvalidValue;
         }
     } else {

@@ -63,10 +63,10 @@ def dtype_of(t) -> DType:
 
 
 def set_deterministic(on: bool = True) -> None:
-    """Static split only, bitwise-reproducible results (the reference's
-    determinism property, test_decode.cpp:185-202). The default hands the last
-    ~15% of each (batch, kv-head) row out dynamically to the SMs that stream
-    fastest; results then agree to ~1e-7 between calls."""
+    """On (the default): the static, calibrated split -- bitwise-reproducible
+    results like the reference's (test_decode.cpp:185-202). Off: every call
+    hands the last ~15% of each (batch, kv-head) row out dynamically to the SMs
+    that stream fastest (TD_DYNAMIC); results then agree to ~1e-7 between calls."""
     check(lib().td_set_deterministic(1 if on else 0))
 
 

@@ -10,10 +10,14 @@
 //           the K1 structure without the math
 //   ldg   : plain 128-bit ld.global.nc, grid-stride, many CTAs
 // Prints one JSON line per (variant, size): best and median of 20 launches.
+// Between launches the L2 is flushed by a 256 MB memset (FLUSH=write, the
+// default), a 256 MB read (FLUSH=read: leaves clean lines, no write-back in the
+// timed kernel) or not at all (NOFLUSH=1 or FLUSH=none).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <vector>
@@ -100,9 +104,14 @@ void timeit(const char* name, size_t bytes, int ctas, F launch, uint8_t* flush, 
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     std::vector<float> ms;
-    static const bool no_flush = getenv("NOFLUSH") != nullptr;
+    static const char* fm = getenv("FLUSH");
+    static const bool no_flush = getenv("NOFLUSH") != nullptr || (fm && !strcmp(fm, "none"));
+    static const bool read_flush = fm && !strcmp(fm, "read");
     for (int it = 0; it < 23; ++it) {
-        if (!no_flush) CK(cudaMemsetAsync(flush, it & 255, flush_bytes));
+        if (!no_flush && read_flush)
+            k_ldg<<<1184, 512>>>(reinterpret_cast<const uint4*>(flush), flush_bytes / 16, reinterpret_cast<unsigned*>(flush));
+        else if (!no_flush)
+            CK(cudaMemsetAsync(flush, it & 255, flush_bytes));
         CK(cudaEventRecord(a));
         launch();
         CK(cudaEventRecord(b));
@@ -113,9 +122,9 @@ void timeit(const char* name, size_t bytes, int ctas, F launch, uint8_t* flush, 
     }
     CK(cudaGetLastError());
     std::sort(ms.begin(), ms.end());
-    printf("{\"flush\": %d, \"variant\": \"%s\", \"ctas\": %d, \"mb\": %.1f, \"best_us\": %.2f, \"median_us\": %.2f, "
+    printf("{\"flush\": \"%s\", \"variant\": \"%s\", \"ctas\": %d, \"mb\": %.1f, \"best_us\": %.2f, \"median_us\": %.2f, "
            "\"best_gbs\": %.1f, \"median_gbs\": %.1f}\n",
-           no_flush ? 0 : 1, name, ctas, bytes / 1e6, ms[0] * 1e3, ms[ms.size() / 2] * 1e3, bytes / (ms[0] * 1e-3) / 1e9,
+           no_flush ? "none" : (read_flush ? "read" : "write"), name, ctas, bytes / 1e6, ms[0] * 1e3, ms[ms.size() / 2] * 1e3, bytes / (ms[0] * 1e-3) / 1e9,
            bytes / (ms[ms.size() / 2] * 1e-3) / 1e9);
     fflush(stdout);
 }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--nq", type=int, default=32)
     ap.add_argument("--nkv", type=int, default=8)
     ap.add_argument("--append", action="store_true", help="append one token before every step")
+    ap.add_argument("--isolated", action="store_true", help="synchronise after every step (a cold call each time)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -53,6 +54,8 @@ def main():
         if args.append:
             w.append_kv(tok, tok)
         w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
+        if args.isolated:
+            w._sync_worker()
     torch.cuda.synchronize()
     st = w.debug_stamps(6144)
     rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(3, 3 + args.steps)]
@@ -63,6 +66,8 @@ def main():
     waits = [round(tl[i + 1][1] - tl[i][3], 2) for i in range(len(tl) - 1)]
     steps = [round(tl[i + 1][1] - tl[i][1], 2) for i in range(len(tl) - 1)]
     print(json.dumps({"rank": local, "world": world, "seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
+                      "isolated": args.isolated,
+                      "k1_first_start_to_first_past_wait": [round(r[1] - r[0], 2) for r in tl],
                       "abs_k1_start_us": [round(r[0] / 1000.0, 2) for r in rows],
                       "abs_k1_end_us": [round(r[2] / 1000.0, 2) for r in rows],
                       "abs_k2_done_us": [round(r[3] / 1000.0, 2) for r in rows],

@@ -26,7 +26,7 @@ def main():
         dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to("cuda").to(torch.bfloat16)  # noqa: E731
         w = td.Worker(0)
         w.place_kv(dev(k), dev(v))
-        outs = [w.tree_decode(dev(q)) for _ in range(3)]
+        outs = [w.tree_decode(dev(q), flags=td._capi.TD_DYNAMIC) for _ in range(3)]  # the pool feeds the stealing
         want = orc.tree_decode(q, k, v, 1, HIER, 1.0, F64, nthreads=os.cpu_count() or 8)
         errs = [rel_err(o.double().cpu().numpy(), want) for o in outs]
         good = max(errs) <= 1e-3

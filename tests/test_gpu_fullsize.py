@@ -9,9 +9,9 @@ check every head (test_decode.cpp:44-58, acceptance_main.cpp:154-187); so do
 these, at the sizes bench.py measures:
 
 * cfg3: Llama-3-8B attention, 32 q / 8 kv heads, d 128, 1,048,576 tokens --
-  the default N=1 path (calibrated partition, dynamic pool, cross-row
-  stealing), through the device and the host-buffer (e2e) calls, and the
-  deterministic static split;
+  the default N=1 path (calibrated static partition), through the device and
+  the host-buffer (e2e) calls, and the opt-in dynamic pool with cross-row
+  stealing;
 * cfg4: batch 16, 64 q / 8 kv heads, 131,072 tokens per sequence (1024 rows);
 * cfg2: 32-head MHA, 262,144 tokens, one GPU and p = 8 in-process workers;
 * one p = 8 shard of cfg3 (131,072 tokens), the per-GPU work of the north star.
@@ -59,7 +59,7 @@ def test_cfg3_1m_every_row(td, oracle, scale):
     outs = [w.tree_decode(q, scale) for _ in range(3)]  # the first call calibrates the partition
     qhost = q.cpu()
     outs.append(w.tree_decode(qhost, scale))                           # host buffers (the e2e call)
-    outs.append(w.tree_decode(q, scale, flags=td._capi.TD_DETERMINISTIC))  # static split
+    outs.append(w.tree_decode(q, scale, flags=td._capi.TD_DYNAMIC))  # dynamic pool + cross-row stealing
     gain, state = w.calibration_info()
     w.close()
     torch.cuda.synchronize()
@@ -84,7 +84,7 @@ def test_cfg3_p8_shard_every_row(td, oracle):
 def test_cfg4_batch16_every_row(td, oracle):
     b, n_q, n_kv, n, d = 16, 64, 8, 131072, 128
     w, q, qh, sk, sv = _seeded_case(td, oracle, BF16, b, n_q, n_kv, n, d)
-    outs = [w.tree_decode(q) for _ in range(2)]
+    outs = [w.tree_decode(q), w.tree_decode(q, flags=td._capi.TD_DYNAMIC)]
     w.close()
     want = full_decode(oracle, qh, n_kv, n, sk, sv, BF16)
     assert len(want) == b * n_q == 1024

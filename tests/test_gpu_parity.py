@@ -218,28 +218,34 @@ def test_tree_decode_validation(td, oracle):
 
 
 def test_decode_is_deterministic(td, oracle):
-    """test_decode.cpp:185-202: bitwise-identical results in deterministic mode;
-    the default (dynamic tail) mode agrees to ~1e-7."""
+    """test_decode.cpp:185-202: bitwise-identical results by default (the static
+    calibrated split); the opt-in dynamic pool (TD_DYNAMIC / set_deterministic(False))
+    agrees to ~1e-7."""
     import torch
     q, k, v = make_inputs(oracle, 9, 1, 32, 8, 400000, 128, BF16)
     qd, kd, vd = dev(q, BF16), dev(k, BF16), dev(v, BF16)
     cache = td.shard_kv(kd, vd, 8)
+    a = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+    b = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+    assert torch.equal(a, b)
+    w = td.Worker(0)
+    w.place_kv(kd, vd)
+    x = w.tree_decode(qd)
+    y = w.tree_decode(qd)
+    h = w.tree_decode(qd.cpu())  # the host-buffer path computes the same split
+    assert torch.equal(x, y) and torch.equal(x.cpu(), h)
+    dyn = [w.tree_decode(qd, flags=td._capi.TD_DYNAMIC) for _ in range(3)]
     try:
-        td.set_deterministic(True)
-        a = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
-        b = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
-        assert torch.equal(a, b)
-        w = td.Worker(0)
-        w.place_kv(kd, vd)
-        x = w.tree_decode(qd)
-        y = w.tree_decode(qd)
-        assert torch.equal(x, y)
-    finally:
         td.set_deterministic(False)
-    c = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
-    z = w.tree_decode(qd)
+        c = td.tree_decode(qd, cache, td.topology_for_workers(8)).output
+        z = w.tree_decode(qd)
+    finally:
+        td.set_deterministic(True)
     w.close()
     assert rel_err(host(c), host(a)) <= 5e-6 and rel_err(host(z), host(x)) <= 5e-6
+    assert max(rel_err(host(o), host(x)) for o in dyn) <= 5e-6
+    want = oracle.tree_decode(q, k, v, 1, HIER, 1.0, F64, nthreads=8)
+    assert rel_err(host(x), want) <= 1e-3 and rel_err(host(dyn[0]), want) <= 1e-3
 
 
 # ---------------------------------------------------------------- the Worker (C-ABI context) path
@@ -355,14 +361,16 @@ def test_worker_append_validation_and_output_buffers(td, oracle):
 
 
 def test_long_shard_default_path(td, oracle):
-    """A shard long enough (>= 1024 tiles per CTA) for the default to turn
-    cross-row stealing on, with the calibrated partition: the bench's N=1 path."""
+    """A shard long enough (>= 1024 tiles per CTA) for the dynamic mode to turn
+    cross-row stealing on, with the calibrated partition; and the default static
+    split (the bench's N=1 path)."""
     n, n_q, n_kv = 655360, 32, 8
     seed = oracle.mix64(0, n)
     w = td.Worker(0)
     w.generate_kv(td.DType(BF16), 1, n_kv, n, 128, oracle.mix64(seed, 2), oracle.mix64(seed, 3))
     q = oracle.seeded(oracle.mix64(seed, 1), n_q * 128, BF16).reshape(1, n_q, 128)
-    outs = [w.tree_decode(dev(q, BF16)) for _ in range(3)]
+    outs = [w.tree_decode(dev(q, BF16)) for _ in range(2)]
+    outs += [w.tree_decode(dev(q, BF16), flags=td._capi.TD_DYNAMIC) for _ in range(2)]  # pool + stealing
     w.close()
     want = full_decode(oracle, q, n_kv, n, oracle.mix64(seed, 2), oracle.mix64(seed, 3), BF16)  # every row
     for o in outs:
