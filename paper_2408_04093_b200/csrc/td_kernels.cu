@@ -881,6 +881,11 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         const int64_t rem = a.t - tok0;
         const int nvalid = rem < T ? static_cast<int>(rem) : T;
         mbar_wait(&bars[warp][s], phase);
+        if (a.reverse & 2) {  // debug (TD_DEBUG_REVERSE=2): no math, the stream alone
+            __syncwarp();
+            if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+            continue;
+        }
         const float* ks_ = reinterpret_cast<const float*>(wsm + size_t(s) * STAGE_BYTES);
         const float* vs_ = ks_ + T * D;
 

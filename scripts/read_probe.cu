@@ -86,6 +86,40 @@ __global__ void __launch_bounds__(W * 32) k_bulk(const uint8_t* src, size_t byte
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// The split kernel's fp32 stream: every stage is a K chunk and a V chunk at
+// the same offset of two separate arrays (W warps x S stages, CHUNK bytes each).
+template <int W, int S, int CHUNK>
+__global__ void __launch_bounds__(W * 32) k_bulk_kv(const uint8_t* k, const uint8_t* v, size_t bytes, unsigned* sink) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bars[W][S];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t nchunks = bytes / CHUNK;
+    const size_t c0 = nchunks * blockIdx.x / gridDim.x, c1 = nchunks * (blockIdx.x + 1) / gridDim.x;
+    uint8_t* ring = smem + size_t(warp) * S * 2 * CHUNK;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const size_t mine = c1 > c0 + warp ? (c1 - c0 - warp + W - 1) / W : 0;
+    auto issue = [&](size_t kk, int s) {
+        const size_t off = (c0 + warp + kk * W) * CHUNK;
+        mbar_expect(&bars[warp][s], 2 * CHUNK);
+        bulk(ring + s * 2 * CHUNK, k + off, CHUNK, &bars[warp][s]);
+        bulk(ring + s * 2 * CHUNK + CHUNK, v + off, CHUNK, &bars[warp][s]);
+    };
+    if (lane == 0)
+        for (int s = 0; s < S && s < (int)mine; ++s) issue(s, s);
+    unsigned acc = 0;
+    for (size_t kk = 0; kk < mine; ++kk) {
+        const int s = int(kk % S);
+        mbar_wait(&bars[warp][s], unsigned((kk / S) & 1));
+        acc += reinterpret_cast<const unsigned*>(ring + s * 2 * CHUNK)[lane];
+        __syncwarp();
+        if (lane == 0 && kk + S < mine) issue(kk + S, s);
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
 __global__ void k_ldg(const uint4* src, size_t n, unsigned* sink) {
     unsigned acc = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
@@ -149,8 +183,22 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(k_bulk<W, S, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     constexpr int W2 = 8, S2 = 3, CH2 = 8192;
     CK(cudaFuncSetAttribute(k_bulk<W2, S2, CH2>, cudaFuncAttributeMaxDynamicSharedMemorySize, W2 * S2 * CH2));
+    constexpr int W3 = 3, S3 = 2, CH3 = 16384;
+    CK(cudaFuncSetAttribute(k_bulk_kv<W3, S3, CH3>, cudaFuncAttributeMaxDynamicSharedMemorySize, W3 * S3 * 2 * CH3));
+    CK(cudaFuncSetAttribute(k_bulk_kv<4, 3, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * 2 * 8192));
     for (double mb : mbs) {
         const size_t bytes = size_t(mb * 1e6) / 16384 * 16384;
+        // K and V halves of the same total bytes: the fp32 split kernel's two streams
+        const size_t half = bytes / 2 / 16384 * 16384;
+        const uint8_t* vsrc = src + (maxb / 2) / (size_t(2) << 20) * (size_t(2) << 20);  // a 2 MB-aligned second array
+        if (vsrc + half <= src + maxb) {
+            timeit("bulk_kv_w3_s2_16k", 2 * half, sms,
+                   [&] { k_bulk_kv<W3, S3, CH3><<<sms, W3 * 32, W3 * S3 * 2 * CH3>>>(src, vsrc, half, sink); }, flush,
+                   flush_bytes);
+            timeit("bulk_kv_w4_s3_8k", 2 * half, sms,
+                   [&] { k_bulk_kv<4, 3, 8192><<<sms, 4 * 32, 4 * 3 * 2 * 8192>>>(src, vsrc, half, sink); }, flush,
+                   flush_bytes);
+        }
         timeit("bulk_w4_s3_16k", bytes, sms, [&] { k_bulk<W, S, CH><<<sms, W * 32, smem>>>(src, bytes, sink); },
                flush, flush_bytes);
         timeit("bulk_w8_s3_8k", bytes, sms,

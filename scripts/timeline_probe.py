@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--nkv", type=int, default=8)
     ap.add_argument("--append", action="store_true", help="append one token before every step")
     ap.add_argument("--isolated", action="store_true", help="synchronise after every step (a cold call each time)")
+    ap.add_argument("--dynamic", action="store_true", help="TD_DYNAMIC: the dynamic tile pool")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -38,6 +39,8 @@ def main():
         flags = _capi.TD_P2P
     else:
         w = td.Worker(local)
+    if args.dynamic:
+        flags |= _capi.TD_DYNAMIC
     w.generate_kv(td.DType.Bf16, args.b, args.nkv, args.seq_len, 128, 2, 3)
     q = td.seeded_tensor([args.b, args.nq, 128], 1, 1.0, td.DType.Bf16)
     out = torch.empty(args.b, args.nq, 128, device="cuda")
