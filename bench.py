@@ -96,10 +96,10 @@ def interconnect(args, world, b, n_q, n_kv, n, d, esz, ms):
 
 def read_ceiling(nbytes):
     """The measured ceiling of a plain streaming-read kernel at the nearest
-    working-set size (scripts/read_probe.cu, profiles/r1_read_probe_noflush.jsonl):
+    working-set size (scripts/read_probe.cu, profiles/r2_read_ceiling.jsonl):
     MEASURED_PEAKS.json's HBM figure is a read+write copy, which a read-only
-    stream exceeds."""
-    path = os.path.join(ROOT, "profiles", "r1_read_probe_noflush.jsonl")
+    stream exceeds at large sizes and cannot reach at small ones (ramp)."""
+    path = os.path.join(ROOT, "profiles", "r2_read_ceiling.jsonl")
     try:
         rows = [json.loads(x) for x in open(path) if x.startswith("{")]
     except OSError:
@@ -107,9 +107,8 @@ def read_ceiling(nbytes):
     if not rows:
         return None
     mb = nbytes / 1e6
-    near = min({r["mb"] for r in rows}, key=lambda m: abs(m - mb))
-    best = max(r["best_gbs"] for r in rows if r["mb"] == near)
-    return {"gbs": best, "at_mb": near, "source": "profiles/r1_read_probe_noflush.jsonl (best of the variants)"}
+    near = min(rows, key=lambda r: abs(math.log(r["mb"] / mb)))
+    return {"gbs": near["gbs"], "at_mb": near["mb"], "how": near["how"], "source": near["source"]}
 
 
 def load_peaks():
