@@ -526,16 +526,19 @@ def main():
             w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, _capi.TD_TIME_PHASES)
         barrier(world)
         nccl_phases = [round(max_over_ranks(x, world) * 1000.0, 2) for x in w.phase_times()]
+        graph_ms = timed_loop(lambda fl: w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale,
+                                                             fl | _capi.TD_GRAPH), ks)
         ring_ms = timed_loop(lambda fl: w.ring_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, fl), ks)
         compare = {
             "steps": ks,
             "tree_us": ms * 1000.0, "tree_combine": args.combine,
             "nccl_us": nccl_ms * 1000.0,
             "nccl_phases_us": dict(zip(("K1", "K2", "allreduce_max", "K3", "allreduce_sum", "K4"), nccl_phases)),
+            "nccl_graph_us": graph_ms * 1000.0,
             "ring_us": ring_ms * 1000.0,
             "tree_over_ring": ring_ms / ms,
             "note": "same cache and query; nccl = K1, K2, ncclAllReduce(max), K3, ncclAllReduce(sum), K4 "
-                    "(decode.cpp:129-173 literally); ring = p-1 NCCL send/recv rotations of the KV shards with "
+                    "(decode.cpp:129-173 literally), nccl_graph = the same step replayed as a CUDA graph; ring = p-1 NCCL send/recv rotations of the KV shards with "
                     "the partial of the chunk in hand overlapped (decode.cpp:186-251); tree_over_ring = "
                     "ring_us / tree_us",
         }

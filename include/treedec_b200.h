@@ -71,11 +71,15 @@ enum {
                              call returns when the host sees that signal (no stream
                              synchronisation). Ignored where it cannot apply (the
                              NCCL path, TD_BF16_OUT). */
-    TD_DYNAMIC = 256      /* this call: hand the last ~15% of each (batch, kv-head)
+    TD_DYNAMIC = 256,     /* this call: hand the last ~15% of each (batch, kv-head)
                              row out at run time to the SMs that stream fastest
                              (and let idle warps take other rows' chunks on long
                              shards). Up to ~2.5% faster on some shapes; results
                              then agree to ~1e-7, not bitwise, between calls. */
+    TD_GRAPH = 512        /* paper-literal NCCL path (nranks > 1 without TD_P2P), device
+                             buffers: capture the step (K1, K2, allreduce(max), K3,
+                             allreduce(sum), K4) as a CUDA graph once per shape and
+                             replay it (TD_NCCL_GRAPH=1 sets it for every call) */
 };
 
 typedef struct td_context td_context;

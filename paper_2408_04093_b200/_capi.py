@@ -18,6 +18,7 @@ TD_TREE_BINARY, TD_RING_ALLREDUCE, TD_HIERARCHICAL = 0, 1, 2
 TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT, TD_TIME_PHASES, TD_P2P, TD_DEBUG_TS, TD_DETERMINISTIC = 1, 2, 4, 8, 16, 32, 64
 TD_PINNED_IO = 128
 TD_DYNAMIC = 256
+TD_GRAPH = 512
 
 # Every symbol include/treedec_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = [

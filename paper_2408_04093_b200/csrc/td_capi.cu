@@ -258,6 +258,23 @@ struct td_context {
     ncclWindow_t win = nullptr;
     int win_state = 0;  // 0 untried, 1 registered, -1 unavailable (plain buffers)
 
+    // TD_GRAPH: the paper-literal NCCL step (K1, K2, allreduce(max), K3,
+    // allreduce(sum), K4) captured once per shape and replayed; only the split
+    // kernel's SM-affinity claim epoch changes between replays
+    struct Graph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t k1 = nullptr;
+        const void* q = nullptr;
+        float* out = nullptr;
+        double scale = 0.0;
+        int64_t rows = 0, total = -1, per_bh = 0, len = 0, cap = 0, t_safe = -1;
+        int ctas = 0, maxseg = 0, kernel = -1;
+        const void* x_table = nullptr;
+        const void* k = nullptr;
+        float* lse = nullptr;
+    } graph;
+
     DevBuf ctr;        // K1 dynamic-pool counters (SplitPlan::counters)
     int64_t ctr_bh = -1;
     int kpar = 0;      // parity of the next launch
@@ -915,6 +932,8 @@ int td_destroy(td_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->xfer);
+    if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
+    if (ctx->graph.graph) cudaGraphDestroy(ctx->graph.graph);
     if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
     if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -1433,6 +1452,95 @@ int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xd
     return TD_OK;
 }
 
+// TD_GRAPH (per call) or TD_NCCL_GRAPH=1 (process): replay the paper-literal NCCL
+// step as a CUDA graph. Applies to device buffers with the static split (no pool
+// counters to alternate) and no per-call instrumentation.
+bool graph_mode(td_context* ctx, const SplitPlan& plan, int flags) {
+    static const bool env = [] { const char* e = std::getenv("TD_NCCL_GRAPH"); return e && std::atoi(e) != 0; }();
+    if (!(env || (flags & TD_GRAPH))) return false;
+    if (flags & (TD_HOST_IO | TD_TIME_KERNELS | TD_TIME_PHASES | TD_BF16_OUT | TD_DEBUG_TS)) return false;
+    return plan.pool_tiles == 0 && !plan.dbg && !plan.tl && ctx->comm;
+}
+
+// The NCCL tree step as a graph: captured on the first call of a shape (the
+// capture records the launches without running them), then launched; later calls
+// with the same shape, buffers and scale only patch K1's claim epoch and relaunch.
+int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, double scale, int64_t rows, float* lse,
+                    float* shift, float* nd, float* out) {
+    auto& g = ctx->graph;
+    const int64_t d = ctx->d;
+    const bool same = g.exec && g.q == qd && g.out == out && g.scale == scale && g.rows == rows &&
+                      g.total == plan.total_tiles && g.per_bh == plan.tiles_per_bh && g.len == ctx->len &&
+                      g.cap == ctx->cap && g.ctas == plan.ctas && g.maxseg == plan.maxseg && g.kernel == plan.kernel &&
+                      g.x_table == plan.x_table && g.k == ctx->k.p && g.lse == lse && g.t_safe == plan.t_safe;
+    if (same) {
+        TD_CUDA(td::graph_set_k1_epoch(g.exec, g.k1, plan));
+    } else {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+        g = td_context::Graph{};
+        TD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok, ctx->row_max, lse,
+                             ctx->out_local, false);
+        if (rc == TD_OK && nccl().AllReduce(lse, shift, size_t(rows), ncclFloat32, ncclMax, ctx->comm, ctx->stream) !=
+                               ncclSuccess)
+            rc = set_err(TD_ENCCL, "tree_decode (graph): allreduce(max) capture failed");
+        if (rc == TD_OK && td::launch_to_numerator(lse, ctx->out_local, shift, rows, static_cast<int>(d), nd,
+                                                   ctx->stream) != cudaSuccess)
+            rc = set_err(TD_ECUDA, "tree_decode (graph): K3 capture failed");
+        if (rc == TD_OK && nccl().AllReduce(nd, nd, size_t(rows * d + rows), ncclFloat32, ncclSum, ctx->comm,
+                                            ctx->stream) != ncclSuccess)
+            rc = set_err(TD_ENCCL, "tree_decode (graph): allreduce(sum) capture failed");
+        if (rc == TD_OK &&
+            td::launch_finalize(nd, rows, static_cast<int>(d), out, nullptr, ctx->stream) != cudaSuccess)
+            rc = set_err(TD_ECUDA, "tree_decode (graph): K4 capture failed");
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        TD_CUDA(ec);
+        g.graph = graph;
+        TD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+        size_t n = 0;
+        TD_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        TD_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n));
+        const void* k1f = td::k1_function(plan);
+        for (cudaGraphNode_t node : nodes) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            if (cudaGraphKernelNodeGetParams(node, &kp) == cudaSuccess && kp.func == k1f) g.k1 = node;
+        }
+        cudaGetLastError();
+        if (!g.k1) return set_err(TD_ECUDA, "tree_decode (graph): split kernel node not found");
+        g.q = qd;
+        g.out = out;
+        g.scale = scale;
+        g.rows = rows;
+        g.total = plan.total_tiles;
+        g.per_bh = plan.tiles_per_bh;
+        g.len = ctx->len;
+        g.cap = ctx->cap;
+        g.ctas = plan.ctas;
+        g.maxseg = plan.maxseg;
+        g.kernel = plan.kernel;
+        g.x_table = plan.x_table;
+        g.k = ctx->k.p;
+        g.lse = lse;
+        g.t_safe = plan.t_safe;
+    }
+    TD_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+    ctx->kv_safe = ctx->len;
+    ctx->last_kernels = 4;  // K1, K2, K3, K4 (+ two NCCL kernels)
+    ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
+                         td::dtype_bytes(ctx->dtype);
+    ctx->last_split_kernel = plan.kernel;
+    return note_table_use(ctx);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1502,6 +1610,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
             nd = w + 2 * pr;
         }
     }
+    if (ctx->nranks > 1 && graph_mode(ctx, plan, flags)) return tree_nccl_graph(ctx, plan, qd, scale, rows, lse, shift, nd, out);
     // 1. local partial (out, lse) of this shard
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
                           ctx->row_max, lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0,

@@ -140,6 +140,12 @@ cudaError_t launch_decode_exchange(const SplitPlan& plan, const void* q, const v
                                    void* workspace, const XchgArgs& xa, float* out, cudaStream_t stream,
                                    cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
+// CUDA-graph replay of a captured step: the split kernel's entry point for `plan`
+// (to find its node) and an update of that node's per-launch state -- the SM
+// affinity claim epoch -- in an instantiated graph.
+const void* k1_function(const SplitPlan& plan);
+cudaError_t graph_set_k1_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const SplitPlan& plan);
+
 // Builds the 2-D tensor map used by the bf16 kernel over rows x d elements.
 bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,
                      std::string& msg);

@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     __shared__ uint64_t bars[W][S];
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
 
-    const unsigned long long t_start = a.dbg ? gtimer() : 0ull;
+    const unsigned long long t_start = (a.dbg || a.tl) ? gtimer() : 0ull;
     // PDL: K2 may be scheduled as soon as CTAs of this grid retire; it waits
     // (griddepcontrol.wait) for this grid's completion before reading.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -803,6 +803,10 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     __syncwarp();
     // this grid is itself a programmatic dependent: inputs only after the wait
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.tl && threadIdx.x == 0) {
+        atomicMin(a.tl + 0, t_start);
+        atomicMin(a.tl + 1, gtimer());
+    }
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int64_t kk, int s) {
         const int64_t x = x0 + warp + kk * W;
@@ -824,10 +828,13 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         for (int h = 0; h < G; ++h) {
             const float4 qq = __ldcg(reinterpret_cast<const float4*>(
                 static_cast<const float*>(a.q) + ((b * a.n_q) + kvh * G + h) * int64_t(D)) + lane);
-            qv[h][0] = qq.x * a.scale_log2;
-            qv[h][1] = qq.y * a.scale_log2;
-            qv[h][2] = qq.z * a.scale_log2;
-            qv[h][3] = qq.w * a.scale_log2;
+            // raw q: no arithmetic on the loaded value here, so the warp does not
+            // wait for it before issuing its first bulk copies (the scale is applied
+            // to the reduced score instead)
+            qv[h][0] = qq.x;
+            qv[h][1] = qq.y;
+            qv[h][2] = qq.z;
+            qv[h][3] = qq.w;
         }
     };
     auto reset = [&]() {
@@ -909,7 +916,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
                     part[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
                 }
             }
-            sc[h] = lane < nvalid ? part[0] : -CUDART_INF_F;
+            sc[h] = lane < nvalid ? part[0] * a.scale_log2 : -CUDART_INF_F;
         }
         float p[G];
 #pragma unroll
@@ -952,7 +959,8 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         }
     }
     __syncthreads();
-    cta_merge<W>(a, c, reinterpret_cast<float*>(smem));
+    cta_merge_batched<W, D, 8>(a, c, reinterpret_cast<float*>(smem));
+    if (a.tl && threadIdx.x == 0) atomicMax(a.tl + 2, gtimer());
     if (a.dbg && threadIdx.x == 0) {
         const unsigned long long t_end = gtimer();
         atomicMin(a.dbg + 0, t_start);
@@ -1218,62 +1226,96 @@ __device__ __forceinline__ void merge_row_warp(const K1Args& a, int64_t r, const
         rmax_o = empty ? -CUDART_INF_F : M * kLn2;
         return;
     }
-    float ml = -CUDART_INF_F, ll = 0.f;  // lane i holds (m, l) of candidate i0 + i (BO <= 32)
-    auto load = [&](int i0) {
+    // General path (foreign states, or more than BO candidates): an online merge over
+    // batches of BO candidates -- lane i holds (m, l) of the batch's candidate i, every
+    // lane the o columns of all of them. When the registers allow two batches, the next
+    // batch's loads are issued before the current one is combined, so T candidates cost
+    // about one L2 round trip plus the issue of T / BO batches.
+    if (T <= 0) {  // no state covers the row (an empty shard): the identity
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) res.v[c][v] = 0.f;
+        lse_o = rmax_o = -CUDART_INF_F;
+        return;
+    }
+    constexpr int NB = (V * NC * BO <= 64) ? 2 : 1;
+    vec ob[NB][BO][NC];
+    float mlb[NB], llb[NB];
+    auto load = [&](int i0, auto bufc) {
+        constexpr int b = decltype(bufc)::value;
         {
             const int i = i0 + lane;
-            ml = -CUDART_INF_F;
-            ll = 0.f;
+            mlb[b] = -CUDART_INF_F;
+            llb[b] = 0.f;
             if (lane < BO && i < T) {
                 const int off = off_of(i);
-                ml = __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off);
-                ll = __ldcg((i >= S ? a.fslot_l : a.cslot_l) + off);
+                mlb[b] = __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off);
+                llb[b] = __ldcg((i >= S ? a.fslot_l : a.cslot_l) + off);
             }
         }
 #pragma unroll
         for (int u = 0; u < BO; ++u) {
             const int i = i0 + u;
-            const int off = off_of(i);
-            const float* ob = i >= S ? a.fslot_o : a.cslot_o;
+            const int off = off_of(i < T ? i : T - 1);
+            const float* obase = (i < T ? i : T - 1) >= S ? a.fslot_o : a.cslot_o;
 #pragma unroll
             for (int c = 0; c < NC; ++c)
-                if (i < T && col0 + c * 32 * V < D)
-                    ov[u][c] = __ldcg(reinterpret_cast<const vec*>(ob + off * D + col0 + c * 32 * V));
+                if (col0 + c * 32 * V < D)
+                    ob[b][u][c] = __ldcg(reinterpret_cast<const vec*>(obase + off * D + col0 + c * 32 * V));
         }
     };
-    load(0);
-    float M = -CUDART_INF_F;
-    if (T <= BO) {
-        M = ml;
-    } else {
-        for (int i = lane; i < T; i += 32) M = fmaxf(M, __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off_of(i)));
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float acc[NC][V], L = 0.f;
+    float M = -CUDART_INF_F, L = 0.f, acc[NC][V];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[c][v] = 0.f;
-    for (int i0 = 0; i0 < T; i0 += BO) {
-        if (i0 > 0) load(i0);
-        // lane-parallel weights, then broadcast per candidate
-        const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - M);
+    auto combine = [&](int i0, auto bufc) {
+        constexpr int b = decltype(bufc)::value;
+        const float ml = mlb[b], ll = llb[b];
+        float Mb = ml;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, off));
+        const float Mn = fmaxf(M, Mb);
+        const float cs = M == -CUDART_INF_F ? 0.f : fast_exp2(M - Mn);  // rescale what is merged so far
+        L *= cs;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[c][v] *= cs;
+        const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - Mn);
         float lsum = e_l * ll;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
         L += lsum;
 #pragma unroll
         for (int u = 0; u < BO; ++u) {
-            const float e = __shfl_sync(0xffffffffu, e_l, u);
-            if (i0 + u < T) {
+            const float e = __shfl_sync(0xffffffffu, e_l, u);  // 0 past the last candidate
 #pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const float* o = reinterpret_cast<const float*>(&ov[u][c]);
+            for (int c = 0; c < NC; ++c) {
+                const float* o = reinterpret_cast<const float*>(&ob[b][u][c]);
 #pragma unroll
-                    for (int v = 0; v < V; ++v) acc[c][v] += e * o[v];
-                }
+                for (int v = 0; v < V; ++v)  // an empty state's o is never read as a value (it may be stale)
+                    acc[c][v] = fmaf(e, e != 0.f ? o[v] : 0.f, acc[c][v]);
             }
+        }
+        M = Mn;
+    };
+    using B0 = std::integral_constant<int, 0>;
+    if constexpr (NB == 2) {
+        using B1 = std::integral_constant<int, 1>;
+        load(0, B0{});
+        for (int i0 = 0; i0 < T; i0 += 2 * BO) {
+            if (i0 + BO < T) load(i0 + BO, B1{});
+            combine(i0, B0{});
+            if (i0 + BO >= T) break;
+            if (i0 + 2 * BO < T) load(i0 + 2 * BO, B0{});
+            combine(i0 + BO, B1{});
+        }
+    } else {
+        for (int i0 = 0; i0 < T; i0 += BO) {
+            load(i0, B0{});
+            combine(i0, B0{});
         }
     }
     const bool empty = M == -CUDART_INF_F;
@@ -1395,6 +1437,107 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
         }
     }
     if (a.tl && (threadIdx.x & 31) == 0) atomicMax(a.tl + 3, gtimer());
+    signal_done(a);
+}
+
+// K2 for rows with many candidate states (few (b, kv-head) rows over many CTAs,
+// e.g. cfg1's single row merges ~148 CTA states): each (row, column quarter)
+// gets a block of WS warps that split the candidates -- each warp merges its
+// share (at most 32 per L2 round trip) into an unnormalised (M, L, o) -- and warp
+// 0 combines the WS partials from shared memory. One warp walking 148
+// candidates took ~7 us; this takes about one round trip per warp plus the
+// shared-memory combine. Same arithmetic per column as k2_combine_cols.
+template <int Q, int WS>
+__global__ void __launch_bounds__(32 * WS) k2_combine_split(const K1Args a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ float sm_m[WS], sm_l[WS], sm_o[WS][32];
+    const int64_t rows = a.bh_count * a.group, units = rows * Q;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Cover cv0 = blockIdx.x < units ? cover_of(a, (int64_t(blockIdx.x) / Q) / a.group) : Cover{};
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pool_tiles > 0)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
+             i += int64_t(gridDim.x) * blockDim.x) {
+            a.pool_next[i] = 0u;
+            if (a.fcnt_next) a.fcnt_next[i] = 0u;
+        }
+    const Tail& t = a.tail;
+    const int D = a.d, g = a.group, st = a.maxseg * g;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t r = u / Q;
+        const int col = static_cast<int>(u % Q) * 32 + lane;
+        const int h = static_cast<int>(r % g);
+        Cover cv = u == blockIdx.x ? cv0 : cover_of(a, r / g);
+        cv.nf = foreign_of(a, r / g);
+        const int S = cv.S, T = cv.S + cv.nf;
+        const int b0 = static_cast<int>((cv.c_lo * a.maxseg + cv.seg_lo) * g + h);
+        const int b1 = static_cast<int>((cv.c_lo + 1) * a.maxseg * g + h);
+        const int fb = static_cast<int>((r / g) * a.fslots * g + h);
+        auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
+        const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
+        float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
+        for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+            const int n = min(32, i_hi - i0);
+            float ml = -CUDART_INF_F, ll = 0.f;
+            if (lane < n) {
+                const int i = i0 + lane, off = off_of(i);
+                ml = __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off);
+                ll = __ldcg((i >= S ? a.fslot_l : a.cslot_l) + off);
+            }
+            float ov[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int i = i0 + min(k, n - 1);
+                ov[k] = __ldcg((i >= S ? a.fslot_o : a.cslot_o) + int64_t(off_of(i)) * D + col);
+            }
+            float Mb = ml;
+#pragma unroll
+            for (int o2 = 16; o2 >= 1; o2 >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, o2));
+            const float Mn = fmaxf(M, Mb);
+            const float cs = M == -CUDART_INF_F ? 0.f : fast_exp2(M - Mn);
+            L *= cs;
+            acc *= cs;
+            const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - Mn);
+            float ls = e_l * ll;
+#pragma unroll
+            for (int o2 = 16; o2 >= 1; o2 >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o2);
+            L += ls;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const float e = __shfl_sync(0xffffffffu, e_l, k);
+                acc = fmaf(e, e != 0.f ? ov[k] : 0.f, acc);
+            }
+            M = Mn;
+        }
+        if (lane == 0) {
+            sm_m[warp] = M;
+            sm_l[warp] = L;
+        }
+        sm_o[warp][lane] = acc;
+        __syncthreads();
+        if (warp == 0) {
+            float Mx = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < WS; ++w) Mx = fmaxf(Mx, sm_m[w]);
+            float Lt = 0.f, O = 0.f;
+#pragma unroll
+            for (int w = 0; w < WS; ++w) {
+                const float mw = sm_m[w];
+                const float e = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - Mx);
+                Lt += e * sm_l[w];
+                O += e != 0.f ? e * sm_o[w][lane] : 0.f;
+            }
+            const bool empty = Mx == -CUDART_INF_F;
+            const int64_t orow = out_row_of(a, r);
+            if (col < D) t.out[orow * D + col] = empty ? 0.f : O / Lt;
+            if (t.mode == kTailPartial && col == 0) {
+                t.lse[orow] = empty ? -CUDART_INF_F : (Mx + log2f(Lt)) * kLn2;
+                t.row_max[orow] = empty ? -CUDART_INF_F : Mx * kLn2;
+            }
+        }
+        __syncthreads();
+    }
+    if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
     signal_done(a);
 }
 
@@ -2102,6 +2245,28 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
     if (blocks > limit) blocks = limit;
 #define TD_K2(VV, NN, BB) launch_k2_t<VV, NN, BB>(a, blocks, warps, exchange, st)
     static const int cols = [] { const char* e = std::getenv("TD_K2_COLS"); return e ? std::atoi(e) : 4; }();
+    // few rows with many candidate states each (e.g. one row over every CTA): split
+    // each (row, quarter)'s candidates over the warps of a block
+    const int64_t cands = a.bh_count > 0 ? int64_t(a.ctas) / a.bh_count + 2 : 0;  // CTAs covering a row
+    static const int split = [] { const char* e = std::getenv("TD_K2_SPLIT"); return e ? std::atoi(e) : 1; }();
+    if (split && !exchange && a.d == 128 && force_w == 0 && rows * 4 <= limit && cands > 32 && !a.dbg) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(rows * 4));
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cands > 128) {
+            cfg.blockDim = dim3(32 * 8);
+            if (cudaError_t e = prefer_max_smem(k2_combine_split<4, 8>)) return e;
+            return cudaLaunchKernelEx(&cfg, k2_combine_split<4, 8>, a);
+        }
+        cfg.blockDim = dim3(32 * 4);
+        if (cudaError_t e = prefer_max_smem(k2_combine_split<4, 4>)) return e;
+        return cudaLaunchKernelEx(&cfg, k2_combine_split<4, 4>, a);
+    }
     if (cols == 4 && a.d == 128 && force_w == 0 && rows * 4 <= limit && !a.dbg) {
         const int64_t b4 = rows * 4;  // one (row, column quarter) per single-warp block
         cudaLaunchConfig_t cfg{};
@@ -2125,6 +2290,49 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
 }
 
 }  // namespace
+
+const void* k1_function(const SplitPlan& p) {
+    if (p.kernel == 1) {
+        switch (p.d) {
+        case 64: return reinterpret_cast<const void*>(k1_bf16<64, kBf16Tile, bf16_warps(64), bf16_stages(64)>);
+        case 128: return reinterpret_cast<const void*>(k1_bf16<128, kBf16Tile, bf16_warps(128), bf16_stages(128)>);
+        case 256: return reinterpret_cast<const void*>(k1_bf16<256, kBf16Tile, bf16_warps(256), bf16_stages(256)>);
+        default: return nullptr;
+        }
+    }
+    if (p.kernel == 2) {
+        static constexpr int wv[4] = {3, 2, 6, 1}, sv[4] = {2, 3, 1, 6};
+        const int w = wv[f32_cfg()], st = sv[f32_cfg()];
+        if (p.group == 1) {
+            if (w == 3) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 3, 2, 1>);
+            if (w == 2) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 2, 3, 1>);
+            if (w == 6) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 6, 1, 1>);
+            return reinterpret_cast<const void*>(k1_f32<kF32Tile, 1, 6, 1>);
+        }
+        if (w == 3) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 3, 2, 2>);
+        if (w == 2) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 2, 3, 2>);
+        if (w == 6) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 6, 1, 2>);
+        (void)st;
+        return reinterpret_cast<const void*>(k1_f32<kF32Tile, 1, 6, 2>);
+    }
+    return p.dtype == kBF16 ? reinterpret_cast<const void*>(k1_generic<__nv_bfloat16>)
+                            : reinterpret_cast<const void*>(k1_generic<float>);
+}
+
+cudaError_t graph_set_k1_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const SplitPlan& p) {
+    cudaKernelNodeParams kp{};
+    cudaError_t e = cudaGraphKernelNodeGetParams(node, &kp);
+    if (e != cudaSuccess) return e;
+    K1Args a = *static_cast<const K1Args*>(kp.kernelParams[0]);
+    a.epoch = p.epoch;
+    void* args[3] = {&a, nullptr, nullptr};
+    if (p.kernel == 1) {  // k1_bf16(K1Args, CUtensorMap, CUtensorMap)
+        args[1] = kp.kernelParams[1];
+        args[2] = kp.kernelParams[2];
+    }
+    kp.kernelParams = args;
+    return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
+}
 
 cudaError_t launch_decode_partial(const SplitPlan& p, const void* q, const void* k,
                                   const void* v, float scale, const CUtensorMap* tmk,

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--append", action="store_true", help="append one token before every step")
     ap.add_argument("--isolated", action="store_true", help="synchronise after every step (a cold call each time)")
     ap.add_argument("--dynamic", action="store_true", help="TD_DYNAMIC: the dynamic tile pool")
+    ap.add_argument("--f32", action="store_true", help="fp32 cache and query (the cfg1 kernel)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -41,8 +42,9 @@ def main():
         w = td.Worker(local)
     if args.dynamic:
         flags |= _capi.TD_DYNAMIC
-    w.generate_kv(td.DType.Bf16, args.b, args.nkv, args.seq_len, 128, 2, 3)
-    q = td.seeded_tensor([args.b, args.nq, 128], 1, 1.0, td.DType.Bf16)
+    dt = td.DType.Float32 if args.f32 else td.DType.Bf16
+    w.generate_kv(dt, args.b, args.nkv, args.seq_len, 128, 2, 3)
+    q = td.seeded_tensor([args.b, args.nq, 128], 1, 1.0, dt)
     out = torch.empty(args.b, args.nq, 128, device="cuda")
     for _ in range(3):
         w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)

@@ -45,6 +45,8 @@ def main():
         q = td.seeded_tensor([b, n_q, d], orc.mix64(seed, 1), 1.0, td.DType(dt))
         tree = w.tree_decode(q, scale)
         ring = w.ring_decode(q, scale)
+        # the same NCCL step replayed as a CUDA graph (captured on the first call)
+        graphed = [w.tree_decode(q, scale, flags=td._capi.TD_GRAPH) for _ in range(3)]
         fits = b * n_q <= 64 and d == 128
         p2p = w.tree_decode(q, scale, flags=td._capi.TD_P2P) if fits else tree
         # every rank must hold the same output
@@ -58,11 +60,13 @@ def main():
             e_ring = rel_err_rows(ring.double().cpu().numpy(), want)
             e_p2p = rel_err_rows(p2p.double().cpu().numpy(), want)
             same = all(torch.equal(t_all[0], x) for x in t_all)
-            good = e_tree <= tol and e_ring <= tol and e_p2p <= tol and same and w.p2p_status() == 0
+            same_graph = all(torch.equal(tree, x) for x in graphed)  # static split: bitwise
+            good = (e_tree <= tol and e_ring <= tol and e_p2p <= tol and same and same_graph
+                    and w.p2p_status() == 0)
             ok &= good
             print(json.dumps({"world": world, "dtype": "bf16" if dt == BF16 else "f32", "n": n, "b": b, "n_q": n_q,
                               "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring, "p2p_rel_err": e_p2p,
-                              "ranks_agree": same, "ok": good}), flush=True)
+                              "ranks_agree": same, "graph_equals_stream": same_graph, "ok": good}), flush=True)
     # generation loop: append tokens to rank p-1's shard, decode the grown cache
     b, n_q, n_kv, d, n0, steps = 1, 8, 2, 128, 4096 * world + 5, 40
     seed = orc.mix64(7, n0)
