@@ -120,12 +120,13 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(workload, algo, n):
-    """dram bytes per K1 launch from the committed ncu summary, if any."""
+def load_traffic(workload, algo, shard_tokens):
+    """dram bytes per K1 launch from the committed ncu summary (keyed by the
+    shard's tokens per (batch, kv-head) row), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s.get(f"{workload}/{algo}/p{n}", {}).get("dram_bytes_per_launch")
+        return s.get(f"{workload}/{algo}/t{shard_tokens}", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -583,7 +584,7 @@ def main():
             "hbm_gbs_step": kv_per_rank / (ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": load_traffic(args.workload, args.algo, world),
+                         "traffic": load_traffic(args.workload, args.algo, math.ceil(n / world)),
                          "kernel": {1: "k1_bf16 (split-KV, TMA + mma.sync)", 2: "k1_f32 (split-KV, bulk copy)",
                                     0: "k1_generic"}.get(split_kernel), "kernel_ms": k1_ms_max,
                          "bytes_per_launch": kv_per_rank, "peak_kind": peak_kind,

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise ncu captures (run here, on reports fetched from the GPU box).
 
-  python scripts/ncu_summary.py --rep gpurun_out/prof.ncu-rep --key cfg3/tree/p1 \
+  python scripts/ncu_summary.py --rep gpurun_out/prof.ncu-rep --key cfg3/tree/t1048576 \
       --launches gpurun_out/launches.csv --out profiles/r1_ncu_cfg3_p1.md
 
 Writes a markdown summary (per-kernel duration, DRAM bytes, throughput,
@@ -43,7 +43,7 @@ def raw(rep):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", required=True)
-    ap.add_argument("--key", required=True, help="workload/algo/pN, e.g. cfg3/tree/p1")
+    ap.add_argument("--key", required=True, help="workload/algo/t<shard tokens>, e.g. cfg3/tree/t1048576 (bench.py looks traffic up by it)")
     ap.add_argument("--launches", default=None)
     ap.add_argument("--out", required=True)
     ap.add_argument("--note", default="")
