@@ -696,11 +696,16 @@ float* mapped_host(td_context* ctx, float* host) {
 // error, after which the exchange must be re-opened on every rank
 // (td_p2p_handle / td_p2p_open) so that the epochs agree again.
 int exchange_failed(td_context* ctx) {
-    if (!ctx->x_err || !*reinterpret_cast<volatile int*>(ctx->x_err)) return TD_OK;
+    if (!ctx->x_err) return TD_OK;
+    const int v = *reinterpret_cast<volatile int*>(ctx->x_err);
+    if (!v) return TD_OK;
     *reinterpret_cast<volatile int*>(ctx->x_err) = 0;
     ctx->x_ready = false;
-    return set_err(TD_ECUDA, "tree_decode: NVLink exchange timed out (a peer never delivered its partial); "
-                             "re-open the exchange with td_p2p_handle / td_p2p_open");
+    const int miss = (v >> 8) & 255;
+    return set_err(TD_ECUDA, "tree_decode: NVLink exchange timed out on rank " + std::to_string(ctx->rank) +
+                                 " (epoch " + std::to_string(ctx->x_epoch) + ", first missing source " +
+                                 (miss == 255 ? std::string("beyond the batched peers") : std::to_string(miss)) +
+                                 "); re-open the exchange with td_p2p_handle / td_p2p_open");
 }
 
 // The NCCL combine's buffers [lse rows | shift rows | n rows*d, d rows] inside a
@@ -1411,14 +1416,16 @@ int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int fl
 }
 
 // K1 + K2x: split-KV partial, then one exchange + exact combine into xdst
-// (device memory or a mapped host buffer); no synchronisation.
-int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xdst, int flags) {
+// (device memory or a mapped host buffer); no synchronisation. parts = 1 launches
+// K1 only, 2 the exchange kernel only (with the same arguments), 3 both.
+int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xdst, int flags, int parts = 3) {
     const SplitPlan& plan = tc.plan;
     const int64_t d = ctx->d;
     if (!ctx->x_ready) return set_err(TD_ESTATE, "tree_decode: TD_P2P without td_p2p_open");
     if (tc.rows > ctx->x_max_rows || d != ctx->x_d)
         return set_err(TD_EINVAL, "tree_decode: exchange buffer too small for b * n_q rows");
-    if (int rc = exchange_failed(ctx)) return rc;  // an earlier asynchronous step timed out
+    if (parts & 1)
+        if (int rc = exchange_failed(ctx)) return rc;  // an earlier asynchronous step timed out
     td::XchgArgs xa;
     xa.peers = static_cast<float* const*>(ctx->x_ptrs.p);
     xa.p = ctx->nranks;
@@ -1440,8 +1447,9 @@ int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xd
         e1 = (*ctx->cur_phase)[ctx->cur_mark++];
     }
     TD_CUDA(td::launch_decode_exchange(plan, tc.qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
-                                       ctx->ws.p, xa, xdst, ctx->stream, e0, e1));
-    launched(ctx, plan);
+                                       ctx->ws.p, xa, xdst, ctx->stream, e0, e1, parts));
+    if (parts & 1) launched(ctx, plan);
+    if (!(parts & 2)) return TD_OK;  // the exchange kernel follows (group, shared GPU)
     ctx->x_epoch = xa.epoch;
     ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
     phase_mark(ctx);
@@ -1918,6 +1926,8 @@ struct td_group {
     std::vector<td_context*> w;
     std::vector<int> dev;
     cudaEvent_t entry = nullptr;  // on worker 0's device: start of a call (orders the others after it)
+    bool shared = false;          // some GPU hosts several workers
+    std::vector<cudaEvent_t> k1_done;  // per worker (its device): K1 of the current call finished
 };
 
 extern "C" {
@@ -1964,12 +1974,24 @@ int td_group_create(int ndev, const int* devs, int workers, td_group** out) {
     cudaSetDevice(g->dev[0]);
     if (cudaEventCreateWithFlags(&g->entry, cudaEventDisableTiming) != cudaSuccess)
         return fail(set_err(TD_ECUDA, "td_group_create: event"));
+    for (int w = 0; w < workers; ++w) {
+        g->shared = g->shared || g->w[size_t(w)]->shared_device;
+        cudaSetDevice(g->dev[size_t(w)]);
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return fail(set_err(TD_ECUDA, "td_group_create: event"));
+        g->k1_done.push_back(e);
+    }
     *out = g;
     return TD_OK;
 }
 
 int td_group_destroy(td_group* g) {
     if (!g) return TD_OK;
+    for (size_t w = 0; w < g->k1_done.size(); ++w) {
+        cudaSetDevice(g->dev[w]);
+        cudaEventDestroy(g->k1_done[w]);
+    }
     for (td_context* ctx : g->w) td_destroy(ctx);
     if (g->entry) {
         cudaSetDevice(g->dev[0]);
@@ -2049,11 +2071,33 @@ int td_group_tree_decode(td_group* g, const void* q, int64_t n_q, double scale, 
         float* m = mapped_host(c0, out);
         dst0 = m ? m : c0->out;
     }
-    for (int w = 0; w < p; ++w) {
-        td_context* ctx = g->w[size_t(w)];
-        require_ctx(ctx);
-        if (int rc = launch_tree_p2p(ctx, tc[size_t(w)], scale, w == 0 ? dst0 : ctx->out, flags)) return rc;
-        if (int rc = note_table_use(ctx)) return rc;
+    if (g->shared) {
+        // Workers sharing a GPU: every worker's K1 first, then the exchange kernels,
+        // each ordered after ALL the K1s. Exchange warps spin until their peers'
+        // words arrive; resident before a peer's K1 has run, they could hold the
+        // registers that K1's CTAs need and starve it (a deadlock the ~2 s timeout
+        // ended: tests/cpp/shim_parity.cpp at p = 16 workers on one GPU).
+        for (int w = 0; w < p; ++w) {
+            td_context* ctx = g->w[size_t(w)];
+            require_ctx(ctx);
+            if (int rc = launch_tree_p2p(ctx, tc[size_t(w)], scale, w == 0 ? dst0 : ctx->out, flags, 1)) return rc;
+            TD_CUDA(cudaEventRecord(g->k1_done[size_t(w)], ctx->stream));
+        }
+        for (int w = 0; w < p; ++w) {
+            td_context* ctx = g->w[size_t(w)];
+            require_ctx(ctx);
+            for (int v = 0; v < p; ++v)
+                if (v != w) TD_CUDA(cudaStreamWaitEvent(ctx->stream, g->k1_done[size_t(v)], 0));
+            if (int rc = launch_tree_p2p(ctx, tc[size_t(w)], scale, w == 0 ? dst0 : ctx->out, flags, 2)) return rc;
+            if (int rc = note_table_use(ctx)) return rc;
+        }
+    } else {
+        for (int w = 0; w < p; ++w) {
+            td_context* ctx = g->w[size_t(w)];
+            require_ctx(ctx);
+            if (int rc = launch_tree_p2p(ctx, tc[size_t(w)], scale, w == 0 ? dst0 : ctx->out, flags)) return rc;
+            if (int rc = note_table_use(ctx)) return rc;
+        }
     }
     if (!host) return TD_OK;
     require_ctx(c0);

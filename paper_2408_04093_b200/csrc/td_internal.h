@@ -134,11 +134,12 @@ struct XchgArgs {
 constexpr int kXchgBlocks = 1024;  // upper bound on K2x blocks
 
 // K1 + exchange tail: split-KV partial, merge, one-shot exchange and exact combine;
-// out [b, n_q, d] fp32 final (identical on every rank).
+// out [b, n_q, d] fp32 final (identical on every rank). parts: 1 = K1 only, 2 = K2x
+// only (same arguments, e.g. after a cross-stream wait), 3 = both.
 cudaError_t launch_decode_exchange(const SplitPlan& plan, const void* q, const void* k, const void* v,
                                    float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
                                    void* workspace, const XchgArgs& xa, float* out, cudaStream_t stream,
-                                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+                                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr, int parts = 3);
 
 // CUDA-graph replay of a captured step: the split kernel's entry point for `plan`
 // (to find its node) and an update of that node's per-launch state -- the SM

@@ -1681,7 +1681,12 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
             }
             if (__all_sync(0xffffffffu, all)) break;
             if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
-                *reinterpret_cast<volatile int*>(x.error) = 1;  // mapped host memory: a plain store
+                // mapped host memory, a plain store: 1 | first missing source << 8 | rank << 16
+                int miss = 255;
+#pragma unroll
+                for (int k = PMAX - 1; k >= 0; --k)
+                    if (k < x.p && wl[k].y != x.epoch) miss = k;
+                *reinterpret_cast<volatile int*>(x.error) = 1 | (miss << 8) | (x.rank << 16);
                 break;
             }
         }
@@ -2366,7 +2371,7 @@ cudaError_t launch_decode_final(const SplitPlan& p, const void* q, const void* k
 cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void* k, const void* v,
                                    float scale, const CUtensorMap* tmk, const CUtensorMap* tmv,
                                    void* ws, const XchgArgs& xa, float* out, cudaStream_t st,
-                                   cudaEvent_t ev0, cudaEvent_t ev1) {
+                                   cudaEvent_t ev0, cudaEvent_t ev1, int parts) {
     K1Args a = make_args(p, q, k, v, scale, ws);
     a.tail.mode = kTailExchange;
     a.tail.out = out;
@@ -2377,9 +2382,11 @@ cudaError_t launch_decode_exchange(const SplitPlan& p, const void* q, const void
     a.tail.x.max_rows = xa.max_rows;
     a.tail.x.error = xa.error;
     a.tail.x.pull = xa.pull;
-    cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
-    if (e != cudaSuccess) return e;
-    return launch_k2(a, xa.max_blocks, true, st);
+    if (parts & 1) {
+        cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
+        if (e != cudaSuccess) return e;
+    }
+    return (parts & 2) ? launch_k2(a, xa.max_blocks, true, st) : cudaSuccess;
 }
 
 namespace {

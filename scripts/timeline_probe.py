@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--isolated", action="store_true", help="synchronise after every step (a cold call each time)")
     ap.add_argument("--dynamic", action="store_true", help="TD_DYNAMIC: the dynamic tile pool")
     ap.add_argument("--f32", action="store_true", help="fp32 cache and query (the cfg1 kernel)")
+    ap.add_argument("--reserve", type=int, default=0, help="reserve this many extra tokens per row first")
+    ap.add_argument("--distinct", action="store_true", help="with --append: a different token every step")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -51,16 +53,29 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if args.reserve:
+        w.reserve_kv(args.reserve)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
+        torch.cuda.synchronize()
     if args.append:
         w.reserve_kv(args.steps + 8)
         tok = td.seeded_tensor([args.b, args.nkv, 128], 9, 1.0, td.DType.Bf16)
+        toks = td.seeded_tensor([args.steps, args.b, args.nkv, 128], 4, 1.0, td.DType.Bf16)
         torch.cuda.synchronize()
-    for _ in range(args.steps):
+    import time
+    t_host = time.perf_counter()
+    for i in range(args.steps):
         if args.append:
-            w.append_kv(tok, tok)
+            if args.distinct:
+                w.append_kv(toks[i], toks[i])
+            else:
+                w.append_kv(tok, tok)
         w.tree_decode_async(q.data_ptr(), args.nq, out.data_ptr(), 1.0, flags)
         if args.isolated:
             w._sync_worker()
+    host_us = (time.perf_counter() - t_host) / args.steps * 1e6
     torch.cuda.synchronize()
     st = w.debug_stamps(6144)
     rows = [st[5000 + 4 * i: 5004 + 4 * i] for i in range(3, 3 + args.steps)]
@@ -71,7 +86,7 @@ def main():
     waits = [round(tl[i + 1][1] - tl[i][3], 2) for i in range(len(tl) - 1)]
     steps = [round(tl[i + 1][1] - tl[i][1], 2) for i in range(len(tl) - 1)]
     print(json.dumps({"rank": local, "world": world, "seq_len": args.seq_len, "pdl": os.environ.get("TD_K1_PDL", "1"),
-                      "isolated": args.isolated,
+                      "isolated": args.isolated, "host_us_per_step": round(host_us, 2),
                       "k1_first_start_to_first_past_wait": [round(r[1] - r[0], 2) for r in tl],
                       "abs_k1_start_us": [round(r[0] / 1000.0, 2) for r in rows],
                       "abs_k1_end_us": [round(r[2] / 1000.0, 2) for r in rows],

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 using namespace treedec;
 
@@ -35,6 +36,7 @@ void expect(bool ok, const char* what, double err, double tol) {
 
 int main() {
     char what[256];
+    const bool verbose = std::getenv("SHIM_VERBOSE") != nullptr;
     // exactness grid: f32 / bf16 grids, heads {1, 16}, d_h {8, 128}
     for (const DType dt : {DType::Float32, DType::Bf16})
         for (const std::int64_t n : {17LL, 64LL, 1024LL, 5000LL})
@@ -54,6 +56,9 @@ int main() {
                              {ReduceStrategy::TreeBinary, ReduceStrategy::Ring, ReduceStrategy::Hierarchical}) {
                             const DecodeResult want = tree_decode(q64, cache64, topo, st);
                             const DecodeResult ref = tree_decode(q, cache, topo, st);
+                            if (verbose)
+                                std::fprintf(stderr, "case tree dt=%s n=%lld h=%lld d=%lld p=%d st=%s\n", dtype_name(dt),
+                                             (long long)n, (long long)n_h, (long long)d_h, p, strategy_name(st));
                             const DecodeResult got = gpu::tree_decode(q, cache, topo, st);
                             const double tol = decode_tolerance_abs(dt, max_abs(want.output));
                             const double err = max_abs_diff(got.output, want.output);
