@@ -67,7 +67,10 @@ def main():
     q = td.seeded_tensor([b, n_q, d], 1, 1.0, td.DType.Bf16)
     out = torch.empty(b, n_q, d, device="cuda")
     stream = torch.cuda.ExternalStream(w.stream)
-    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # L2 flush between steps of small shards: a read-only 256 MB sweep (a write flush
+    # would leave dirty lines whose write-back lands in the timed step)
+    scratch = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
     rows, lines = [], []
     for n in [int(x) for x in args.seq.split(",")]:
         if n < world:
@@ -94,7 +97,7 @@ def main():
             for i in range(steps):
                 if flush:
                     with torch.cuda.stream(stream):
-                        scratch.fill_(i & 255)
+                        torch.sum(scratch, dim=0, out=sink)
                 evs[i][0].record(stream)
                 fn(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags)
                 evs[i][1].record(stream)
