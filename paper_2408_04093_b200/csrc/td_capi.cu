@@ -535,8 +535,12 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
              bool generic_only = false) {
     std::string msg;
     if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
+    // deterministic calls: the static split plus, unless TD_DPOOL=0, the deterministic
+    // chunk pool; TD_DYNAMIC calls: the run-time home pool
+    static const bool dpool = [] { const char* e = std::getenv("TD_DPOOL"); return !e || std::atoi(e) != 0; }();
+    const int mode = ctx->det ? (dpool ? 2 : 0) : 1;
     if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), t,
-                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg, !ctx->det, generic_only))
+                        static_cast<int>(ctx->d), ctx->sm_count, plan, msg, mode, generic_only))
         return set_err(TD_EINVAL, msg);
     plan.row_stride = stride;
     plan.t_safe = stride > 0 ? std::min(ctx->kv_safe, t) : 0;  // the context's own cache only
@@ -782,7 +786,7 @@ int td_decode_workspace_bytes(int dtype, int64_t b, int64_t n_q, int64_t n_kv, i
     int dev = 0;
     cudaGetDevice(&dev);
     if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
-                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0))
+                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0 ? 1 : 0))
         return set_err(TD_EINVAL, msg);
     // + the pool counters, carved from the end of the caller's workspace
     *bytes = (plan.workspace_bytes() + 255) / 256 * 256 + plan.counters_bytes();
@@ -803,7 +807,7 @@ int td_decode_partial(int dtype, const void* q, const void* k, const void* v, in
     int dev = 0;
     cudaGetDevice(&dev);
     if (!td::plan_split(dtype, b, static_cast<int>(n_q), static_cast<int>(n_kv), t,
-                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0))
+                        static_cast<int>(d), sm_count_of(dev), plan, msg, g_deterministic == 0 ? 1 : 0))
         return set_err(TD_EINVAL, msg);
     const size_t ctr_off = (plan.workspace_bytes() + 255) / 256 * 256;
     if (workspace_bytes < ctr_off + plan.counters_bytes())

@@ -45,6 +45,11 @@ struct SplitPlan {
     // any row's pool and fold them into one of that row's fslots foreign states
     // ([bh_count][fslots]; 0 = off)
     int fslots = 0;
+    // deterministic chunk pool (pool mode 2): every pool chunk k of row bh is its own
+    // state, fslot (bh, k) with fslots = chunks per row; any warp of the grid claims
+    // chunks from one queue (pool counter [0]), and since a chunk's state does not
+    // depend on who computes it, results stay bitwise reproducible
+    bool dpool = false;
     // tokens of every row that no kernel ahead of this launch on the stream may
     // still be writing (0: none). k1_bf16 loads its first tiles below it before
     // griddepcontrol.wait. Set only for the context's own cache (td_capi.cu
@@ -93,10 +98,12 @@ cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
 
 // Chooses the kernel and grid for a shard. Returns false (with msg) when the
 // shape is unsupported.
-// allow_pool = false gives a static split: bitwise-reproducible results.
-// generic_only forces k1_generic (needed for an energy source term).
+// pool_mode: 0 static split; 1 the dynamic home pool (+ stealing on long shards),
+// results agree to ~1e-7 between calls; 2 the deterministic chunk pool (bitwise
+// reproducible, see SplitPlan::dpool). generic_only forces k1_generic (needed for
+// an energy source term).
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& plan, std::string& msg, bool allow_pool = true, bool generic_only = false);
+                SplitPlan& plan, std::string& msg, int pool_mode = 1, bool generic_only = false);
 
 // Static partition proportional to per-CTA speeds (weights[c] > 0, size
 // plan.ctas): x[c] = first static tile of CTA c (x has ctas + 1 entries),

@@ -92,6 +92,7 @@ struct K1Args {
     // cross-row stealing (SplitPlan::fslots): foreign states [bh][fslots][group]
     // (+ [..][d]); fcnt[bh] counts the claimed ones (this parity), fcnt_next is zeroed by K2
     int fslots;
+    int dpool;                   // SplitPlan::dpool: fslots are the pool's chunk states
     int steal_scans, steal_min;  // scans per warp; least chunks left worth a visit
     unsigned* fcnt;
     unsigned* fcnt_next;
@@ -364,13 +365,19 @@ __global__ void __launch_bounds__(W * 32, 1)
     const int64_t last_static = x1 > x0 + warp ? x0 + warp + ((x1 - 1 - x0 - warp) / W) * W : -1;
     const int64_t cb_start = last_static >= 0 ? last_static / A : cb_hi;  // stay on the current bh first
     int64_t p_bh = -1, p_pos = 0, p_end = 0, p_tries = 0;
-    bool p_done = nch == 0 || ncb <= 0;
+    bool p_done = nch == 0 || ncb <= 0 || a.dpool;
+    // deterministic chunk pool: after its static tiles a warp takes whole chunks
+    // from one grid-wide queue (chunk-major over the rows); a chunk is its own
+    // state (fslot (bh, k)), so who computes it does not change the result
+    int64_t d_bh = -1, d_pos = 0, d_end = 0;
+    int d_k = 0;
+    bool d_on = a.dpool && nch > 0;
     // cross-row stealing, once the own rows' pools are empty: the row whose pool
     // has the most chunks left (one coalesced read of the counters), one claimed
     // foreign state per visit; a claimed state that gets no chunk is written empty
     int64_t f_bh = -1, f_pos = 0, f_end = 0;
     int f_slot = 0, f_scans = 0;
-    bool f_got = false, f_on = a.fslots > 0 && nch > 0;
+    bool f_got = false, f_on = a.fslots > 0 && nch > 0 && !a.dpool;
     uint64_t f_full = 0;  // rows whose foreign states ran out (first 64 rows)
     auto empty_foreign = [&](int64_t bh, int slot) {
         const int64_t fs = (bh * a.fslots + slot) * a.group;
@@ -475,6 +482,25 @@ __global__ void __launch_bounds__(W * 32, 1)
             f_bh = best;
             f_slot = static_cast<int>(fidx);
             f_got = false;
+        }
+        while (d_on) {
+            if (d_pos < d_end) {
+                bh = d_bh;
+                tb = d_pos++;
+                rec = 2 + d_k;
+                return true;
+            }
+            unsigned j = 0;
+            if (lane == 0) j = atomicAdd(a.pool_ctr, 1u);
+            j = __shfl_sync(0xffffffffu, j, 0);
+            if (int64_t(j) >= nch * a.bh_count) {
+                d_on = false;
+                break;
+            }
+            d_k = static_cast<int>(div_nn(j, a.bh_count));
+            d_bh = int64_t(j) - int64_t(d_k) * a.bh_count;
+            d_pos = a.pool_first + int64_t(d_k) * a.pool_chunk;
+            d_end = min(d_pos + a.pool_chunk, a.pool_first + a.pool_tiles);
         }
         return false;
     };
@@ -1115,6 +1141,7 @@ struct Cover {
 };
 // The foreign states K1 claimed for bh (read after griddepcontrol.wait).
 __device__ __forceinline__ int foreign_of(const K1Args& a, int64_t bh) {
+    if (a.dpool) return a.fslots;  // every chunk of the deterministic pool has its state
     if (a.fslots <= 0 || !a.fcnt) return 0;
     const unsigned n = __ldcg(a.fcnt + bh);
     return static_cast<int>(n < unsigned(a.fslots) ? n : unsigned(a.fslots));
@@ -1740,6 +1767,181 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
     signal_done(a);
 }
 
+// K2x for rows with many candidate states (the deterministic chunk pool, or few
+// rows over many CTAs): the split merge of k2_combine_split per (row, column
+// quarter) block, then warp 0 pushes the row's LL words into every peer and,
+// after all of this block's units are pushed, polls and combines them like
+// k2_exchange (one column per lane).
+template <int Q, int WS>
+__global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    constexpr int PMAX = 8;
+    __shared__ float sm_m[WS], sm_l[WS], sm_o[WS][32];
+    const int64_t rows = a.bh_count * a.group, units = rows * Q;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Xchg& x = a.tail.x;
+    uint2* pp[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) pp[k] = k < x.p ? reinterpret_cast<uint2* const*>(x.peers)[k] : nullptr;
+    const uint2* own = reinterpret_cast<uint2* const*>(x.peers)[x.rank];
+    uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
+    const Cover cv0 = blockIdx.x < units ? cover_of(a, (int64_t(blockIdx.x) / Q) / a.group) : Cover{};
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pool_tiles > 0)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
+             i += int64_t(gridDim.x) * blockDim.x) {
+            a.pool_next[i] = 0u;
+            if (a.fcnt_next) a.fcnt_next[i] = 0u;
+        }
+    const int D = a.d, g = a.group, st = a.maxseg * g;
+    const unsigned par = x.epoch & 1u;
+    const int64_t stride = x.max_rows * int64_t(D + 1);
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {  // merge + push
+        const int64_t r = u / Q;
+        const int col = static_cast<int>(u % Q) * 32 + lane;
+        const int h = static_cast<int>(r % g);
+        Cover cv = u == blockIdx.x ? cv0 : cover_of(a, r / g);
+        cv.nf = foreign_of(a, r / g);
+        const int S = cv.S, T = cv.S + cv.nf;
+        const int b0 = static_cast<int>((cv.c_lo * a.maxseg + cv.seg_lo) * g + h);
+        const int b1 = static_cast<int>((cv.c_lo + 1) * a.maxseg * g + h);
+        const int fb = static_cast<int>((r / g) * a.fslots * g + h);
+        auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
+        const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
+        float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
+        for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+            const int n = min(32, i_hi - i0);
+            float ml = -CUDART_INF_F, ll = 0.f;
+            if (lane < n) {
+                const int i = i0 + lane, off = off_of(i);
+                ml = __ldcg((i >= S ? a.fslot_m : a.cslot_m) + off);
+                ll = __ldcg((i >= S ? a.fslot_l : a.cslot_l) + off);
+            }
+            float ov[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int i = i0 + min(k, n - 1);
+                ov[k] = col < D ? __ldcg((i >= S ? a.fslot_o : a.cslot_o) + int64_t(off_of(i)) * D + col) : 0.f;
+            }
+            float Mb = ml;
+#pragma unroll
+            for (int o2 = 16; o2 >= 1; o2 >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, o2));
+            const float Mn = fmaxf(M, Mb);
+            const float cs = M == -CUDART_INF_F ? 0.f : fast_exp2(M - Mn);
+            L *= cs;
+            acc *= cs;
+            const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - Mn);
+            float ls = e_l * ll;
+#pragma unroll
+            for (int o2 = 16; o2 >= 1; o2 >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o2);
+            L += ls;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const float e = __shfl_sync(0xffffffffu, e_l, k);
+                acc = fmaf(e, e != 0.f ? ov[k] : 0.f, acc);
+            }
+            M = Mn;
+        }
+        if (lane == 0) {
+            sm_m[warp] = M;
+            sm_l[warp] = L;
+        }
+        sm_o[warp][lane] = acc;
+        __syncthreads();
+        if (warp == 0) {
+            float Mx = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < WS; ++w) Mx = fmaxf(Mx, sm_m[w]);
+            float Lt = 0.f, O = 0.f;
+#pragma unroll
+            for (int w = 0; w < WS; ++w) {
+                const float mw = sm_m[w];
+                const float e = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - Mx);
+                Lt += e * sm_l[w];
+                O += e != 0.f ? e * sm_o[w][lane] : 0.f;
+            }
+            const bool empty = Mx == -CUDART_INF_F;
+            const float val = empty ? 0.f : O / Lt;
+            const float lse = empty ? -CUDART_INF_F : (Mx + log2f(Lt)) * kLn2;
+            const int64_t orow = out_row_of(a, r);
+            const int64_t off = (int64_t(par) * x.p + x.rank) * stride + orow * (D + 1);
+            auto push = [&](uint2* dst) {
+                if (col < D) st_ll(dst + col, val, x.epoch);
+                if (lane == 0 && col == 0) st_ll(dst + D, lse, x.epoch);
+            };
+            if (x.pull) {
+                push(peers[x.rank] + off);
+            } else {
+#pragma unroll
+                for (int q = 0; q < PMAX; ++q)
+                    if (q < x.p) push(pp[q] + off);
+                for (int q = PMAX; q < x.p; ++q) push(peers[q] + off);
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {  // exact combine of the p partials
+            const int64_t r = u / Q;
+            const int col = static_cast<int>(u % Q) * 32 + lane;
+            const int64_t orow = out_row_of(a, r);
+            const int64_t roff = int64_t(par) * x.p * stride + orow * (D + 1);
+            const uint2* base = own + roff;
+            uint2 wl[PMAX], wo[PMAX];
+            const long long t0 = clock64();
+            for (;;) {
+                bool all = true;
+#pragma unroll
+                for (int k = 0; k < PMAX; ++k) {
+                    if (k >= x.p) continue;
+                    const uint2* slot = (x.pull ? pp[k] + roff : base) + k * stride;
+                    wl[k] = ld_word(slot + D);
+                    if (col < D) wo[k] = ld_word(slot + col);
+                }
+#pragma unroll
+                for (int k = 0; k < PMAX; ++k) {
+                    if (k >= x.p) continue;
+                    all &= wl[k].y == x.epoch;
+                    if (col < D) all &= wo[k].y == x.epoch;
+                }
+                if (__all_sync(0xffffffffu, all)) break;
+                if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a peer never arrived
+                    int miss = 255;
+#pragma unroll
+                    for (int k = PMAX - 1; k >= 0; --k)
+                        if (k < x.p && wl[k].y != x.epoch) miss = k;
+                    *reinterpret_cast<volatile int*>(x.error) = 1 | (miss << 8) | (x.rank << 16);
+                    break;
+                }
+            }
+            float shift = -CUDART_INF_F, den = 0.f, num = 0.f;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k)
+                if (k < x.p) shift = fmaxf(shift, __uint_as_float(wl[k].x));
+            for (int q = PMAX; q < x.p; ++q)
+                shift = fmaxf(shift, ld_ll((x.pull ? peers[q] + roff : base) + q * stride + D, x.epoch, x.error));
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                const float l = __uint_as_float(wl[k].x);
+                const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - shift);
+                den += wgt;
+                if (col < D) num += wgt * __uint_as_float(wo[k].x);
+            }
+            for (int q = PMAX; q < x.p; ++q) {
+                const uint2* slot = (x.pull ? peers[q] + roff : base) + q * stride;
+                const float l = ld_ll(slot + D, x.epoch, x.error);
+                const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - shift);
+                den += wgt;
+                if (col < D) num += wgt * ld_ll(slot + col, x.epoch, x.error);
+            }
+            if (col < D) a.tail.out[orow * D + col] = num / den;
+        }
+    }
+    if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
+    signal_done(a);
+}
+
 // =========================================================================
 // K3 / K4 / K5 / combine_partials / K6
 // =========================================================================
@@ -1917,6 +2119,7 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
         a.fcnt = cnt + (2 + p.parity) * p.bh_count;
         a.fcnt_next = cnt + (3 - p.parity) * p.bh_count;
         a.fslots = p.fslots;
+        a.dpool = p.dpool ? 1 : 0;
         static const int scans = [] { const char* e = std::getenv("TD_STEAL_SCANS"); return e ? std::atoi(e) : 2; }();
         static const int smin = [] { const char* e = std::getenv("TD_STEAL_MIN"); return e ? std::atoi(e) : 4; }();
         a.steal_scans = scans;
@@ -1976,7 +2179,7 @@ cudaError_t launch_stamp(unsigned long long* p, cudaStream_t st) {
 }
 
 bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int sm_count,
-                SplitPlan& p, std::string& msg, bool allow_pool, bool generic_only) {
+                SplitPlan& p, std::string& msg, int pool_mode, bool generic_only) {
     if (b < 1 || n_q < 1 || n_kv < 1 || d < 1 || t < 0) {
         msg = "decode: dimensions must be positive";
         return false;
@@ -2029,12 +2232,38 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
         const char* e = std::getenv("TD_POOL_CHUNK");
         return e ? std::max(1, std::atoi(e)) : 2;
     }();
+    // Deterministic chunk pool: the last dpool_frac of every row (at most
+    // dpool_maxch chunks of dpool_chunk tiles), each chunk its own merge candidate.
+    // 64 x 5 tiles measured best at 131K among 32x6..192x2 (profiles/r2_balance_131k/)
+    static const double dpool_frac = [] {
+        const char* e = std::getenv("TD_DPOOL_FRAC");
+        return e ? std::atof(e) : 0.08;
+    }();
+    static const int dpool_chunk = [] {
+        const char* e = std::getenv("TD_DPOOL_CHUNK");
+        return e ? std::max(1, std::atoi(e)) : 5;
+    }();
+    static const int dpool_maxch = [] {
+        const char* e = std::getenv("TD_DPOOL_MAXCH");
+        return e ? std::max(1, std::atoi(e)) : 64;
+    }();
     int64_t pool = 0;
-    if (allow_pool && p.kernel == 1 && p.full_tiles_per_bh >= 16 && pool_frac > 0.0)
+    // only where the merge stays one K2 block per (row, column quarter): the chunk
+    // states multiply every row's merge candidates
+    const bool dpool = pool_mode == 2 && p.kernel == 1 && p.full_tiles_per_bh >= 32 && dpool_frac > 0.0 &&
+                       b * int64_t(n_q) * 4 <= sm_count;
+    if (pool_mode == 1 && p.kernel == 1 && p.full_tiles_per_bh >= 16 && pool_frac > 0.0)
         pool = std::min<int64_t>(p.full_tiles_per_bh / 2, static_cast<int64_t>(p.full_tiles_per_bh * pool_frac));
+    int chunk = pool_chunk;
+    if (dpool) {  // at most dpool_maxch chunk states per row (one round trip of the split K2)
+        pool = std::min<int64_t>(p.full_tiles_per_bh / 2, static_cast<int64_t>(p.full_tiles_per_bh * dpool_frac));
+        chunk = dpool_chunk;
+        pool = std::min<int64_t>(pool, int64_t(dpool_maxch) * chunk);
+    }
+    p.dpool = dpool && pool > 0;
     p.pool_tiles = pool;
     p.pool_first = p.full_tiles_per_bh - pool;
-    p.pool_chunk = pool_chunk;
+    p.pool_chunk = chunk;
     // cross-row stealing pays on long shards (measured: -2 % at 1M tokens and on
     // cfg4's 8.6 GB, +1-2 % at 131K, where the scans and the extra merge
     // candidates cost more than the imbalance they remove): on when a CTA
@@ -2046,6 +2275,7 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     const int64_t tiles_per_cta = sm_count > 0 ? p.bh_count * p.full_tiles_per_bh / sm_count : 0;
     const int fslots = fslots_env >= 0 ? fslots_env : (tiles_per_cta >= 1024 ? 16 : 0);
     p.fslots = pool > 0 ? fslots : 0;
+    if (p.dpool) p.fslots = static_cast<int>((pool + chunk - 1) / chunk);  // one state per chunk
     p.tiles_per_bh = p.full_tiles_per_bh - pool;
     p.total_tiles = p.bh_count * p.tiles_per_bh;
     // one CTA per SM (the per-warp pipelines fill shared memory); without a
@@ -2053,7 +2283,7 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
     int64_t ctas = sm_count;
     if (pool == 0 && p.total_tiles < ctas) ctas = p.total_tiles > 0 ? p.total_tiles : 1;
     p.ctas = static_cast<int>(ctas);
-    p.slot_warps = p.warps * (pool > 0 ? 2 : 1);
+    p.slot_warps = p.warps * (pool > 0 && !p.dpool ? 2 : 1);  // chunk states live in fslot
     const int64_t per_cta = (p.total_tiles + p.ctas - 1) / p.ctas;
     const int64_t tpb = p.tiles_per_bh > 0 ? p.tiles_per_bh : 1;
     p.maxseg = static_cast<int>((per_cta + tpb - 1) / tpb + 1);
@@ -2252,11 +2482,31 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
     static const int cols = [] { const char* e = std::getenv("TD_K2_COLS"); return e ? std::atoi(e) : 4; }();
     // few rows with many candidate states each (e.g. one row over every CTA): split
     // each (row, quarter)'s candidates over the warps of a block
-    const int64_t cands = a.bh_count > 0 ? int64_t(a.ctas) / a.bh_count + 2 : 0;  // CTAs covering a row
+    // CTAs covering a row, plus the chunk states of the deterministic pool
+    const int64_t cands = (a.bh_count > 0 ? int64_t(a.ctas) / a.bh_count + 2 : 0) + (a.dpool ? a.fslots : 0);
     static const int split = [] { const char* e = std::getenv("TD_K2_SPLIT"); return e ? std::atoi(e) : 1; }();
-    if (split && !exchange && a.d == 128 && force_w == 0 && rows * 4 <= limit && cands > 32 && !a.dbg) {
+    if (split && exchange && a.d == 128 && force_w == 0 && cands > 32 && !a.dbg) {
+        const int64_t units = rows * 4;
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(rows * 4));
+        cfg.gridDim = dim3(static_cast<unsigned>(units < limit ? units : limit));
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cands > 128) {
+            cfg.blockDim = dim3(32 * 8);
+            if (cudaError_t e = prefer_max_smem(k2_exchange_split<4, 8>)) return e;
+            return cudaLaunchKernelEx(&cfg, k2_exchange_split<4, 8>, a);
+        }
+        cfg.blockDim = dim3(32 * 4);
+        if (cudaError_t e = prefer_max_smem(k2_exchange_split<4, 4>)) return e;
+        return cudaLaunchKernelEx(&cfg, k2_exchange_split<4, 4>, a);
+    }
+    if (split && !exchange && a.d == 128 && force_w == 0 && cands > 32 && !a.dbg) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(rows * 4 < limit ? rows * 4 : limit));
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
