@@ -233,6 +233,7 @@ struct td_context {
     // (blocks land on the same SMs launch after launch), measured once
     std::vector<float> cal_w;
     bool cal_failed = false;
+    int64_t cal_bytes = 0;      // KV bytes of the shard the weights were measured on
     double cal_gain = 0.0;      // measured K1 gain of the weights over the equal split
     DevBuf sm_map, claims;      // SM affinity of the calibrated CTA indices
     bool sm_map_ok = false;
@@ -525,6 +526,7 @@ int calibrate(td_context* ctx, int64_t n_q) {
     tab.release();
     ctx->cal_gain = t_eq.empty() ? 0.0 : (t_eq[t_eq.size() / 2] - t_cal[t_cal.size() / 2]) / t_eq[t_eq.size() / 2];
     ctx->cal_w = ctx->cal_gain > 0.005 ? w : ones;  // equal weights: the affinity alone stays harmless
+    ctx->cal_bytes = 2 * ctx->b * ctx->n_kv * ctx->len * ctx->d * td::dtype_bytes(ctx->dtype);
     ctx->sm_map_ok = true;
     return TD_OK;
 }
@@ -549,6 +551,16 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
     plan.tl_cta = ctx->cur_tl_cta;
     plan.pdl = !ctx->shared_device;
     if (plan.kernel == 1 && calibration_enabled() && plan.total_tiles >= 8 * int64_t(plan.ctas)) {
+        // a shard more than 4x larger or smaller than the one the weights were measured
+        // on streams differently (ramp, L2): measure again (results change with the
+        // partition, which changed shape anyway)
+        const int64_t bytes = 2 * ctx->b * ctx->n_kv * t * ctx->d * td::dtype_bytes(ctx->dtype);
+        if (!ctx->cal_w.empty() && ctx->cal_bytes > 0 && (bytes > 4 * ctx->cal_bytes || 4 * bytes < ctx->cal_bytes)) {
+            ctx->cal_w.clear();
+            ctx->cal_failed = false;
+            ctx->sm_map_ok = false;
+            for (auto& tb : ctx->tabs) tb.total = -1;
+        }
         if (ctx->cal_w.size() != size_t(plan.ctas) && !ctx->cal_failed && ctx->kv_ok && !ctx->shared_device) {
             if (calibrate(ctx, n_q) != TD_OK) {
                 ctx->cal_failed = true;  // keep the equal split
