@@ -274,7 +274,7 @@ struct td_context {
         const void* x_table = nullptr;
         const void* k = nullptr;
         float* lse = nullptr;
-    } graph;
+    } graph[2];  // one per pool-counter parity (launches alternate them)
 
     DevBuf ctr;        // K1 dynamic-pool counters (SplitPlan::counters)
     int64_t ctr_bh = -1;
@@ -953,8 +953,10 @@ int td_destroy(td_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->xfer);
-    if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
-    if (ctx->graph.graph) cudaGraphDestroy(ctx->graph.graph);
+    for (auto& g : ctx->graph) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
     if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
     if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -1483,15 +1485,16 @@ bool graph_mode(td_context* ctx, const SplitPlan& plan, int flags) {
     static const bool env = [] { const char* e = std::getenv("TD_NCCL_GRAPH"); return e && std::atoi(e) != 0; }();
     if (!(env || (flags & TD_GRAPH))) return false;
     if (flags & (TD_HOST_IO | TD_TIME_KERNELS | TD_TIME_PHASES | TD_BF16_OUT | TD_DEBUG_TS)) return false;
-    return plan.pool_tiles == 0 && !plan.dbg && !plan.tl && ctx->comm;
+    return !plan.dbg && !plan.tl && ctx->comm;
 }
 
-// The NCCL tree step as a graph: captured on the first call of a shape (the
-// capture records the launches without running them), then launched; later calls
+// The NCCL tree step as a graph: captured on the first call of a shape and pool
+// parity (the capture records the launches without running them; launches with a
+// tile pool alternate two counter sets, hence two graphs), then launched; later calls
 // with the same shape, buffers and scale only patch K1's claim epoch and relaunch.
 int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, double scale, int64_t rows, float* lse,
                     float* shift, float* nd, float* out) {
-    auto& g = ctx->graph;
+    auto& g = ctx->graph[plan.pool_tiles > 0 ? plan.parity & 1 : 0];
     const int64_t d = ctx->d;
     const bool same = g.exec && g.q == qd && g.out == out && g.scale == scale && g.rows == rows &&
                       g.total == plan.total_tiles && g.per_bh == plan.tiles_per_bh && g.len == ctx->len &&
@@ -1499,6 +1502,7 @@ int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, doub
                       g.x_table == plan.x_table && g.k == ctx->k.p && g.lse == lse && g.t_safe == plan.t_safe;
     if (same) {
         TD_CUDA(td::graph_set_k1_epoch(g.exec, g.k1, plan));
+        launched(ctx, plan);  // (the capture path's run_partial does this)
     } else {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         if (g.graph) cudaGraphDestroy(g.graph);
