@@ -183,10 +183,15 @@ int td_kv_generate(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t 
  * section 8(f)2): the cache grows by one token that lands at the end of the
  * last shard (rank p-1). Every rank calls it (seq_len += 1 everywhere); only
  * rank p-1 reads k/v, one [b, n_kv, 1, d] token in the cache dtype (host or
- * device). Capacity grows geometrically (or to td_kv_reserve's size), so a
- * step costs two strided copies of b*n_kv*d elements. tree_decode is exact
- * under any partition (safe-softmax invariance), so the result equals the
- * reference's decode over the grown cache. */
+ * device). Capacity grows geometrically (or to td_kv_reserve's size).
+ * A host token is copied in by the call. A device token on a bf16 cache is
+ * fused: the next td_tree_decode's split kernel writes it into the cache while
+ * it streams (no append kernel on the step); any other use of the cache first
+ * writes it with an append kernel. The device buffers must therefore stay
+ * unchanged until the next call on this context that reads the cache has run
+ * on the context's stream (td_stream). TD_FUSED_APPEND=0 appends eagerly.
+ * tree_decode is exact under any partition (safe-softmax invariance), so the
+ * result equals the reference's decode over the grown cache. */
 int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host);
 /* Reserves room for `tokens` more appended tokens on rank p-1 (no-op elsewhere). */
 int td_kv_reserve(td_context* ctx, int64_t tokens);

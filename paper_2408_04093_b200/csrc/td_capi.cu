@@ -175,6 +175,12 @@ struct td_context {
     // cache after a synchronising placement, else the length the last decode's K1
     // saw (appends write past it); SplitPlan::t_safe
     int64_t kv_safe = 0;
+    // fused KV append: a device-source token appended since the last decode that the
+    // next bf16 split kernel writes into the cache itself (SplitPlan::app_*); any other
+    // reader of the cache flushes it first with the append kernel (flush_append)
+    const void* pend_k = nullptr;
+    const void* pend_v = nullptr;
+    int64_t pend_pos = -1;
     std::vector<int64_t> lens;  // every rank's shard length (chunk_extents, then appends on rank p-1)
     DevBuf k, v;
     CUtensorMap tmk{}, tmv{};
@@ -314,6 +320,19 @@ int ensure_rows(td_context* ctx, int64_t rows, int64_t d) {
     return TD_OK;
 }
 
+// The pending fused append as an append kernel, for every reader of the cache
+// other than the bf16 split kernel (and before the cache is reallocated).
+int flush_append(td_context* ctx) {
+    if (!ctx->pend_k) return TD_OK;
+    const void* k = ctx->pend_k;
+    const void* v = ctx->pend_v;
+    ctx->pend_k = ctx->pend_v = nullptr;
+    TD_CUDA(td::launch_kv_append(ctx->dtype, ctx->k.p, ctx->v.p, k, v, ctx->b * ctx->n_kv, ctx->cap, ctx->pend_pos,
+                                 static_cast<int>(ctx->d), ctx->stream));
+    ctx->pend_pos = -1;
+    return TD_OK;
+}
+
 bool calibration_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TD_CALIBRATE");
@@ -405,6 +424,7 @@ int ensure_rows(td_context* ctx, int64_t rows, int64_t d);
 // launch in (e.g. early, under PDL). They only move work, never change what is
 // computed.
 int calibrate(td_context* ctx, int64_t n_q) {
+    if (int rc = flush_append(ctx)) return rc;  // the calibration launches read the whole cache
     SplitPlan p;
     std::string msg;
     if (!td::plan_split(ctx->dtype, ctx->b, static_cast<int>(n_q), static_cast<int>(ctx->n_kv), ctx->len,
@@ -534,7 +554,7 @@ int calibrate(td_context* ctx, int64_t n_q) {
 // stride: tokens per bh row in memory (the placed shard's capacity; 0 for a
 // contiguous [bh][t][d] buffer such as a ring chunk)
 int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t stride,
-             bool generic_only = false) {
+             bool generic_only = false, bool take_append = false) {
     std::string msg;
     if (n_q < 1 || n_q > (1 << 20)) return set_err(TD_EINVAL, "decode: bad query head count");
     // deterministic calls: the static split plus, unless TD_DPOOL=0, the deterministic
@@ -590,6 +610,15 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
             }
         }
     }
+    if (ctx->pend_k) {  // the fused append rides on a bf16 split kernel over the own cache
+        if (take_append && plan.kernel == 1 && stride > 0 && ctx->tm_ok) {
+            plan.app_k = ctx->pend_k;
+            plan.app_v = ctx->pend_v;
+            plan.app_pos = ctx->pend_pos;
+        } else if (int rc = flush_append(ctx)) {
+            return rc;
+        }
+    }
     TD_CUDA(ctx->ws.ensure(plan.workspace_bytes()));
     if (plan.pool_tiles > 0) {
         // pool counters: zero at rest except the last launch's parity; a new
@@ -612,6 +641,12 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
 // launching leaves the parity alone, so the counters at rest stay zero.
 void launched(td_context* ctx, const SplitPlan& plan) {
     if (plan.pool_tiles > 0 && plan.counters == ctx->ctr.p) ctx->kpar = plan.parity ^ 1;
+    if (plan.app_k && plan.app_k == ctx->pend_k) {
+        // the token is in the cache once this split kernel has run; the next K1 must not
+        // load its tile before its own wait (the write is not visible to it earlier)
+        ctx->pend_k = ctx->pend_v = nullptr;
+        ctx->pend_pos = -1;
+    }
 }
 
 void phase_begin(td_context* ctx, int flags) {
@@ -672,7 +707,8 @@ int run_partial(td_context* ctx, const SplitPlan& plan, const void* q, const voi
     TD_CUDA(td::launch_decode_partial(plan, q, kb, vb, static_cast<float>(scale), pk, pv,
                                       ctx->ws.p, rmax, lse, out, ctx->stream, e0, e1));
     launched(ctx, plan);
-    if (kb == ctx->k.p && plan.row_stride > 0) ctx->kv_safe = t;  // later K1s run after this one's wait
+    if (kb == ctx->k.p && plan.row_stride > 0)  // later K1s run after this one's wait
+        ctx->kv_safe = plan.app_k ? std::min(t, plan.app_pos) : t;  // (a fused token: not before their own)
     ctx->last_kernels += 2;  // K1 + K2
     ctx->last_kv_bytes += 2.0 * double(ctx->b) * double(ctx->n_kv) * double(t) * double(ctx->d) *
                           td::dtype_bytes(ctx->dtype);
@@ -1137,6 +1173,8 @@ static int kv_alloc(td_context* ctx, int dtype, int64_t b, int64_t n_kv, int64_t
     ctx->kv_ok = false;
     ctx->tm_ok = false;
     ctx->kv_safe = 0;
+    ctx->pend_k = ctx->pend_v = nullptr;  // a new cache: a token appended to the old one is gone
+    ctx->pend_pos = -1;
     return TD_OK;
 }
 
@@ -1199,6 +1237,7 @@ static int kv_grow(td_context* ctx, int64_t cap) {
     const size_t row_old = size_t(ctx->cap) * size_t(ctx->d) * esz, row_new = size_t(cap) * size_t(ctx->d) * esz;
     const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
     if (int64_t(rows) * cap >= (int64_t(1) << 31)) return set_err(TD_EINVAL, "kv_append: shard too large for 32-bit TMA rows");
+    if (int rc = flush_append(ctx)) return rc;
     TD_CUDA(cudaStreamSynchronize(ctx->stream));
     // both new buffers first, so a failed allocation leaves the shard untouched
     void* fresh[2] = {nullptr, nullptr};
@@ -1240,6 +1279,18 @@ int td_kv_append(td_context* ctx, const void* k, const void* v, int from_host) {
     if (!k || !v) return set_err(TD_EINVAL, "kv_append: the last rank needs the token's k and v");
     if (ctx->len == ctx->cap)  // grows before any state changes: a failure leaves the cache as it was
         if (int rc = kv_grow(ctx, ctx->cap + std::max<int64_t>(1024, ctx->cap / 8))) return rc;
+    if (int rc = flush_append(ctx)) return rc;  // one pending token at a time
+    static const bool fuse = [] { const char* e = std::getenv("TD_FUSED_APPEND"); return !e || std::atoi(e) != 0; }();
+    if (!from_host && fuse && ctx->tm_ok) {
+        // device source, bf16 TMA cache: the next decode's split kernel writes it
+        ctx->pend_k = k;
+        ctx->pend_v = v;
+        ctx->pend_pos = ctx->len;
+        ctx->len += 1;
+        ctx->seq_len += 1;
+        ctx->lens.back() += 1;
+        return TD_OK;
+    }
     const size_t esz = td::dtype_bytes(ctx->dtype);
     const size_t tok = size_t(ctx->d) * esz, pitch = size_t(ctx->cap) * tok;
     const size_t rows = size_t(ctx->b) * size_t(ctx->n_kv);
@@ -1280,6 +1331,7 @@ int td_kv_info(td_context* ctx, int64_t* start, int64_t* len, size_t* bytes) {
 int td_kv_pointers(td_context* ctx, void** k, void** v) {
     if (int rc = require_ctx(ctx)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "no KV shard placed");
+    if (int rc = flush_append(ctx)) return rc;  // the caller reads the cache
     *k = ctx->k.p;
     *v = ctx->v.p;
     return TD_OK;
@@ -1414,7 +1466,7 @@ int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int fl
     ctx->last_kv_bytes = 0.0;
     tc.rows = ctx->b * n_q;
     if (int rc = ensure_rows(ctx, tc.rows, ctx->d)) return rc;
-    if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap)) return rc;
+    if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap, false, true)) return rc;
     int rc = TD_OK;
     if (!q_on_device && pinned_fast_path(ctx, flags, tc.plan)) {
         // the output goes straight into the caller's pinned buffer and the combine
@@ -1469,7 +1521,7 @@ int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xd
     if (parts & 1) launched(ctx, plan);
     if (!(parts & 2)) return TD_OK;  // the exchange kernel follows (group, shared GPU)
     ctx->x_epoch = xa.epoch;
-    ctx->kv_safe = ctx->len;  // later K1s run after this one's wait
+    ctx->kv_safe = plan.app_k ? plan.app_pos : ctx->len;  // later K1s run after this one's wait
     phase_mark(ctx);
     ctx->last_kernels = 2;  // K1 + K2x
     ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
@@ -1485,7 +1537,7 @@ bool graph_mode(td_context* ctx, const SplitPlan& plan, int flags) {
     static const bool env = [] { const char* e = std::getenv("TD_NCCL_GRAPH"); return e && std::atoi(e) != 0; }();
     if (!(env || (flags & TD_GRAPH))) return false;
     if (flags & (TD_HOST_IO | TD_TIME_KERNELS | TD_TIME_PHASES | TD_BF16_OUT | TD_DEBUG_TS)) return false;
-    return !plan.dbg && !plan.tl && ctx->comm;
+    return !plan.dbg && !plan.tl && !plan.app_k && ctx->comm;
 }
 
 // The NCCL tree step as a graph: captured on the first call of a shape and pool
@@ -1761,6 +1813,7 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
     ctx->det = call_deterministic(flags);
     if (int rc = debug_begin(ctx, flags)) return rc;
     if (!ctx->kv_ok) return set_err(TD_ESTATE, "ring_decode: no KV shard placed");
+    if (int rc = flush_append(ctx)) return rc;  // the shard is sent as it sits in HBM
     if (ctx->nranks > ctx->seq_len) return set_err(TD_EINVAL, "ring_decode: more workers than keys");
     if (n_q % ctx->n_kv != 0) return set_err(TD_EINVAL, "ring_decode: q/kv head mismatch");
     ctx->last_kernels = 0;

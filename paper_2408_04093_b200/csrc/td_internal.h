@@ -79,6 +79,13 @@ struct SplitPlan {
     unsigned* done_ctr = nullptr;
     unsigned* done_flag = nullptr;
     unsigned done_epoch = 0;
+    // fused KV append (bf16 kernel): the token appended since the last decode is
+    // still only in the caller's buffers app_k / app_v ([bh][d]); the warp that
+    // processes the tile holding position app_pos of a row patches that row's
+    // token into its staged tile and writes it into the cache (no append kernel)
+    const void* app_k = nullptr;
+    const void* app_v = nullptr;
+    int64_t app_pos = -1;
     // launch K1 as a programmatic dependent of the preceding kernel (off when several
     // contexts share one GPU and a peer's K1 must get SMs while this one's exchange waits)
     bool pdl = true;

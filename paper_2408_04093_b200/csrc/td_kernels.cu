@@ -108,6 +108,9 @@ struct K1Args {
     unsigned* claims;
     unsigned epoch;
     int early_trigger;        // debug: PDL trigger at K1 entry instead of after the main loop
+    const void* app_k;        // fused KV append (SplitPlan::app_*)
+    const void* app_v;
+    int64_t app_pos;
     // TD_PINNED_IO (SplitPlan): completion signalled to the host by K2's last warp
     unsigned* done_ctr;
     unsigned* done_flag;
@@ -649,7 +652,41 @@ __global__ void __launch_bounds__(W * 32, 1)
         const int64_t rem = a.t - tok0;
         const int nvalid = rem < T ? static_cast<int>(rem) : T;
 
+        // fused KV append: this tile holds the row's newest token, which is only in
+        // the caller's buffers. Its loads are issued before the wait for the tile so
+        // their latency hides behind the TMA; after it the token goes into the staged
+        // tile (the SWIZZLE_128B layout: 16-byte chunk c of row r sits at chunk
+        // c ^ (r & 7) of its 128-byte box row) and into the cache for later steps.
+        constexpr int CH = D / 8;                 // 16-byte chunks per row of K (and of V)
+        constexpr int PV = (2 * CH + 31) / 32;    // of K|V per lane
+        const bool patched = a.app_k && a.app_pos >= tok0 && a.app_pos < tok0 + T;
+        uint4 pv[PV];
+        if (patched) {
+#pragma unroll
+            for (int i = 0; i < PV; ++i) {
+                const int cc = lane + 32 * i;
+                if (cc < 2 * CH)
+                    pv[i] = __ldcg(reinterpret_cast<const uint4*>(cc >= CH ? a.app_v : a.app_k) + bh * CH + cc % CH);
+            }
+        }
         mbar_wait(&bars[warp][s], phase);
+        if (patched) {
+            const int r = static_cast<int>(a.app_pos - tok0);
+#pragma unroll
+            for (int i = 0; i < PV; ++i) {
+                const int cc = lane + 32 * i;
+                if (cc >= 2 * CH) continue;
+                const int which = cc / CH, c = cc % CH;
+                const uint4 val = pv[i];
+                uint8_t* tile = wsm + size_t(s) * STAGE_BYTES + (which ? TILE_BYTES : 0);
+                *reinterpret_cast<uint4*>(tile + (c >> 3) * BOX_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = val;
+                uint4* cache = reinterpret_cast<uint4*>(const_cast<void*>(which ? a.v : a.k));
+                cache[(bh * a.row_stride + a.app_pos) * CH + c] = val;
+            }
+            // generic-proxy writes to a stage the TMA (async proxy) refills later
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+        }
         const uint32_t kb = smem_u32(wsm + size_t(s) * STAGE_BYTES);
         const uint32_t vb = kb + TILE_BYTES;
 
@@ -2110,6 +2147,9 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.epoch = p.epoch;
     a.bh_table = p.bh_table;
     a.done_ctr = p.done_ctr;
+    a.app_k = p.app_k;
+    a.app_v = p.app_v;
+    a.app_pos = p.app_pos;
     a.done_flag = p.done_flag;
     a.done_epoch = p.done_epoch;
     if (p.pool_tiles > 0) {

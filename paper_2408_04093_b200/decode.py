@@ -544,8 +544,11 @@ class WorkerGroup:
         if host:
             flags |= _capi.TD_HOST_IO
         w0._sync_in(q)
-        check(lib().td_group_tree_decode(self.h, q.data_ptr(), q.shape[1], float(scale), int(strategy),
-                                         out.data_ptr(), flags))
+        rc = lib().td_group_tree_decode(self.h, q.data_ptr(), q.shape[1], float(scale), int(strategy),
+                                        out.data_ptr(), flags)
+        for w in self.workers:
+            w._consumed(rc)
+        check(rc)
         if not host:
             w0._sync_worker()
             for w in self.workers[1:]:
@@ -556,7 +559,10 @@ class WorkerGroup:
 
     def tree_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0,
                           strategy: int = 2):
-        check(lib().td_group_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags))
+        rc = lib().td_group_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags)
+        for w in self.workers:
+            w._consumed(rc)
+        check(rc)
 
     def close(self):
         if getattr(self, "h", None):
@@ -589,6 +595,7 @@ class Worker:
         self._owned = True  # False: a worker of a WorkerGroup (the group destroys it)
         self.device = device
         self._pending = []  # device tensors an enqueued td_kv_append still reads
+        self._live = None   # the last device token: the next decode's split kernel reads it (fused append)
         self._xs = None     # torch handle of the worker's stream (created on first use)
         self._ev = None     # input-ordering event (created on first use)
         self.nranks, self.rank = 1, 0
@@ -640,7 +647,7 @@ class Worker:
         w.h = handle
         w._owned = False
         w.device = device
-        w._pending, w._xs, w._ev = [], None, None
+        w._pending, w._xs, w._ev, w._live = [], None, None, None
         n, r = ctypes.c_int(), ctypes.c_int()
         check(lib().td_comm_info(handle, ctypes.byref(n), ctypes.byref(r)))
         w.nranks, w.rank = n.value, r.value
@@ -654,6 +661,7 @@ class Worker:
                 lib().td_destroy(self.h)  # synchronizes the worker's streams
             self.h = None
         self._pending = []
+        self._live = None
         self._xs = None
         self._ev = None
 
@@ -665,6 +673,14 @@ class Worker:
     def _sync_worker(self):
         self._worker_stream().synchronize()
         self._pending.clear()
+
+    def _consumed(self, rc: int = 0):
+        """A call that reads the cache returned rc: on success a deferred token is now
+        read by queued work, so its tensors move to the set held until the next
+        synchronisation. After a failure the token may still be deferred: keep it live."""
+        if rc == 0 and self._live is not None:
+            self._pending.append(self._live)
+            self._live = None
 
     def __del__(self):
         try:
@@ -685,6 +701,7 @@ class Worker:
                     scale: float = 1.0):
         """This rank's shard of seeded k/v (bit-exact with the reference generator)."""
         check(lib().td_kv_generate(self.h, int(dtype), b, n_kv, seq_len, d, seed_k, seed_v, scale))
+        self._consumed()
         self._meta(dtype, b, n_kv, seq_len, d)
 
     def place_kv(self, k, v, seq_len: int | None = None, start: int | None = None):
@@ -703,6 +720,7 @@ class Worker:
         self._sync_in(k)  # the device copy runs on the worker's stream: after k / v's producers
         check(lib().td_kv_place(self.h, int(dtype_of(k)), b, n_kv, seq_len, d, start, ln, k.data_ptr(),
                                 v.data_ptr(), 0 if k.is_cuda else 1))
+        self._consumed()
         self._meta(dtype_of(k), b, n_kv, seq_len, d)
 
     def append_kv(self, k, v):
@@ -716,8 +734,9 @@ class Worker:
             k, v = k.contiguous(), v.contiguous()
             self._sync_in(k)  # k and v come from the same (current) stream
             check(lib().td_kv_append(self.h, k.data_ptr(), v.data_ptr(), 0 if k.is_cuda else 1))
-            if k.is_cuda:  # the copy runs on the worker's stream: hold the sources until it is synced
-                self._pending.append((k, v))
+            self._consumed()  # an earlier deferred token is now written by an enqueued kernel
+            if k.is_cuda:  # read later on the worker's stream (by the next decode, fused): hold it
+                self._live = (k, v)
                 if len(self._pending) > 256:
                     self._sync_worker()
         else:
@@ -737,8 +756,10 @@ class Worker:
         shape = q.shape[:3]
         value, rm, sh = (torch.empty(shape, dtype=torch.float32, device=q.device) for _ in range(3))
         self._sync_in(q)
-        check(lib().td_energy_forward(self.h, q.data_ptr(), None if src is None else src.data_ptr(), q.shape[2],
-                                      value.data_ptr(), rm.data_ptr(), sh.data_ptr(), 0))
+        rc = lib().td_energy_forward(self.h, q.data_ptr(), None if src is None else src.data_ptr(), q.shape[2],
+                                     value.data_ptr(), rm.data_ptr(), sh.data_ptr(), 0)
+        self._consumed(rc)
+        check(rc)
         self._sync_worker()
         return EnergyEval(value, rm, sh)
 
@@ -753,7 +774,9 @@ class Worker:
         sh = saved.shifted_lse.to(torch.float32).contiguous()
         grad = torch.empty(q.shape, dtype=torch.float32, device=q.device)
         self._sync_in(q)
-        check(lib().td_energy_grad(self.h, q.data_ptr(), q.shape[2], rm.data_ptr(), sh.data_ptr(), grad.data_ptr(), 0))
+        rc = lib().td_energy_grad(self.h, q.data_ptr(), q.shape[2], rm.data_ptr(), sh.data_ptr(), grad.data_ptr(), 0)
+        self._consumed(rc)
+        check(rc)
         self._sync_worker()
         return grad
 
@@ -765,7 +788,9 @@ class Worker:
         return g.value, st.value
 
     def reserve_kv(self, tokens: int):
-        check(lib().td_kv_reserve(self.h, int(tokens)))
+        rc = lib().td_kv_reserve(self.h, int(tokens))
+        self._consumed(rc)  # a growth writes a deferred token first
+        check(rc)
 
     def kv_info(self):
         s, n, nb = self._ct.c_int64(), self._ct.c_int64(), self._ct.c_size_t()
@@ -801,6 +826,7 @@ class Worker:
                 flags |= _capi.TD_PINNED_IO  # the combine kernel writes out in place and signals the host
         self._sync_in(q)
         rc = fn(self.h, q.data_ptr(), n_q, float(scale), *extra, out.data_ptr(), flags)
+        self._consumed(rc)
         check(rc)
         if not host:
             self._sync_worker()
@@ -825,10 +851,14 @@ class Worker:
     # -- async launch (no synchronisation) for timing loops ----------------
     def tree_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0,
                           strategy: int = 2):
-        check(lib().td_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags))
+        rc = lib().td_tree_decode(self.h, q_ptr, n_q, float(scale), strategy, out_ptr, flags)
+        self._consumed(rc)
+        check(rc)
 
     def ring_decode_async(self, q_ptr: int, n_q: int, out_ptr: int, scale: float = 1.0, flags: int = 0):
-        check(lib().td_ring_decode(self.h, q_ptr, n_q, float(scale), out_ptr, flags))
+        rc = lib().td_ring_decode(self.h, q_ptr, n_q, float(scale), out_ptr, flags)
+        self._consumed(rc)
+        check(rc)
 
     def kernel_time(self) -> tuple[float, int]:
         ms, n = self._ct.c_double(), self._ct.c_int()

@@ -64,12 +64,17 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         t0 = time.perf_counter()
+        t_app = 0.0
         for s in range(K):
             if do_append:
+                ta = time.perf_counter()
                 w.append_kv(ks[s], vs[s])
+                t_app += time.perf_counter() - ta
             if do_decode:
                 w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags)
         host_us[(do_append, do_decode)] = (time.perf_counter() - t0) / K * 1e6
+        if do_append:
+            host_us[("append only", True)] = t_app / K * 1e6
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / K
@@ -98,8 +103,8 @@ def main():
         print(json.dumps({"metric": "generation loop: append + exact tree decode, us per token", "n_gpus": world,
                           "start_len": n, "steps": K, "us_per_token": ms * 1000.0,
                           "decode_only_us_per_token": decode_only * 1000.0,
-                          "host_enqueue_us_per_step": {("append+decode" if a else "decode"): round(v, 1)
-                                                       for (a, _), v in host_us.items()},
+                          "host_enqueue_us_per_step": {(a if isinstance(a, str) else ("append+decode" if a else "decode")):
+                                                       round(v, 1) for (a, _), v in host_us.items()},
                           "final_len": n + K, "rel_err_vs_oracle": err}), flush=True)
     w.close()
     if world > 1:

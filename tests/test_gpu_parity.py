@@ -337,6 +337,52 @@ def test_append_decode_loop_without_host_sync(td, oracle):
     w.close()
 
 
+def test_group_fused_append_loop(td, oracle):
+    """Device-token appends into a 3-worker group on one GPU, decoded through the
+    exchange combine with no host synchronisation. The last worker's split kernel
+    writes each token as it streams (fused append); on every third step two tokens
+    are appended before one decode, so the first is written by the append kernel
+    the second append enqueues. A token read before it landed, or written twice at
+    the wrong position, moves the output past the tolerance (needle keys as above)."""
+    import torch
+    b, n_q, n_kv, n, d, steps, p = 1, 32, 8, 5000, 128, 40, 3
+    q, k, v = make_inputs(oracle, 47, b, n_q, n_kv, n + steps, d, BF16)
+    qb = q.reshape(b, n_kv, n_q // n_kv, d)[:, :, 0]
+    k = k.copy()
+    for s in range(steps):
+        k[:, :, n + s] = qb * float(2 << (s % 2))
+    g = td.WorkerGroup(p, [0])
+    start = 0
+    for w, e in zip(g.workers, td.chunk_extents(n, p)):
+        w.place_kv(dev(np.ascontiguousarray(k[:, :, start:start + e]), BF16),
+                   dev(np.ascontiguousarray(v[:, :, start:start + e]), BF16), seq_len=n, start=start)
+        start += e
+    g.enable_p2p(b * n_q, d)
+    qd = dev(q, BF16)
+    kn = dev(np.ascontiguousarray(np.moveaxis(k[:, :, n:], 2, 0)[:, :, :, None]), BF16)
+    vn = dev(np.ascontiguousarray(np.moveaxis(v[:, :, n:], 2, 0)[:, :, :, None]), BF16)
+    out = torch.empty(steps, b, n_q, d, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    decoded = []
+    for s in range(steps):
+        for w in g.workers:
+            w.append_kv(kn[s], vn[s])
+        if s % 3 != 1:
+            g.tree_decode_async(qd.data_ptr(), n_q, out[s].data_ptr())
+            decoded.append(s)
+    for w in g.workers:
+        w._sync_worker()
+        assert w.p2p_status() == 0
+    assert g.workers[-1].kv_info()[1] == td.chunk_extents(n, p)[-1] + steps
+    got = out.cpu().double().numpy()
+    g.close()
+    for s in decoded:
+        m = n + s + 1
+        want = oracle.tree_decode(q, np.ascontiguousarray(k[:, :, :m]), np.ascontiguousarray(v[:, :, :m]), 1, HIER,
+                                  1.0, F64)
+        assert rel_err(got[s], want) <= TOL[BF16], (s, rel_err(got[s], want))
+
+
 def test_worker_append_validation_and_output_buffers(td, oracle):
     """Append errors leave the cache unchanged; host outputs work pinned
     (zero-copy store) and pageable (D2H copy) alike."""
