@@ -529,6 +529,13 @@ def main():
         nccl_phases = [round(max_over_ranks(x, world) * 1000.0, 2) for x in w.phase_times()]
         graph_ms = timed_loop(lambda fl: w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale,
                                                              fl | _capi.TD_GRAPH), ks)
+        try:
+            ndev_ms = timed_loop(lambda fl: w.tree_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale,
+                                                                fl | _capi.TD_NCCL_DEVICE), ks)
+        except td.TreeDecError as e:  # no NCCL device API on this box: every rank fails alike
+            ndev_ms, ndev_err = None, str(e)
+        else:
+            ndev_err = None
         ring_ms = timed_loop(lambda fl: w.ring_decode_async(q.data_ptr(), n_q, out.data_ptr(), args.scale, fl), ks)
         compare = {
             "steps": ks,
@@ -536,10 +543,14 @@ def main():
             "nccl_us": nccl_ms * 1000.0,
             "nccl_phases_us": dict(zip(("K1", "K2", "allreduce_max", "K3", "allreduce_sum", "K4"), nccl_phases)),
             "nccl_graph_us": graph_ms * 1000.0,
+            "nccl_device_us": ndev_ms * 1000.0 if ndev_ms is not None else None,
+            **({"nccl_device_error": ndev_err} if ndev_err else {}),
             "ring_us": ring_ms * 1000.0,
             "tree_over_ring": ring_ms / ms,
             "note": "same cache and query; nccl = K1, K2, ncclAllReduce(max), K3, ncclAllReduce(sum), K4 "
-                    "(decode.cpp:129-173 literally), nccl_graph = the same step replayed as a CUDA graph; ring = p-1 NCCL send/recv rotations of the KV shards with "
+                    "(decode.cpp:129-173 literally), nccl_graph = the same step replayed as a CUDA graph; "
+                    "nccl_device = the same two allreduces inside one combine kernel through NCCL's device API "
+                    "(symmetric window, ncclGetLsaPointer); ring = p-1 NCCL send/recv rotations of the KV shards with "
                     "the partial of the chunk in hand overlapped (decode.cpp:186-251); tree_over_ring = "
                     "ring_us / tree_us",
         }
@@ -595,6 +606,7 @@ def main():
             "compare": compare,
             "ring_us": compare["ring_us"] if compare else None,
             "nccl_us": compare["nccl_us"] if compare else None,
+            "nccl_device_us": compare["nccl_device_us"] if compare else None,
             "tree_over_ring": compare["tree_over_ring"] if compare else None,
             "sequences_per_s": b / (ms * 1e-3),
             "e2e": {"value": e2e_ms * 1000.0, "unit": "µs/token",

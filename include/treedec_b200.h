@@ -76,10 +76,18 @@ enum {
                              (and let idle warps take other rows' chunks on long
                              shards). Up to ~2.5% faster on some shapes; results
                              then agree to ~1e-7, not bitwise, between calls. */
-    TD_GRAPH = 512        /* paper-literal NCCL path (nranks > 1 without TD_P2P), device
+    TD_GRAPH = 512,       /* paper-literal NCCL path (nranks > 1 without TD_P2P), device
                              buffers: capture the step (K1, K2, allreduce(max), K3,
                              allreduce(sum), K4) as a CUDA graph once per shape and
                              replay it (TD_NCCL_GRAPH=1 sets it for every call) */
+    TD_NCCL_DEVICE = 1024 /* tree decode, nranks > 1 (after td_comm_init): the same
+                             two allreduces -- max of lse, then sum of [n|d] -- run
+                             inside one combine kernel through NCCL's device API:
+                             every rank stores into and polls the others' copies of
+                             a symmetric NCCL window (NCCL >= 2.28, all ranks in one
+                             NVLink domain). The window is registered on the first
+                             such call of a size (collective: every rank makes the
+                             call). TD_EINVAL when unavailable. */
 };
 
 typedef struct td_context td_context;

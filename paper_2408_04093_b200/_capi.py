@@ -19,6 +19,7 @@ TD_HOST_IO, TD_TIME_KERNELS, TD_BF16_OUT, TD_TIME_PHASES, TD_P2P, TD_DEBUG_TS, T
 TD_PINNED_IO = 128
 TD_DYNAMIC = 256
 TD_GRAPH = 512
+TD_NCCL_DEVICE = 1024
 
 # Every symbol include/treedec_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = [

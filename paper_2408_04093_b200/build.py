@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtreedec_b200.so")
-SOURCES = ["td_kernels.cu", "td_capi.cu"]
+SOURCES = ["td_kernels.cu", "td_capi.cu", "td_nccl_dev.cu"]
 HEADERS = ["td_device.cuh", "td_internal.h"]
 
 NVCC_FLAGS = [
@@ -23,6 +23,27 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
     "-I" + os.path.join(ROOT, "include"),
 ]
+
+
+def _nccl_device_include() -> str | None:
+    """NCCL's device-API headers (NCCL >= 2.28, shipped with torch's NCCL wheel)."""
+    cands = [os.environ.get("TD_NCCL_INCLUDE")]
+    try:
+        import nvidia.nccl
+        cands += [os.path.join(p, "include") for p in nvidia.nccl.__path__]
+    except ImportError:
+        pass
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "nccl_device.h")):
+            return c
+    return None
+
+
+def _extra_flags(src: str) -> list[str]:
+    if src != "td_nccl_dev.cu":
+        return []
+    inc = _nccl_device_include()
+    return ["-I" + inc, "-DTD_HAVE_NCCL_DEVICE"] if inc else []
 
 
 def _nvcc() -> str:
@@ -49,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [_nvcc(), *NVCC_FLAGS, *_extra_flags(src), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

@@ -81,6 +81,11 @@ struct NcclApi {
     ncclResult_t (*WindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
     ncclResult_t (*WindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
     bool symmetric() const { return MemAlloc && MemFree && WindowRegister && WindowDeregister; }
+    // device API (NCCL >= 2.28): the load/store-accessible team of this rank
+    struct Team {
+        int nRanks, rank, stride;
+    };
+    Team (*TeamLsa)(ncclComm_t) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -115,6 +120,7 @@ NcclApi& nccl() {
         opt(a.MemFree, "ncclMemFree");
         opt(a.WindowRegister, "ncclCommWindowRegister");
         opt(a.WindowDeregister, "ncclCommWindowDeregister");
+        opt(a.TeamLsa, "ncclTeamLsa");
         if (!all) a.err = "libnccl.so.2 lacks a required symbol";
         return a;
     }();
@@ -264,6 +270,14 @@ struct td_context {
     size_t win_bytes = 0;
     ncclWindow_t win = nullptr;
     int win_state = 0;  // 0 untried, 1 registered, -1 unavailable (plain buffers)
+    // TD_NCCL_DEVICE: K2n's LL words in a second symmetric window; nx_ptrs holds
+    // every rank's copy's address (ncclGetLsaPointer)
+    void* nx_buf = nullptr;
+    ncclWindow_t nx_win = nullptr;
+    int64_t nx_rows = 0, nx_d = 0;
+    DevBuf nx_ptrs;
+    unsigned nx_epoch = 0;
+    bool nx_ready = false;
 
     // TD_GRAPH: the paper-literal NCCL step (K1, K2, allreduce(max), K3,
     // allreduce(sum), K4) captured once per shape and replayed; only the split
@@ -753,11 +767,70 @@ int exchange_failed(td_context* ctx) {
     if (!v) return TD_OK;
     *reinterpret_cast<volatile int*>(ctx->x_err) = 0;
     ctx->x_ready = false;
+    ctx->nx_ready = false;
     const int miss = (v >> 8) & 255;
     return set_err(TD_ECUDA, "tree_decode: NVLink exchange timed out on rank " + std::to_string(ctx->rank) +
                                  " (epoch " + std::to_string(ctx->x_epoch) + ", first missing source " +
                                  (miss == 255 ? std::string("beyond the batched peers") : std::to_string(miss)) +
-                                 "); re-open the exchange with td_p2p_handle / td_p2p_open");
+                                 "); re-open the exchange with td_p2p_handle / td_p2p_open (TD_NCCL_DEVICE: "
+                                 "the next call re-registers its window on every rank)");
+}
+
+void nccl_dev_close(td_context* ctx) {
+    if (ctx->nx_win) nccl().WindowDeregister(ctx->comm, ctx->nx_win);
+    if (ctx->nx_buf) nccl().MemFree(ctx->nx_buf);
+    ctx->nx_win = nullptr;
+    ctx->nx_buf = nullptr;
+    ctx->nx_rows = ctx->nx_d = 0;
+    ctx->nx_ready = false;
+}
+
+// TD_NCCL_DEVICE: K2n's window for rows x d, zeroed (epoch 0 matches no step)
+// before the collective registration, so no rank can store into a copy that is
+// still being cleared; then every rank's copy's address from the device API.
+int nccl_dev_open(td_context* ctx, int64_t rows, int64_t d) {
+    if (ctx->nx_ready && rows <= ctx->nx_rows && d == ctx->nx_d) return TD_OK;
+    if (!ctx->comm) return set_err(TD_ESTATE, "tree_decode: TD_NCCL_DEVICE needs td_comm_init");
+    if (!nccl().symmetric() || !nccl().TeamLsa)
+        return set_err(TD_EINVAL, "tree_decode: TD_NCCL_DEVICE needs NCCL >= 2.28 (symmetric windows, device API)");
+    const auto team = nccl().TeamLsa(ctx->comm);
+    if (team.nRanks != ctx->nranks || team.rank != ctx->rank)
+        return set_err(TD_EINVAL, "tree_decode: TD_NCCL_DEVICE needs every rank in one NVLink domain");
+    nccl_dev_close(ctx);
+    const size_t bytes = td::literal_window_bytes(ctx->nranks, rows, d);
+    if (nccl().MemAlloc(&ctx->nx_buf, bytes) != ncclSuccess) {
+        ctx->nx_buf = nullptr;
+        return set_err(TD_ENCCL, "tree_decode: ncclMemAlloc of the combine window failed");
+    }
+    TD_CUDA(cudaMemsetAsync(ctx->nx_buf, 0, bytes, ctx->stream));
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (nccl().WindowRegister(ctx->comm, ctx->nx_buf, bytes, &ctx->nx_win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+        ctx->nx_win = nullptr;
+        nccl_dev_close(ctx);
+        return set_err(TD_ENCCL, "tree_decode: ncclCommWindowRegister of the combine window failed");
+    }
+    TD_CUDA(ctx->nx_ptrs.ensure(size_t(ctx->nranks) * sizeof(void*) + 64));
+    int* ok = reinterpret_cast<int*>(static_cast<char*>(ctx->nx_ptrs.p) + size_t(ctx->nranks) * sizeof(void*));
+    const cudaError_t e = td::launch_lsa_peers(ctx->nx_win, ctx->nranks, static_cast<void**>(ctx->nx_ptrs.p), ok,
+                                               ctx->stream);
+    if (e == cudaErrorNotSupported) {
+        nccl_dev_close(ctx);
+        return set_err(TD_EINVAL, "tree_decode: TD_NCCL_DEVICE: library built without NCCL's device headers");
+    }
+    TD_CUDA(e);
+    int ok_h = 0;
+    TD_CUDA(cudaMemcpyAsync(&ok_h, ok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!ok_h) {
+        nccl_dev_close(ctx);
+        return set_err(TD_EINVAL, "tree_decode: TD_NCCL_DEVICE: NVLink-domain rank differs from the world rank");
+    }
+    if (!ctx->x_err) TD_CUDA(cudaHostAlloc(&ctx->x_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    ctx->nx_rows = rows;
+    ctx->nx_d = d;
+    ctx->nx_epoch = 0;
+    ctx->nx_ready = true;
+    return TD_OK;
 }
 
 // The NCCL combine's buffers [lse rows | shift rows | n rows*d, d rows] inside a
@@ -995,6 +1068,8 @@ int td_destroy(td_context* ctx) {
     }
     if (ctx->win) nccl().WindowDeregister(ctx->comm, ctx->win);
     if (ctx->win_buf) nccl().MemFree(ctx->win_buf);
+    nccl_dev_close(ctx);
+    ctx->nx_ptrs.release();
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     ctx->k.release();
     ctx->v.release();
@@ -1057,6 +1132,7 @@ int td_comm_init(td_context* ctx, int nranks, int rank, const unsigned char id[1
         ctx->win_buf = nullptr;
         ctx->win_bytes = 0;
         ctx->win_state = 0;
+        nccl_dev_close(ctx);
         nccl().CommDestroy(ctx->comm);
         ctx->comm = nullptr;
     }
@@ -1679,6 +1755,33 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         if (!tc.fast) return deliver_out(ctx, dst, rows, out, flags);
         if (int rc2 = note_table_use(ctx)) return rc2;
         return wait_done(ctx, plan.done_epoch);
+    }
+    if (flags & TD_NCCL_DEVICE) {
+        // K1 -> K2 (lse, out per row) -> K2n: allreduce(max), n/d numerators,
+        // allreduce(sum), n/d in one kernel over the ranks' symmetric windows
+        if (int rc2 = exchange_failed(ctx)) return rc2;
+        if (int rc2 = nccl_dev_open(ctx, rows, d)) return rc2;
+        if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok, ctx->row_max, ctx->lse,
+                              ctx->out_local, (flags & TD_TIME_KERNELS) != 0, ctx->cur_phase ? ctx : nullptr)))
+            return rc;
+        phase_mark(ctx);
+        float* dst = ctx->out;
+        if (!(flags & TD_HOST_IO)) dst = out;
+        else if (!(flags & TD_BF16_OUT)) if (float* m = mapped_host(ctx, out)) dst = m;
+        td::XchgArgs xa;
+        xa.peers = static_cast<float* const*>(ctx->nx_ptrs.p);
+        xa.p = ctx->nranks;
+        xa.rank = ctx->rank;
+        xa.epoch = ctx->nx_epoch + 1;
+        xa.max_rows = ctx->nx_rows;
+        xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));
+        xa.error = ctx->x_err;
+        TD_CUDA(td::launch_literal_combine(ctx->lse, ctx->out_local, xa, rows, static_cast<int>(d), dst, ctx->stream));
+        ctx->nx_epoch = xa.epoch;
+        phase_mark(ctx);
+        ctx->last_kernels += 1;
+        if (int rc2 = deliver_out(ctx, dst, rows, out, flags)) return rc2;
+        return (flags & TD_HOST_IO) ? exchange_failed(ctx) : TD_OK;
     }
     // the allreduced buffers: in a symmetric NCCL window when available
     float *lse = ctx->lse, *shift = ctx->shift, *nd = ctx->nd;

@@ -165,6 +165,21 @@ cudaError_t graph_set_k1_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const
 bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,
                      std::string& msg);
 
+// K2n: allreduce(max) + partial_to_numerator + allreduce(sum) + n/d of K2's
+// per-row (lse, out) over the ranks' symmetric NCCL windows (xa.peers: every
+// rank's window base, from launch_lsa_peers); programmatic dependent of K2.
+cudaError_t launch_literal_combine(const float* lse, const float* o, const XchgArgs& xa, int64_t rows, int d,
+                                   float* out, cudaStream_t stream);
+// Words of one rank's K2n window: A [2][p][max_rows] + B [2][p][max_rows][d + 1].
+inline size_t literal_window_bytes(int p, int64_t max_rows, int64_t d) {
+    return 2 * size_t(p) * size_t(max_rows) * size_t(d + 2) * 8;
+}
+// NCCL device API (td_nccl_dev.cu): ptrs[k] = ncclGetLsaPointer(win, 0, k) for
+// k < p, the load/store address of rank k's copy of a symmetric window; *ok
+// (device int) = 1 when this rank's LSA team index equals its world rank.
+// Returns cudaErrorNotSupported when built without the NCCL device headers.
+cudaError_t launch_lsa_peers(void* win, int p, void** ptrs, int* ok, cudaStream_t stream);
+
 // K3: partial_to_numerator; nd = [num rows*d | den rows].
 cudaError_t launch_to_numerator(const float* lse, const float* out, const float* shift,
                                 int64_t rows, int d, float* nd, cudaStream_t stream);

@@ -1980,6 +1980,123 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
 }
 
 // =========================================================================
+// K2n: the paper-literal combine of decode.cpp:129-173 -- allreduce(max) of the
+// shard lse, partial_to_numerator, allreduce(sum) of [n|d], n/d -- as one kernel
+// over a symmetric NCCL window (NCCL's device API makes every rank's window
+// load/store-addressable: ncclGetLsaPointer, td_nccl_dev.cu). Each allreduce is
+// one round of LL words (value, epoch): a warp stores its rows' words into slot
+// `rank` of every rank's window, then polls the p slots of its own. It runs as a
+// programmatic dependent of K2 (kTailPartial: lse and out per output row).
+// Window layout, 8-byte words: A [2 parities][p][max_rows] lse, then
+// B [2][p][max_rows][d + 1] [n | d]. Parities alternate by epoch, so a slot is
+// rewritten only after every rank has read it (as in K2x). One-warp blocks, at
+// most the co-resident count, each pushing all its rows before any wait: the
+// exchange cannot deadlock; spins are bounded and report through x.error.
+// =========================================================================
+template <int NC>
+__global__ void __launch_bounds__(32) k2n_literal(const float* lse, const float* o, const XchgArgs x, int64_t rows,
+                                                  int d, float* out) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's K1 may get resident
+    constexpr int PMAX = 8;  // sources polled as one batch
+    const int lane = threadIdx.x & 31;
+    uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
+    uint2* pp[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) pp[k] = k < x.p ? peers[k] : nullptr;
+    const uint2* own = peers[x.rank];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const unsigned par = x.epoch & 1u;
+    const int64_t a_src = x.max_rows;  // region A words per (parity, source)
+    const int64_t b0 = 2 * int64_t(x.p) * a_src;                             // region B
+    // allreduce(max), send: this rank's lse of each of its rows to every rank
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float l = __ldcg(lse + r);
+        const int64_t off = (int64_t(par) * x.p + x.rank) * a_src + r;
+        for (int q = lane; q < x.p; q += 32) st_ll(peers[q] + off, l, x.epoch);
+    }
+    // receive -> shift; n = o e^(l - shift), d = e^(l - shift); allreduce(sum), send
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        float m = -CUDART_INF_F;
+        for (int k = lane; k < x.p; k += 32)
+            m = fmaxf(m, ld_ll(own + (int64_t(par) * x.p + k) * a_src + r, x.epoch, x.error));
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+        const float l = __ldcg(lse + r);
+        const float wgt = l == -CUDART_INF_F ? 0.f : expf(l - m);
+        float nv[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const int col = c * 32 + lane;
+            nv[c] = col < d ? __ldcg(o + r * d + col) * wgt : 0.f;
+        }
+        const int64_t off = b0 + ((int64_t(par) * x.p + x.rank) * x.max_rows + r) * (d + 1);
+        for (int q = 0; q < x.p; ++q) {
+            uint2* dst = (q < PMAX ? pp[q] : peers[q]) + off;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (c * 32 + lane < d) st_ll(dst + c * 32 + lane, nv[c], x.epoch);
+            if (lane == 0) st_ll(dst + d, wgt, x.epoch);
+        }
+    }
+    // receive: sum the p sources' [n | d] (first PMAX polled as one batch), n / d
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const uint2* base = own + b0 + (int64_t(par) * x.p * x.max_rows + r) * (d + 1);
+        const int64_t sstride = x.max_rows * int64_t(d + 1);
+        uint2 wd[PMAX], wn[PMAX][NC];
+        const long long t0 = clock64();
+        for (;;) {
+            bool all = true;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                const uint2* slot = base + k * sstride;
+                wd[k] = ld_word(slot + d);
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (c * 32 + lane < d) wn[k][c] = ld_word(slot + c * 32 + lane);
+            }
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                all &= wd[k].y == x.epoch;
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (c * 32 + lane < d) all &= wn[k][c].y == x.epoch;
+            }
+            if (__all_sync(0xffffffffu, all)) break;
+            if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a rank never arrived
+                int miss = 255;
+#pragma unroll
+                for (int k = PMAX - 1; k >= 0; --k)
+                    if (k < x.p && wd[k].y != x.epoch) miss = k;
+                *reinterpret_cast<volatile int*>(x.error) = 1 | (miss << 8) | (x.rank << 16);
+                break;
+            }
+        }
+        float den = 0.f, num[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) num[c] = 0.f;
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k) {
+            if (k >= x.p) continue;
+            den += __uint_as_float(wd[k].x);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) num[c] += __uint_as_float(wn[k][c].x);
+        }
+        for (int k = PMAX; k < x.p; ++k) {  // past one batch: word by word
+            const uint2* slot = base + k * sstride;
+            den += ld_ll(slot + d, x.epoch, x.error);
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (c * 32 + lane < d) num[c] += ld_ll(slot + c * 32 + lane, x.epoch, x.error);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c * 32 + lane < d) out[r * d + c * 32 + lane] = num[c] / den;
+    }
+}
+
+// =========================================================================
 // K3 / K4 / K5 / combine_partials / K6
 // =========================================================================
 __global__ void k3_to_numerator(const float* lse, const float* out, const float* shift,
@@ -2687,6 +2804,19 @@ unsigned grid_for(int64_t n, int threads) {
     return static_cast<unsigned>(g);
 }
 }  // namespace
+
+cudaError_t launch_literal_combine(const float* lse, const float* o, const XchgArgs& xa, int64_t rows, int d,
+                                   float* out, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<int64_t>(rows, xa.max_blocks));
+    if (grid < 1) return cudaSuccess;
+    switch ((d + 31) / 32) {
+        case 1: return launch_pdl(k2n_literal<1>, grid, 32, 0, st, true, lse, o, xa, rows, d, out);
+        case 2: return launch_pdl(k2n_literal<2>, grid, 32, 0, st, true, lse, o, xa, rows, d, out);
+        case 3:
+        case 4: return launch_pdl(k2n_literal<4>, grid, 32, 0, st, true, lse, o, xa, rows, d, out);
+        default: return launch_pdl(k2n_literal<8>, grid, 32, 0, st, true, lse, o, xa, rows, d, out);
+    }
+}
 
 cudaError_t launch_to_numerator(const float* lse, const float* out, const float* shift,
                                 int64_t rows, int d, float* nd, cudaStream_t st) {

@@ -50,6 +50,10 @@ def main():
         graphed = [w.tree_decode(q, scale, out=gbuf, flags=td._capi.TD_GRAPH).clone() for _ in range(5)]
         fits = b * n_q <= 64 and d == 128
         p2p = w.tree_decode(q, scale, flags=td._capi.TD_P2P) if fits else tree
+        # the two allreduces inside one kernel through NCCL's device API (several
+        # calls: the window's parities alternate), device and host buffers
+        ndev = [w.tree_decode(q, scale, flags=td._capi.TD_NCCL_DEVICE).clone() for _ in range(3)]
+        ndev.append(w.tree_decode(q.cpu(), scale, flags=td._capi.TD_NCCL_DEVICE))
         # every rank must hold the same output
         t_all = [torch.empty_like(tree) for _ in range(world)]
         dist.all_gather(t_all, tree)
@@ -60,13 +64,15 @@ def main():
             e_tree = rel_err_rows(tree.double().cpu().numpy(), want)
             e_ring = rel_err_rows(ring.double().cpu().numpy(), want)
             e_p2p = rel_err_rows(p2p.double().cpu().numpy(), want)
+            e_ndev = max(rel_err_rows(x.double().cpu().numpy(), want) for x in ndev)
             same = all(torch.equal(t_all[0], x) for x in t_all)
             same_graph = all(torch.equal(tree, x) for x in graphed)  # static split: bitwise
-            good = (e_tree <= tol and e_ring <= tol and e_p2p <= tol and same and same_graph
+            good = (e_tree <= tol and e_ring <= tol and e_p2p <= tol and e_ndev <= tol and same and same_graph
                     and w.p2p_status() == 0)
             ok &= good
             print(json.dumps({"world": world, "dtype": "bf16" if dt == BF16 else "f32", "n": n, "b": b, "n_q": n_q,
                               "n_kv": n_kv, "tree_rel_err": e_tree, "ring_rel_err": e_ring, "p2p_rel_err": e_p2p,
+                              "nccl_device_rel_err": e_ndev,
                               "ranks_agree": same, "graph_equals_stream": same_graph, "ok": good}), flush=True)
     # generation loop: append tokens to rank p-1's shard, decode the grown cache
     b, n_q, n_kv, d, n0, steps = 1, 8, 2, 128, 4096 * world + 5, 40
@@ -82,18 +88,20 @@ def main():
         w.append_kv(bf(kh[:, :, n0 + s:n0 + s + 1]).cuda(), bf(vh[:, :, n0 + s:n0 + s + 1]).cuda())
         if s not in (0, steps - 1):
             continue
-        tree, ring = w.tree_decode(q), w.ring_decode(q)
-        p2p = w.tree_decode(q, flags=td._capi.TD_P2P)
+        # the first decode after a device append writes the token (fused): a different
+        # combine takes it at the first and at the last step
+        fl = {"tree": 0, "p2p": td._capi.TD_P2P, "nccl_device": td._capi.TD_NCCL_DEVICE}
+        order = ["tree", "ring", "p2p", "nccl_device"] if s == 0 else ["nccl_device", "p2p", "ring", "tree"]
+        res = {k: (w.ring_decode(q) if k == "ring" else w.tree_decode(q, flags=fl[k])) for k in order}
         if rank == 0:
             m = n0 + s + 1
             want = orc.tree_decode(qh, np.ascontiguousarray(kh[:, :, :m]), np.ascontiguousarray(vh[:, :, :m]),
                                    world, HIER, 1.0, F64, nthreads=8)
             mx = np.max(np.abs(want))
-            errs = [float(np.max(np.abs(x.double().cpu().numpy() - want)) / mx) for x in (tree, ring, p2p)]
-            good = max(errs) <= 1e-3
+            errs = {k + "_rel_err": float(np.max(np.abs(x.double().cpu().numpy() - want)) / mx) for k, x in res.items()}
+            good = max(errs.values()) <= 1e-3
             ok &= good
-            print(json.dumps({"world": world, "append_step": s, "n": m, "tree_rel_err": errs[0],
-                              "ring_rel_err": errs[1], "p2p_rel_err": errs[2], "ok": good}), flush=True)
+            print(json.dumps({"world": world, "append_step": s, "n": m, **errs, "ok": good}), flush=True)
     # energy formulation across the ranks (Alg. 1 / Alg. 2, energy.cpp:152-259)
     b, h, nq, n, d = 1, 4, 2, 2048 * world + 3, 128
     seed = orc.mix64(9, n)
