@@ -54,9 +54,10 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
     ap.add_argument("--seq-len", type=int, default=None)
     ap.add_argument("--algo", choices=["tree", "ring"], default="tree")
-    ap.add_argument("--combine", choices=["nccl", "p2p"], default="p2p",
+    ap.add_argument("--combine", choices=["nccl", "p2p", "nccl_device"], default="p2p",
                     help="tree exchange (N > 1): one-shot NVLink exchange (default; falls back to nccl "
-                         "if CUDA IPC is unavailable on any rank) or two NCCL allreduces (paper-literal)")
+                         "if CUDA IPC is unavailable on any rank), two NCCL allreduces (paper-literal), or "
+                         "the same two allreduces inside one kernel through NCCL's device API")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=None)
@@ -88,6 +89,9 @@ def interconnect(args, world, b, n_q, n_kv, n, d, esz, ms):
     elif args.combine == "p2p":
         nbytes = (world - 1) * rows * (d + 1) * 8
         what = "one-shot exchange: LL words (value, epoch) of [out | lse] pushed to every peer"
+    elif args.combine == "nccl_device":
+        nbytes = (world - 1) * rows * (d + 2) * 8
+        what = "NCCL device API: LL words of lse, then of [n | d], stored into every rank's symmetric window"
     else:
         nbytes = rows * 4 + rows * (d + 1) * 4
         what = "NCCL allreduce(max) of lse + allreduce(sum) of [n | d] (payload)"
@@ -335,7 +339,8 @@ def run_reference_arm(args, wl, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "µs/token", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value / 1000.0, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": dt, "data": "synthetic (reference generator)",
-        "config": bench_config(args, wl, args.gpus, combine=("p2p" if args.gpus > 1 else "none"),
+        "config": bench_config(args, wl, args.gpus, combine=(args.combine if args.gpus > 1 and args.algo == "tree"
+                                                             else "none"),
                                flush=2 * b * n_kv * math.ceil((args.seq_len or n) / args.gpus) * d
                                * (2 if dt == "bf16" else 4) < 4 * L2_BYTES),
         "cpu_baseline": {"value": value, "unit": "µs/token", "cores": info["cores"], "kind": "reference",
@@ -411,6 +416,8 @@ def main():
             base_flags = _capi.TD_P2P
         else:
             args.combine = "nccl"
+    elif args.combine == "nccl_device" and world > 1 and args.algo == "tree":
+        base_flags = _capi.TD_NCCL_DEVICE
 
     def step(flags):
         decode(q.data_ptr(), n_q, out.data_ptr(), args.scale, flags | base_flags)
