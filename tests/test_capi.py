@@ -62,3 +62,26 @@ def test_no_cpu_fallback_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("oracle/_ref", ""), f
+
+
+def test_header_flags_match_python(tmp_path):
+    """Every TD_* flag / status / dtype value of the header, compiled by a C
+    compiler, equals the constant the Python mirror passes."""
+    from paper_2408_04093_b200 import _capi
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(TD_[A-Z0-9_]+)\s*=", src)))
+    assert "TD_NCCL_DEVICE" in names and "TD_P2P" in names
+    c = tmp_path / "f.c"
+    c.write_text('#include <stdio.h>\n#include "treedec_b200.h"\nint main(void){\n' +
+                 "".join(f'printf("{n} %d\\n", (int){n});\n' for n in names) + "return 0;}\n")
+    exe = tmp_path / "f"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(c), "-o",
+                        str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n")
+               if line)
+    for n, v in got.items():
+        if hasattr(_capi, n):
+            assert getattr(_capi, n) == int(v), n
+    for flag in ("TD_HOST_IO", "TD_P2P", "TD_PINNED_IO", "TD_DYNAMIC", "TD_GRAPH", "TD_NCCL_DEVICE"):
+        assert hasattr(_capi, flag) and int(got[flag]) == getattr(_capi, flag), flag
