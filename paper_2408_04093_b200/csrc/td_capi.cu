@@ -757,6 +757,16 @@ float* mapped_host(td_context* ctx, float* host) {
     return dev;
 }
 
+// Whether the exchange kernel (K2x) should store a host-buffer call's output
+// straight into pinned host memory. Small outputs gain ~2 us that way; large ones
+// lose: K2x's warps stall on their PCIe stores between the exchange polls (cfg4 at
+// N = 2, 1024 rows x 512 B: e2e 830 us in place vs 704 us with a device buffer and
+// one copy). The single-GPU combine K2 has no polls and keeps writing in place.
+bool xchg_in_place(int64_t rows, int64_t d) {
+    static const int64_t cap = [] { const char* e = std::getenv("TD_XCHG_HOST_MAX"); return e ? std::atoll(e) : 65536; }();
+    return rows * d * int64_t(sizeof(float)) <= cap;
+}
+
 // A K2x spin that timed out (a peer never delivered this step's words) stores
 // 1 into the mapped flag; the step's output is then garbage. Reported as an
 // error, after which the exchange must be re-opened on every rank
@@ -1485,8 +1495,8 @@ bool pinned_fast_path(td_context* ctx, int flags, const SplitPlan& plan) {
         (flags & (TD_BF16_OUT | TD_DEBUG_TS)))
         return false;
     if (flags & TD_TIME_PHASES) return false;
-    (void)plan;
     if (ctx->nranks > 1 && !(flags & TD_P2P)) return false;  // the NCCL path ends in K4, not in a signalling K2
+    if (ctx->nranks > 1 && !xchg_in_place(plan.bh_count * plan.group, ctx->d)) return false;
     if (ctx->host_ptr_ok < 0) {
         int uva = 0, reg = 0;
         cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, ctx->device);
@@ -1713,7 +1723,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
     if ((flags & TD_P2P) && ctx->nranks > 1) {
         float* xdst = out;
         if ((flags & TD_HOST_IO) && !tc.fast) {
-            float* m = (flags & TD_BF16_OUT) ? nullptr : mapped_host(ctx, out);
+            float* m = (flags & TD_BF16_OUT) || !xchg_in_place(rows, d) ? nullptr : mapped_host(ctx, out);
             xdst = m ? m : ctx->out;
         }
         if (int rc2 = launch_tree_p2p(ctx, tc, scale, xdst, flags)) return rc2;
@@ -1767,7 +1777,7 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         phase_mark(ctx);
         float* dst = ctx->out;
         if (!(flags & TD_HOST_IO)) dst = out;
-        else if (!(flags & TD_BF16_OUT)) if (float* m = mapped_host(ctx, out)) dst = m;
+        else if (!(flags & TD_BF16_OUT) && xchg_in_place(rows, d)) if (float* m = mapped_host(ctx, out)) dst = m;
         td::XchgArgs xa;
         xa.peers = static_cast<float* const*>(ctx->nx_ptrs.p);
         xa.p = ctx->nranks;
@@ -2244,7 +2254,7 @@ int td_group_tree_decode(td_group* g, const void* q, int64_t n_q, double scale, 
     float* dst0 = out;
     if (host) {
         require_ctx(c0);
-        float* m = mapped_host(c0, out);
+        float* m = xchg_in_place(tc[0].rows, c0->d) ? mapped_host(c0, out) : nullptr;
         dst0 = m ? m : c0->out;
     }
     if (g->shared) {
