@@ -124,3 +124,20 @@ def test_group_over_every_gpu(td, oracle):
         want = full_decode(oracle, qh, n_kv, n, sk, sv, BF16)
         assert rel_err_rows(a.double().cpu().numpy(), want) <= 1e-3
         assert rel_err_rows(h.double().numpy(), want) <= 1e-3
+
+
+def test_group_host_buffers_large_output(td, oracle):
+    """A host-buffer call whose output exceeds what the exchange stores in place
+    (b * n_q * d * 4 > 64 KB): the exchange writes a device buffer, the call copies
+    it once (td_capi.cu xchg_in_place). Pinned and pageable outputs, every row."""
+    import torch
+    b, n_q, n_kv, n, d = 8, 32, 8, 4096 + 3, 128
+    g, q, qh, sk, sv = _group_case(td, oracle, 2, BF16, b, n_q, n_kv, n, d)
+    dev_out = g.tree_decode(q).double().cpu().numpy()
+    pinned = g.tree_decode(q.cpu()).double().numpy()  # the default host output is pinned
+    pageable = torch.empty(b, n_q, d, dtype=torch.float32)
+    g.tree_decode(q.cpu(), out=pageable)
+    g.close()
+    want = full_decode(oracle, qh, n_kv, n, sk, sv, BF16)
+    for got in (dev_out, pinned, pageable.double().numpy()):
+        assert rel_err_rows(got, want) <= 1e-3
