@@ -832,15 +832,19 @@ __global__ void __launch_bounds__(W * 32, 1)
 // K1, fp32 (d = 128): lane j owns dims [4j, 4j+4); per-warp bulk-copy ring.
 // Scores of the 32 tokens of a tile are formed with a butterfly
 // reduce-scatter (31 shuffles for 32 tokens) so lane j ends with token j.
+// The ring holds E half-tile entries (a K or a V tile of T tokens, 16 KB),
+// each with its own mbarrier: half h of the warp's sequence is tile h / 2's
+// K (h even) or V (h odd) and lands in entry h % E. A K entry is refilled as
+// soon as the scores are formed, before P.V waits for its V.
 // =========================================================================
-template <int T, int W, int S, int G>
+template <int T, int W, int E, int G>
 __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     constexpr int D = 128;
     static_assert(T == 32, "one token per lane after the reduce-scatter");
+    static_assert(E >= 2, "a tile's K and V entries are in flight together");
     constexpr int TILE_BYTES = T * D * 4;
-    constexpr int STAGE_BYTES = 2 * TILE_BYTES;
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[W][S];
+    __shared__ uint64_t bars[W][E];
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
 
     const unsigned long long t_start = (a.dbg || a.tl) ? gtimer() : 0ull;
@@ -855,12 +859,12 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     const int64_t nmine = span > warp ? (span - warp + W - 1) / W : 0;
     const int64_t bh_first = x0 / (a.tiles_per_bh > 0 ? a.tiles_per_bh : 1);
     const int64_t rows_total = a.bh_count * a.row_stride;
-    uint8_t* wsm = smem + size_t(warp) * S * STAGE_BYTES;
+    uint8_t* wsm = smem + size_t(warp) * E * TILE_BYTES;
     const float* kg = static_cast<const float*>(a.k);
     const float* vg = static_cast<const float*>(a.v);
 
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[warp][s], 1);
+        for (int s = 0; s < E; ++s) mbar_init(&bars[warp][s], 1);
         mbar_fence_init();
     }
     __syncwarp();
@@ -871,16 +875,20 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         atomicMin(a.tl + 1, gtimer());
     }
     const uint64_t pol = policy_evict_first();
-    auto issue = [&](int64_t kk, int s) {
-        const int64_t x = x0 + warp + kk * W;
+    const int64_t nhalf = 2 * nmine;
+    auto issue = [&](int64_t h) {  // half h into entry h % E
+        const int64_t x = x0 + warp + (h >> 1) * W;
         const int64_t bh = x / a.tiles_per_bh;
         const int64_t row = bh * a.row_stride + (x - bh * a.tiles_per_bh) * T;
         const int64_t avail = rows_total - row;
         const uint32_t bytes = static_cast<uint32_t>((avail < T ? avail : T) * D * 4);
-        uint8_t* kd = wsm + size_t(s) * STAGE_BYTES;
-        mbar_expect_tx(&bars[warp][s], 2 * bytes);
-        bulk_load(kd, kg + row * D, bytes, &bars[warp][s], pol);
-        bulk_load(kd + TILE_BYTES, vg + row * D, bytes, &bars[warp][s], pol);
+        const int e = static_cast<int>(h % E);
+        mbar_expect_tx(&bars[warp][e], bytes);
+        bulk_load(wsm + size_t(e) * TILE_BYTES, ((h & 1) ? vg : kg) + row * D, bytes, &bars[warp][e], pol);
+    };
+    auto wait_half = [&](int64_t h) {
+        mbar_wait(&bars[warp][static_cast<int>(h % E)], static_cast<uint32_t>((h / E) & 1));
+        return reinterpret_cast<const float*>(wsm + size_t(h % E) * TILE_BYTES);
     };
     float qv[G][4], o[G][4], m[G], l[G];
     int64_t cur_bh = -1;
@@ -933,10 +941,8 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         load_q(cur_bh);
     }
     if (lane == 0)
-        for (int s = 0; s < S && s < nmine; ++s) issue(s, s);
+        for (int64_t h = 0; h < E && h < nhalf; ++h) issue(h);
     for (int64_t kk = 0; kk < nmine; ++kk) {
-        const int s = static_cast<int>(kk % S);
-        const uint32_t phase = static_cast<uint32_t>((kk / S) & 1);
         const int64_t x = x0 + warp + kk * W;
         const int64_t bh = x / a.tiles_per_bh;
         const int64_t tok0 = (x - bh * a.tiles_per_bh) * T;
@@ -950,14 +956,14 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
         }
         const int64_t rem = a.t - tok0;
         const int nvalid = rem < T ? static_cast<int>(rem) : T;
-        mbar_wait(&bars[warp][s], phase);
+        const float* ks_ = wait_half(2 * kk);
         if (a.reverse & 2) {  // debug (TD_DEBUG_REVERSE=2): no math, the stream alone
+            wait_half(2 * kk + 1);
             __syncwarp();
-            if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+            if (lane == 0 && 2 * kk + E < nhalf) issue(2 * kk + E);
+            if (lane == 0 && 2 * kk + 1 + E < nhalf) issue(2 * kk + 1 + E);
             continue;
         }
-        const float* ks_ = reinterpret_cast<const float*>(wsm + size_t(s) * STAGE_BYTES);
-        const float* vs_ = ks_ + T * D;
 
         float sc[G];
 #pragma unroll
@@ -997,6 +1003,9 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
             o[h][2] *= cr;
             o[h][3] *= cr;
         }
+        __syncwarp();  // every lane has read the K entry
+        if (lane == 0 && 2 * kk + E < nhalf) issue(2 * kk + E);
+        const float* vs_ = wait_half(2 * kk + 1);
 #pragma unroll 8
         for (int tk = 0; tk < nvalid; ++tk) {
             const float4 vv = reinterpret_cast<const float4*>(vs_ + tk * D)[lane];
@@ -1010,7 +1019,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
             }
         }
         __syncwarp();
-        if (lane == 0 && kk + S < nmine) issue(kk + S, s);
+        if (lane == 0 && 2 * kk + 1 + E < nhalf) issue(2 * kk + 1 + E);
     }
     if (cur_bh >= 0) flush(static_cast<int>(cur_bh - bh_first));
     for (int seg = 0; seg < a.maxseg; ++seg) {
@@ -2194,16 +2203,18 @@ namespace {
 
 constexpr int kBf16Tile = 32;
 constexpr int kF32Tile = 32;
-// k1_f32 geometry (warps x stages of 32-token K+V tiles, 192 KB of stages):
-// TD_F32_CFG = 0 (3 x 2, default), 1 (2 x 3), 2 (6 x 1), 3 (1 x 6)
+// k1_f32 geometry: warps x half-tile ring entries (a 32-token K or V tile, 16 KB).
+// TD_F32_CFG = 0 (4 x 2, default), 1 (2 x 6), 2 (6 x 2), 3 (1 x 12), 4 (4 x 3),
+// 5 (3 x 4: round 1's 3 warps x 2 K+V stages), 6 (5 x 2), 7 (3 x 3).
+// cfg1 (profiles/r2_cfg1/geometry/): 4 x 2 streams 64K fp32 tokens in 17.4 us
+// (ncu, clean L2) against 18.8 for 3 x 4; 6 x 2 and 5 x 2 sit in between.
+constexpr int kF32Warps[8] = {4, 2, 6, 1, 4, 3, 5, 3};
+constexpr int kF32Entries[8] = {2, 6, 2, 12, 3, 4, 2, 3};
 int f32_cfg() {
-    static const int c = [] { const char* e = std::getenv("TD_F32_CFG"); return e ? std::atoi(e) & 3 : 0; }();
+    static const int c = [] { const char* e = std::getenv("TD_F32_CFG"); return e ? std::atoi(e) & 7 : 0; }();
     return c;
 }
-int f32_warps() {
-    static constexpr int w[4] = {3, 2, 6, 1};
-    return w[f32_cfg()];
-}
+int f32_warps() { return kF32Warps[f32_cfg()]; }
 constexpr int kGenTile = 32, kGenWarps = 4;
 constexpr int kSmemBudget = 192 * 1024;  // per CTA, one CTA per SM
 
@@ -2215,7 +2226,7 @@ template <int D>
 size_t bf16_smem() {
     return size_t(bf16_warps(D)) * bf16_stages(D) * bf16_stage_bytes(D) + 1024;
 }
-size_t f32_smem() { return size_t(6) * 2 * kF32Tile * 128 * 4 + 128; }
+size_t f32_smem() { return size_t(kF32Warps[f32_cfg()]) * kF32Entries[f32_cfg()] * kF32Tile * 128 * 4 + 128; }
 
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
@@ -2568,10 +2579,14 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
 #define TD_LAUNCH_F32(GG)                                                   \
     case GG:                                                                \
         switch (f32_cfg()) {                                                \
-        case 1: TD_LAUNCH_F32_WS(GG, 2, 3) break;                           \
-        case 2: TD_LAUNCH_F32_WS(GG, 6, 1) break;                           \
-        case 3: TD_LAUNCH_F32_WS(GG, 1, 6) break;                           \
-        default: TD_LAUNCH_F32_WS(GG, 3, 2) break;                          \
+        case 1: TD_LAUNCH_F32_WS(GG, 2, 6) break;                           \
+        case 2: TD_LAUNCH_F32_WS(GG, 6, 2) break;                           \
+        case 3: TD_LAUNCH_F32_WS(GG, 1, 12) break;                          \
+        case 4: TD_LAUNCH_F32_WS(GG, 4, 3) break;                           \
+        case 5: TD_LAUNCH_F32_WS(GG, 3, 4) break;                           \
+        case 6: TD_LAUNCH_F32_WS(GG, 5, 2) break;                           \
+        case 7: TD_LAUNCH_F32_WS(GG, 3, 3) break;                           \
+        default: TD_LAUNCH_F32_WS(GG, 4, 2) break;                          \
         }                                                                   \
         break;
             TD_LAUNCH_F32(1)
@@ -2713,19 +2728,20 @@ const void* k1_function(const SplitPlan& p) {
         }
     }
     if (p.kernel == 2) {
-        static constexpr int wv[4] = {3, 2, 6, 1}, sv[4] = {2, 3, 1, 6};
-        const int w = wv[f32_cfg()], st = sv[f32_cfg()];
-        if (p.group == 1) {
-            if (w == 3) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 3, 2, 1>);
-            if (w == 2) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 2, 3, 1>);
-            if (w == 6) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 6, 1, 1>);
-            return reinterpret_cast<const void*>(k1_f32<kF32Tile, 1, 6, 1>);
+#define TD_F32_FN(WW, EE) \
+    (p.group == 1 ? reinterpret_cast<const void*>(k1_f32<kF32Tile, WW, EE, 1>) \
+                  : reinterpret_cast<const void*>(k1_f32<kF32Tile, WW, EE, 2>))
+        switch (f32_cfg()) {
+        case 1: return TD_F32_FN(2, 6);
+        case 2: return TD_F32_FN(6, 2);
+        case 3: return TD_F32_FN(1, 12);
+        case 4: return TD_F32_FN(4, 3);
+        case 5: return TD_F32_FN(3, 4);
+        case 6: return TD_F32_FN(5, 2);
+        case 7: return TD_F32_FN(3, 3);
+        default: return TD_F32_FN(4, 2);
         }
-        if (w == 3) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 3, 2, 2>);
-        if (w == 2) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 2, 3, 2>);
-        if (w == 6) return reinterpret_cast<const void*>(k1_f32<kF32Tile, 6, 1, 2>);
-        (void)st;
-        return reinterpret_cast<const void*>(k1_f32<kF32Tile, 1, 6, 2>);
+#undef TD_F32_FN
     }
     return p.dtype == kBF16 ? reinterpret_cast<const void*>(k1_generic<__nv_bfloat16>)
                             : reinterpret_cast<const void*>(k1_generic<float>);
