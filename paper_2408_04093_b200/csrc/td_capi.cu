@@ -235,6 +235,10 @@ struct td_context {
     unsigned done_epoch = 0;
     int host_ptr_ok = -1;             // pinned host pointers usable by kernels as is (UVA), probed once
 
+    // streamed combine (SplitPlan::sflag): flag words and the last launch's epoch
+    DevBuf sflags;
+    unsigned s_epoch = 0;
+
     DevBuf dbg;  // TD_DEBUG_TS stamps
     int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
     float* mapped_for = nullptr;   // this call's host output buffer and its device alias (or null)
@@ -286,6 +290,8 @@ struct td_context {
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         cudaGraphNode_t k1 = nullptr;
+        cudaGraphNode_t k2s = nullptr;  // the streamed split K2 (null without the streamed combine)
+        const unsigned* sflag = nullptr;
         const void* q = nullptr;
         float* out = nullptr;
         double scale = 0.0;
@@ -655,12 +661,38 @@ int plan_for(td_context* ctx, int64_t n_q, int64_t t, SplitPlan& plan, int64_t s
 // launching leaves the parity alone, so the counters at rest stay zero.
 void launched(td_context* ctx, const SplitPlan& plan) {
     if (plan.pool_tiles > 0 && plan.counters == ctx->ctr.p) ctx->kpar = plan.parity ^ 1;
+    if (plan.sflag && plan.sflag == ctx->sflags.p) ctx->s_epoch = plan.sepoch;
     if (plan.app_k && plan.app_k == ctx->pend_k) {
         // the token is in the cache once this split kernel has run; the next K1 must not
         // load its tile before its own wait (the write is not visible to it earlier)
         ctx->pend_k = ctx->pend_v = nullptr;
         ctx->pend_pos = -1;
     }
+}
+
+// Streamed combine for the context's own shard (TD_K2_STREAM, default on): the
+// plan's K1 publishes its states with flags and the split K2 folds them as they
+// arrive (td_kernels.cu stream_fold). Every launch gets a new epoch (committed by
+// launched(); graph replays patch it). Not for worker groups sharing a GPU: their
+// K2 warps would spin next to a peer's K1.
+int stream_setup(td_context* ctx, SplitPlan& plan) {
+    static const bool on = [] { const char* e = std::getenv("TD_K2_STREAM"); return !e || std::atoi(e) != 0; }();
+    plan.sflag = nullptr;
+    if (!on || ctx->shared_device) return TD_OK;
+    SplitPlan probe = plan;
+    probe.sflag = reinterpret_cast<unsigned*>(&probe);  // any non-null pointer: the shape test
+    if (!td::stream_plan(probe)) return TD_OK;
+    const size_t cap = ctx->sflags.cap;
+    TD_CUDA(ctx->sflags.ensure(plan.sflag_words() * sizeof(unsigned)));
+    unsigned ep = ctx->s_epoch + 1;
+    if (ctx->sflags.cap != cap || ep == 0) {  // fresh words (or an epoch wrap): zero, epochs from 1
+        TD_CUDA(cudaMemsetAsync(ctx->sflags.p, 0, ctx->sflags.cap, ctx->stream));
+        ctx->s_epoch = 0;
+        ep = 1;
+    }
+    plan.sflag = static_cast<unsigned*>(ctx->sflags.p);
+    plan.sepoch = ep;
+    return TD_OK;
 }
 
 void phase_begin(td_context* ctx, int flags) {
@@ -1553,6 +1585,7 @@ int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int fl
     tc.rows = ctx->b * n_q;
     if (int rc = ensure_rows(ctx, tc.rows, ctx->d)) return rc;
     if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap, false, true)) return rc;
+    if (int rc = stream_setup(ctx, tc.plan)) return rc;
     int rc = TD_OK;
     if (!q_on_device && pinned_fast_path(ctx, flags, tc.plan)) {
         // the output goes straight into the caller's pinned buffer and the combine
@@ -1637,9 +1670,11 @@ int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, doub
     const bool same = g.exec && g.q == qd && g.out == out && g.scale == scale && g.rows == rows &&
                       g.total == plan.total_tiles && g.per_bh == plan.tiles_per_bh && g.len == ctx->len &&
                       g.cap == ctx->cap && g.ctas == plan.ctas && g.maxseg == plan.maxseg && g.kernel == plan.kernel &&
-                      g.x_table == plan.x_table && g.k == ctx->k.p && g.lse == lse && g.t_safe == plan.t_safe;
+                      g.x_table == plan.x_table && g.k == ctx->k.p && g.lse == lse && g.t_safe == plan.t_safe &&
+                      g.sflag == plan.sflag;
     if (same) {
         TD_CUDA(td::graph_set_k1_epoch(g.exec, g.k1, plan));
+        if (g.k2s) TD_CUDA(td::graph_set_k2_epoch(g.exec, g.k2s, plan));
         launched(ctx, plan);  // (the capture path's run_partial does this)
     } else {
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1679,9 +1714,11 @@ int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, doub
             if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
             cudaKernelNodeParams kp{};
             if (cudaGraphKernelNodeGetParams(node, &kp) == cudaSuccess && kp.func == k1f) g.k1 = node;
+            if (plan.sflag && kp.func == td::k2_stream_function()) g.k2s = node;
         }
         cudaGetLastError();
         if (!g.k1) return set_err(TD_ECUDA, "tree_decode (graph): split kernel node not found");
+        if (td::stream_plan(plan) && !g.k2s) return set_err(TD_ECUDA, "tree_decode (graph): combine node not found");
         g.q = qd;
         g.out = out;
         g.scale = scale;
@@ -1697,6 +1734,7 @@ int tree_nccl_graph(td_context* ctx, const SplitPlan& plan, const void* qd, doub
         g.k = ctx->k.p;
         g.lse = lse;
         g.t_safe = plan.t_safe;
+        g.sflag = plan.sflag;
     }
     TD_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
     ctx->kv_safe = ctx->len;
@@ -1949,6 +1987,7 @@ int td_ring_decode(td_context* ctx, const void* q, int64_t n_q, double scale, fl
     // own chunk first: root = parts[w]
     SplitPlan plan;
     if ((rc = plan_for(ctx, n_q, ctx->len, plan, ctx->cap))) return rc;
+    if ((rc = stream_setup(ctx, plan))) return rc;  // as tree_decode: bitwise the same partial
     if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok,
                           ctx->r_max, ctx->r_lse, ctx->r_out, timed)))
         return rc;

@@ -86,6 +86,14 @@ struct SplitPlan {
     const void* app_k = nullptr;
     const void* app_v = nullptr;
     int64_t app_pos = -1;
+    // streamed combine (td_capi.cu stream_setup; stream_plan): K1 publishes each warp's
+    // static state and each chunk state with a flag word = sepoch once written, and
+    // the split K2 folds them as they arrive instead of after K1's grid completes.
+    // Flags: [ctas * warps] static, then [bh_count][fslots] chunks; sepoch is new
+    // for every launch of the buffer (graph replays patch it, graph_set_k*_epoch)
+    unsigned* sflag = nullptr;
+    unsigned sepoch = 0;
+    size_t sflag_words() const { return size_t(ctas) * size_t(warps) + size_t(bh_count) * size_t(fslots); }
     // launch K1 as a programmatic dependent of the preceding kernel (off when several
     // contexts share one GPU and a peer's K1 must get SMs while this one's exchange waits)
     bool pdl = true;
@@ -99,6 +107,9 @@ struct SplitPlan {
     // [2 parities][bh_count] pool chunk counters, then [2][bh_count] foreign-slot counters
     size_t counters_bytes() const { return sizeof(unsigned) * 4 * size_t(bh_count > 0 ? bh_count : 1); }
 };
+
+// Whether launches of the plan use the streamed combine (SplitPlan::sflag).
+bool stream_plan(const SplitPlan& p);
 
 // TD_DEBUG_TS: a one-thread kernel writing %globaltimer to *p (front-end gaps).
 cudaError_t launch_stamp(unsigned long long* p, cudaStream_t stream);
@@ -157,9 +168,12 @@ cudaError_t launch_decode_exchange(const SplitPlan& plan, const void* q, const v
 
 // CUDA-graph replay of a captured step: the split kernel's entry point for `plan`
 // (to find its node) and an update of that node's per-launch state -- the SM
-// affinity claim epoch -- in an instantiated graph.
+// affinity claim epoch and the streamed-combine epoch -- in an instantiated graph;
+// likewise the streamed split K2 (partial tail) and its epoch.
 const void* k1_function(const SplitPlan& plan);
 cudaError_t graph_set_k1_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const SplitPlan& plan);
+const void* k2_stream_function();
+cudaError_t graph_set_k2_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const SplitPlan& plan);
 
 // Builds the 2-D tensor map used by the bf16 kernel over rows x d elements.
 bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, int tile_rows,

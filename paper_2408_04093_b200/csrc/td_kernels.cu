@@ -115,6 +115,12 @@ struct K1Args {
     unsigned* done_ctr;
     unsigned* done_flag;
     unsigned done_epoch;
+    // streamed combine (SplitPlan::sflag): k1_bf16 publishes every warp's static
+    // state (flag c * W + warp) and every chunk state (flag ctas * W + bh * fslots + k)
+    // by storing sepoch once it is written; the split K2 folds them as they arrive
+    unsigned* sflag;
+    unsigned sepoch;
+    int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
     Tail tail;
 };
 
@@ -586,6 +592,12 @@ __global__ void __launch_bounds__(W * 32, 1)
         m0 = m1 = -CUDART_INF_F;
         l0 = l1 = 0.f;
     };
+    // every lane's state stores, then the flag (release at gpu scope)
+    auto publish = [&](unsigned* f) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(f, a.sepoch);
+    };
     // state -> this warp's slot (c, warp, phase, seg); phase 1 holds pool tiles
     auto flush = [&](int64_t bh, int rec) {
         float la = l0, lb = l1;
@@ -626,6 +638,25 @@ __global__ void __launch_bounds__(W * 32, 1)
                 so[hB * D + d0 + 8] = o[md][3];
             }
         }
+        if (a.sflag && rec >= 2) publish(a.sflag + int64_t(a.ctas) * W + bh * a.fslots + (rec - 2));
+    };
+    // streamed combine: the warp's static part is done -- its untouched static
+    // slots become empty partials and the warp's flag is published; the split K2,
+    // resident from here on, folds these states while the chunks still stream
+    bool s_pub = a.sflag == nullptr;
+    auto publish_static = [&]() {
+        for (int seg = 0; seg < a.maxseg; ++seg) {
+            if (flushed & (1ull << (2 * seg))) continue;
+            const int64_t slot = (int64_t(c) * a.slot_warps + warp) * a.maxseg + seg;
+            for (int h = lane; h < a.group; h += 32) {
+                a.slot_m[slot * a.group + h] = -CUDART_INF_F;
+                a.slot_l[slot * a.group + h] = 0.f;
+            }
+            flushed |= 1ull << (2 * seg);
+        }
+        publish(a.sflag + int64_t(c) * W + warp);
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        s_pub = true;
     };
 
     // the first static tile's q before the rest of the first tiles are requested:
@@ -641,6 +672,14 @@ __global__ void __launch_bounds__(W * 32, 1)
         const int64_t tok0 = st_tb[warp][s] * T;
         const int rec = st_rec[warp][s];
         if (bh != cur_bh || rec != cur_rec) {
+            if (!s_pub && rec >= 2) {  // the first chunk: the static states are final
+                if (cur_bh >= 0) {
+                    flush(cur_bh, cur_rec);
+                    reset();
+                    cur_bh = -1;
+                }
+                publish_static();
+            }
             if (cur_bh >= 0) {
                 flush(cur_bh, cur_rec);
                 reset();
@@ -788,6 +827,11 @@ __global__ void __launch_bounds__(W * 32, 1)
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (cur_bh >= 0) flush(cur_bh, cur_rec);
+    if (a.sflag) {  // streamed combine: K2 merges the warp states themselves
+        if (!s_pub) publish_static();
+        if (a.tl && lane == 0) atomicMax(a.tl + 2, gtimer());
+        return;
+    }
     // untouched slots are empty partials (m = -inf)
     const int phases = a.slot_warps == W ? 1 : 2;
     for (int seg = 0; seg < a.maxseg; ++seg)
@@ -1520,14 +1564,124 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
 // 0 combines the WS partials from shared memory. One warp walking 148
 // candidates took ~7 us; this takes about one round trip per warp plus the
 // shared-memory combine. Same arithmetic per column as k2_combine_cols.
-template <int Q, int WS>
+// ---- streamed combine (K1Args::sflag) --------------------------------------
+// Waits until every lane's candidate flag (idx >= 0) carries this launch's
+// epoch; bounded (~1 s of clocks, then *err if given) so a missing state cannot
+// hang the GPU. Afterwards every lane may read every lane's candidate.
+__device__ __forceinline__ void wait_flags(const unsigned* f, int idx, unsigned ep, int spin, int* err) {
+    const long long t0 = clock64();
+    for (;;) {
+        const bool ok = idx < 0 || ld_acquire_gpu(f + idx) == ep;
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (clock64() - t0 > (1ll << 31)) {
+            if (err) *reinterpret_cast<volatile int*>(err) = 1;
+            break;
+        }
+        __nanosleep(spin);
+    }
+    __syncwarp();
+    __threadfence();  // the states behind every lane's flag, for every lane
+}
+
+// One online-softmax fold of n <= NB candidate states into the warp's running
+// (M, L, acc) of column col: lane i < n holds candidate i's element offset.
+// The loads of all n states are issued before any is used (one L2 round trip).
+template <int NB>
+__device__ __forceinline__ void fold_batch(const float* bm, const float* bl, const float* bo, int off, int n,
+                                           int col, int D, float& M, float& L, float& acc) {
+    const int lane = threadIdx.x & 31;
+    float ml = -CUDART_INF_F, ll = 0.f;
+    if (lane < n) {
+        ml = __ldcg(bm + off);
+        ll = __ldcg(bl + off);
+    }
+    float ov[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int ok = __shfl_sync(0xffffffffu, off, k);
+        ov[k] = (k < n && col < D) ? __ldcg(bo + int64_t(ok) * D + col) : 0.f;
+    }
+    float Mb = ml;
+#pragma unroll
+    for (int o2 = 16; o2 >= 1; o2 >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, o2));
+    const float Mn = fmaxf(M, Mb);
+    const float cs = M == -CUDART_INF_F ? 0.f : fast_exp2(M - Mn);
+    L *= cs;
+    acc *= cs;
+    const float e_l = ml == -CUDART_INF_F ? 0.f : fast_exp2(ml - Mn);
+    float ls = e_l * ll;
+#pragma unroll
+    for (int o2 = 16; o2 >= 1; o2 >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o2);
+    L += ls;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const float e = __shfl_sync(0xffffffffu, e_l, k);
+        acc = fmaf(e, e != 0.f ? ov[k] : 0.f, acc);
+    }
+    M = Mn;
+}
+
+__device__ __forceinline__ void fold_any(const float* bm, const float* bl, const float* bo, int off, int n, int col,
+                                         int D, float& M, float& L, float& acc) {
+    if (n <= 8) fold_batch<8>(bm, bl, bo, off, n, col, D, M, L, acc);
+    else if (n <= 16) fold_batch<16>(bm, bl, bo, off, n, col, D, M, L, acc);
+    else fold_batch<32>(bm, bl, bo, off, n, col, D, M, L, acc);
+}
+
+// Warp `warp` of a split K2 block folds its share of row r's candidates as K1
+// publishes them: the static warp states (CTAs c_lo.. of the cover, every warp;
+// segment seg_lo in the first CTA, 0 after) in contiguous shares, then the chunk
+// states k = warp, warp + WS, ... (the grid-wide queue completes chunks in about
+// k order, so the last ones spread over the warps). The assignment and the order
+// are fixed: results stay bitwise reproducible.
+template <int WS>
+__device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Cover& cv, int col, float& M,
+                                            float& L, float& acc, int* err) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = a.group, W = a.slot_warps, D = a.d;
+    const int h = static_cast<int>(r % g);
+    const int64_t bh = r / g;
+    const int ns = cv.S * W;
+    const int s_lo = ns * warp / WS, s_hi = ns * (warp + 1) / WS;
+    for (int i0 = s_lo; i0 < s_hi; i0 += 32) {
+        const int n = min(32, s_hi - i0);
+        int off = 0, fi = -1;
+        if (lane < n) {
+            const int i = i0 + lane, cw = i / W;
+            const int64_t cc = cv.c_lo + cw;
+            const int64_t slot = (cc * W + (i - cw * W)) * a.maxseg + (cw == 0 ? cv.seg_lo : 0);
+            off = static_cast<int>(slot * g + h);
+            fi = static_cast<int>(cc * W + (i - cw * W));
+        }
+        wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
+        fold_any(a.slot_m, a.slot_l, a.slot_o, off, n, col, D, M, L, acc);
+    }
+    const int nf = cv.nf;
+    const int nc = nf > warp ? (nf - warp + WS - 1) / WS : 0;
+    for (int j0 = 0; j0 < nc; j0 += 32) {
+        const int n = min(32, nc - j0);
+        int off = 0, fi = -1;
+        if (lane < n) {
+            const int64_t fs = bh * a.fslots + warp + int64_t(j0 + lane) * WS;
+            off = static_cast<int>(fs * g + h);
+            fi = static_cast<int>(int64_t(a.ctas) * W + fs);
+        }
+        wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
+        fold_any(a.fslot_m, a.fslot_l, a.fslot_o, off, n, col, D, M, L, acc);
+    }
+}
+
+template <int Q, int WS, bool SF = false>
 __global__ void __launch_bounds__(32 * WS) k2_combine_split(const K1Args a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __shared__ float sm_m[WS], sm_l[WS], sm_o[WS][32];
     const int64_t rows = a.bh_count * a.group, units = rows * Q;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Cover cv0 = blockIdx.x < units ? cover_of(a, (int64_t(blockIdx.x) / Q) / a.group) : Cover{};
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // streamed combine: no grid-completion wait before the merge (the states are
+    // awaited one by one); the other parity's counters were last used by the
+    // previous K1, which completed before this grid's K1 passed its own wait
+    if constexpr (!SF) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
              i += int64_t(gridDim.x) * blockDim.x) {
@@ -1549,7 +1703,8 @@ __global__ void __launch_bounds__(32 * WS) k2_combine_split(const K1Args a) {
         auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
         const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
         float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
-        for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, nullptr);
+        for (int i0 = i_lo; !SF && i0 < i_hi; i0 += 32) {
             const int n = min(32, i_hi - i0);
             float ml = -CUDART_INF_F, ll = 0.f;
             if (lane < n) {
@@ -1610,6 +1765,7 @@ __global__ void __launch_bounds__(32 * WS) k2_combine_split(const K1Args a) {
         }
         __syncthreads();
     }
+    if constexpr (SF) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after K1
     if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
     signal_done(a);
 }
@@ -1818,7 +1974,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_exchange(const K1Args a) {
 // quarter) block, then warp 0 pushes the row's LL words into every peer and,
 // after all of this block's units are pushed, polls and combines them like
 // k2_exchange (one column per lane).
-template <int Q, int WS>
+template <int Q, int WS, bool SF = false>
 __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int PMAX = 8;
@@ -1832,7 +1988,7 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
     const uint2* own = reinterpret_cast<uint2* const*>(x.peers)[x.rank];
     uint2* const* peers = reinterpret_cast<uint2* const*>(x.peers);
     const Cover cv0 = blockIdx.x < units ? cover_of(a, (int64_t(blockIdx.x) / Q) / a.group) : Cover{};
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (!SF) asm volatile("griddepcontrol.wait;" ::: "memory");  // (streamed: see k2_combine_split)
     if (a.pool_tiles > 0)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.bh_count;
              i += int64_t(gridDim.x) * blockDim.x) {
@@ -1855,7 +2011,8 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
         auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
         const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
         float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
-        for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, x.error);
+        for (int i0 = i_lo; !SF && i0 < i_hi; i0 += 32) {
             const int n = min(32, i_hi - i0);
             float ml = -CUDART_INF_F, ll = 0.f;
             if (lane < n) {
@@ -1984,6 +2141,7 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
             if (col < D) a.tail.out[orow * D + col] = num / den;
         }
     }
+    if constexpr (SF) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after K1
     if (a.tl && lane == 0) atomicMax(a.tl + 3, gtimer());
     signal_done(a);
 }
@@ -2228,6 +2386,16 @@ size_t bf16_smem() {
 }
 size_t f32_smem() { return size_t(kF32Warps[f32_cfg()]) * kF32Entries[f32_cfg()] * kF32Tile * 128 * 4 + 128; }
 
+}  // namespace
+
+// The streamed combine applies to the bf16 kernel with the deterministic chunk pool
+// (per-warp static states, one state per chunk) and d = 128 (the split K2).
+bool stream_plan(const SplitPlan& p) {
+    return p.sflag && p.kernel == 1 && p.dpool && p.fslots > 0 && p.d == 128 && !p.dbg && p.slot_warps == p.warps;
+}
+
+namespace {
+
 K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
                  void* ws) {
     K1Args a{};
@@ -2280,6 +2448,10 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.app_pos = p.app_pos;
     a.done_flag = p.done_flag;
     a.done_epoch = p.done_epoch;
+    a.sflag = stream_plan(p) ? p.sflag : nullptr;
+    a.sepoch = p.sepoch;
+    static const int sspin = [] { const char* e = std::getenv("TD_K2_STREAM_SLEEP"); return e ? std::atoi(e) : 64; }();
+    a.sspin = sspin;
     if (p.pool_tiles > 0) {
         unsigned* cnt = p.counters;  // [2 parities][bh_count] pool, then [2][bh_count] foreign
         a.pool_ctr = cnt + p.parity * p.bh_count;
@@ -2655,9 +2827,14 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
     // few rows with many candidate states each (e.g. one row over every CTA): split
     // each (row, quarter)'s candidates over the warps of a block
     // CTAs covering a row, plus the chunk states of the deterministic pool
-    const int64_t cands = (a.bh_count > 0 ? int64_t(a.ctas) / a.bh_count + 2 : 0) + (a.dpool ? a.fslots : 0);
-    static const int split = [] { const char* e = std::getenv("TD_K2_SPLIT"); return e ? std::atoi(e) : 1; }();
-    if (split && exchange && a.d == 128 && force_w == 0 && cands > 32 && !a.dbg) {
+    // (streamed combine: K2 merges every warp's state, and only the split kernels can)
+    const bool stream = a.sflag != nullptr;
+    const int64_t cands = (a.bh_count > 0 ? int64_t(a.ctas) / a.bh_count + 2 : 0) * (stream ? a.slot_warps : 1) +
+                          (a.dpool ? a.fslots : 0);
+    static const int split_env = [] { const char* e = std::getenv("TD_K2_SPLIT"); return e ? std::atoi(e) : 1; }();
+    const bool split = stream || (split_env && force_w == 0 && cands > 32 && !a.dbg);
+    if (stream && a.d != 128) return cudaErrorInvalidValue;
+    if (split && exchange && a.d == 128) {
         const int64_t units = rows * 4;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(units < limit ? units : limit));
@@ -2667,6 +2844,11 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (stream) {
+            cfg.blockDim = dim3(32 * 8);
+            if (cudaError_t e = prefer_max_smem(k2_exchange_split<4, 8, true>)) return e;
+            return cudaLaunchKernelEx(&cfg, k2_exchange_split<4, 8, true>, a);
+        }
         if (cands > 128) {
             cfg.blockDim = dim3(32 * 8);
             if (cudaError_t e = prefer_max_smem(k2_exchange_split<4, 8>)) return e;
@@ -2676,7 +2858,7 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
         if (cudaError_t e = prefer_max_smem(k2_exchange_split<4, 4>)) return e;
         return cudaLaunchKernelEx(&cfg, k2_exchange_split<4, 4>, a);
     }
-    if (split && !exchange && a.d == 128 && force_w == 0 && cands > 32 && !a.dbg) {
+    if (split && !exchange && a.d == 128) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(rows * 4 < limit ? rows * 4 : limit));
         cfg.stream = st;
@@ -2685,6 +2867,11 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (stream) {
+            cfg.blockDim = dim3(32 * 8);
+            if (cudaError_t e = prefer_max_smem(k2_combine_split<4, 8, true>)) return e;
+            return cudaLaunchKernelEx(&cfg, k2_combine_split<4, 8, true>, a);
+        }
         if (cands > 128) {
             cfg.blockDim = dim3(32 * 8);
             if (cudaError_t e = prefer_max_smem(k2_combine_split<4, 8>)) return e;
@@ -2753,11 +2940,25 @@ cudaError_t graph_set_k1_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const
     if (e != cudaSuccess) return e;
     K1Args a = *static_cast<const K1Args*>(kp.kernelParams[0]);
     a.epoch = p.epoch;
+    a.sepoch = p.sepoch;
     void* args[3] = {&a, nullptr, nullptr};
     if (p.kernel == 1) {  // k1_bf16(K1Args, CUtensorMap, CUtensorMap)
         args[1] = kp.kernelParams[1];
         args[2] = kp.kernelParams[2];
     }
+    kp.kernelParams = args;
+    return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
+}
+
+const void* k2_stream_function() { return reinterpret_cast<const void*>(k2_combine_split<4, 8, true>); }
+
+cudaError_t graph_set_k2_epoch(cudaGraphExec_t exec, cudaGraphNode_t node, const SplitPlan& p) {
+    cudaKernelNodeParams kp{};
+    cudaError_t e = cudaGraphKernelNodeGetParams(node, &kp);
+    if (e != cudaSuccess) return e;
+    K1Args a = *static_cast<const K1Args*>(kp.kernelParams[0]);
+    a.sepoch = p.sepoch;
+    void* args[1] = {&a};
     kp.kernelParams = args;
     return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
 }

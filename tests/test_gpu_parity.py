@@ -437,6 +437,30 @@ def test_cross_row_stealing_parity(lib):
     assert r.returncode == 0, r.stderr[-3000:]
 
 
+def test_streamed_combine_matches_cta_merge(lib, tmp_path):
+    """The streamed combine (default: K2 folds K1's warp and chunk states as they
+    are published) against the CTA-merge combine (TD_K2_STREAM=0): each is bitwise
+    reproducible across calls, entry points and buffers, matches the oracle, and
+    the two agree to fp32 regrouping."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dirs = {}
+    for mode in ("1", "0"):
+        d = tmp_path / f"mode{mode}"
+        d.mkdir()
+        env = dict(os.environ, TD_STREAM_CHECK_MODE=mode)
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "stream_check.py"), str(d)],
+                           capture_output=True, text=True, timeout=600, env=env, cwd=root)
+        print(r.stdout[-2000:])
+        assert r.returncode == 0, r.stderr[-3000:]
+        dirs[mode] = d
+    for f in sorted(os.listdir(dirs["1"])):
+        a, b = np.load(dirs["1"] / f), np.load(dirs["0"] / f)
+        assert rel_err(a, b) <= 5e-6, f
+
+
 def test_worker_place_matches_generate(td, oracle):
     import torch
     q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
