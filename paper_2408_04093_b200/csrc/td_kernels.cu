@@ -121,6 +121,7 @@ struct K1Args {
     unsigned* sflag;
     unsigned sepoch;
     int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
+    int spoll;  // 1: one warp per K2 block polls the chunk flags (TD_K2_STREAM_POLL)
     Tail tail;
 };
 
@@ -1657,6 +1658,14 @@ __device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Co
         fold_any(a.slot_m, a.slot_l, a.slot_o, off, n, col, D, M, L, acc);
     }
     const int nf = cv.nf;
+    if (a.spoll) {  // warp 0 alone polls the row's chunk flags; the others wait at the barrier
+        if (warp == 0)
+            for (int k0 = 0; k0 < nf; k0 += 32)
+                wait_flags(a.sflag, k0 + lane < nf ? static_cast<int>(int64_t(a.ctas) * W + bh * a.fslots + k0 + lane) : -1,
+                           a.sepoch, a.sspin, err);
+        __syncthreads();
+        __threadfence();
+    }
     const int nc = nf > warp ? (nf - warp + WS - 1) / WS : 0;
     for (int j0 = 0; j0 < nc; j0 += 32) {
         const int n = min(32, nc - j0);
@@ -1666,7 +1675,7 @@ __device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Co
             off = static_cast<int>(fs * g + h);
             fi = static_cast<int>(int64_t(a.ctas) * W + fs);
         }
-        wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
+        if (!a.spoll) wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
         fold_any(a.fslot_m, a.fslot_l, a.fslot_o, off, n, col, D, M, L, acc);
     }
 }
@@ -2452,6 +2461,8 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.sepoch = p.sepoch;
     static const int sspin = [] { const char* e = std::getenv("TD_K2_STREAM_SLEEP"); return e ? std::atoi(e) : 64; }();
     a.sspin = sspin;
+    static const int spoll = [] { const char* e = std::getenv("TD_K2_STREAM_POLL"); return e ? std::atoi(e) : 0; }();
+    a.spoll = spoll;
     if (p.pool_tiles > 0) {
         unsigned* cnt = p.counters;  // [2 parities][bh_count] pool, then [2][bh_count] foreign
         a.pool_ctr = cnt + p.parity * p.bh_count;

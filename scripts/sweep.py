@@ -72,6 +72,7 @@ def main():
     scratch = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
     sink = torch.empty((), dtype=torch.float32, device="cuda")
     rows, lines = [], []
+    first = True
     for n in [int(x) for x in args.seq.split(",")]:
         if n < world:
             continue
@@ -84,7 +85,9 @@ def main():
             variants += [("tree", "p2p", _capi.TD_P2P, args.steps), ("ring", "nccl", 0, args.ring_steps)]
         for algo, comb, flags, steps in variants:
             fn = w.tree_decode_async if algo == "tree" else w.ring_decode_async
-            for _ in range(args.warmup):
+            # the first point also pays one-time costs (NCCL's lazily loaded kernels,
+            # connection setup): it gets a longer warm-up
+            for _ in range(args.warmup if not first else max(args.warmup, 30)):
                 fn(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags)
             barrier()
             if world > 1:  # release every rank's first step together (see bench.align_streams)
@@ -115,6 +118,7 @@ def main():
                        "l2": "flushed" if flush else "inputs > L2"}
                 rows.append(rec)
                 print(json.dumps(rec), flush=True)
+        first = False
     if rank == 0:
         for comb in ("nccl", "p2p"):
             sel = [r for c, r in lines if c == comb or (comb == "p2p" and r.algo == "ring")]
