@@ -235,9 +235,11 @@ struct td_context {
     unsigned done_epoch = 0;
     int host_ptr_ok = -1;             // pinned host pointers usable by kernels as is (UVA), probed once
 
-    // streamed combine (SplitPlan::sflag): flag words and the last launch's epoch
+    // streamed combine (SplitPlan::sflag): flag words, the last launch's epoch and the
+    // timeout word (mapped pinned host memory)
     DevBuf sflags;
     unsigned s_epoch = 0;
+    int* s_err = nullptr;
 
     DevBuf dbg;  // TD_DEBUG_TS stamps
     int64_t tl_count = -1;  // TD_DEBUG_TIMELINE: calls stamped so far (-1: not initialised)
@@ -690,9 +692,23 @@ int stream_setup(td_context* ctx, SplitPlan& plan) {
         ctx->s_epoch = 0;
         ep = 1;
     }
+    if (!ctx->s_err) {
+        TD_CUDA(cudaHostAlloc(&ctx->s_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+        *reinterpret_cast<volatile int*>(ctx->s_err) = 0;
+    }
     plan.sflag = static_cast<unsigned*>(ctx->sflags.p);
     plan.sepoch = ep;
+    plan.serr = ctx->s_err;
     return TD_OK;
+}
+
+// A streamed combine that waited ~1 s for a split-kernel state which never came
+// (the split kernel failed): the step's output is invalid. Reported by the next
+// call, or by this call when it synchronised (host buffers).
+int stream_failed(td_context* ctx) {
+    if (!ctx->s_err || !*reinterpret_cast<volatile int*>(ctx->s_err)) return TD_OK;
+    *reinterpret_cast<volatile int*>(ctx->s_err) = 0;
+    return set_err(TD_ECUDA, "tree_decode: the combine kernel timed out waiting for the split kernel's states");
 }
 
 void phase_begin(td_context* ctx, int flags) {
@@ -1131,8 +1147,10 @@ int td_destroy(td_context* ctx) {
     ctx->xbuf.release();
     ctx->x_ptrs.release();
     if (ctx->x_err) cudaFreeHost(ctx->x_err);
+    if (ctx->s_err) cudaFreeHost(ctx->s_err);
     if (ctx->done_host) cudaFreeHost(ctx->done_host);
     ctx->sig.release();
+    ctx->sflags.release();
     ctx->ctr.release();
     ctx->dbg.release();
     ctx->tlbuf.release();
@@ -1584,6 +1602,7 @@ int tree_begin(td_context* ctx, const void* q, int64_t n_q, int strategy, int fl
     ctx->last_kv_bytes = 0.0;
     tc.rows = ctx->b * n_q;
     if (int rc = ensure_rows(ctx, tc.rows, ctx->d)) return rc;
+    if (int rc = stream_failed(ctx)) return rc;  // an earlier asynchronous step
     if (int rc = plan_for(ctx, n_q, ctx->len, tc.plan, ctx->cap, false, true)) return rc;
     if (int rc = stream_setup(ctx, tc.plan)) return rc;
     int rc = TD_OK;
@@ -1800,9 +1819,13 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
                              td::dtype_bytes(ctx->dtype);
         ctx->last_split_kernel = plan.kernel;
-        if (!tc.fast) return deliver_out(ctx, dst, rows, out, flags);
+        if (!tc.fast) {
+            if (int rc2 = deliver_out(ctx, dst, rows, out, flags)) return rc2;
+            return (flags & TD_HOST_IO) ? stream_failed(ctx) : TD_OK;  // synchronised: this step's verdict
+        }
         if (int rc2 = note_table_use(ctx)) return rc2;
-        return wait_done(ctx, plan.done_epoch);
+        if (int rc2 = wait_done(ctx, plan.done_epoch)) return rc2;
+        return stream_failed(ctx);
     }
     if (flags & TD_NCCL_DEVICE) {
         // K1 -> K2 (lse, out per row) -> K2n: allreduce(max), n/d numerators,

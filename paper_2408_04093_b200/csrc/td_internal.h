@@ -93,6 +93,7 @@ struct SplitPlan {
     // for every launch of the buffer (graph replays patch it, graph_set_k*_epoch)
     unsigned* sflag = nullptr;
     unsigned sepoch = 0;
+    int* serr = nullptr;  // mapped host word a streamed K2 sets when it gives up waiting (~1 s)
     size_t sflag_words() const { return size_t(ctas) * size_t(warps) + size_t(bh_count) * size_t(fslots); }
     // launch K1 as a programmatic dependent of the preceding kernel (off when several
     // contexts share one GPU and a peer's K1 must get SMs while this one's exchange waits)

@@ -122,6 +122,7 @@ struct K1Args {
     unsigned sepoch;
     int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
     int spoll;  // 1: one warp per K2 block polls the chunk flags (TD_K2_STREAM_POLL)
+    int* serr;  // set when a streamed K2 gave up waiting for a state (mapped host memory)
     Tail tail;
 };
 
@@ -655,7 +656,8 @@ __global__ void __launch_bounds__(W * 32, 1)
             }
             flushed |= 1ull << (2 * seg);
         }
-        publish(a.sflag + int64_t(c) * W + warp);
+        if (!((a.reverse & 4) && c == 0 && warp == 0))  // debug (TD_DEBUG_REVERSE=4): one state never published
+            publish(a.sflag + int64_t(c) * W + warp);
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         s_pub = true;
     };
@@ -1712,7 +1714,7 @@ __global__ void __launch_bounds__(32 * WS) k2_combine_split(const K1Args a) {
         auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
         const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
         float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
-        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, nullptr);
+        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, a.serr);
         for (int i0 = i_lo; !SF && i0 < i_hi; i0 += 32) {
             const int n = min(32, i_hi - i0);
             float ml = -CUDART_INF_F, ll = 0.f;
@@ -2020,7 +2022,7 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
         auto off_of = [&](int i) { return i >= S ? fb + (i - S) * g : (i == 0 ? b0 : b1 + (i - 1) * st); };
         const int i_lo = static_cast<int>(int64_t(T) * warp / WS), i_hi = static_cast<int>(int64_t(T) * (warp + 1) / WS);
         float M = -CUDART_INF_F, L = 0.f, acc = 0.f;
-        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, x.error);
+        if constexpr (SF) stream_fold<WS>(a, r, cv, col, M, L, acc, a.serr);
         for (int i0 = i_lo; !SF && i0 < i_hi; i0 += 32) {
             const int n = min(32, i_hi - i0);
             float ml = -CUDART_INF_F, ll = 0.f;
@@ -2458,6 +2460,7 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.done_flag = p.done_flag;
     a.done_epoch = p.done_epoch;
     a.sflag = stream_plan(p) ? p.sflag : nullptr;
+    a.serr = p.serr;
     a.sepoch = p.sepoch;
     static const int sspin = [] { const char* e = std::getenv("TD_K2_STREAM_SLEEP"); return e ? std::atoi(e) : 64; }();
     a.sspin = sspin;

@@ -461,6 +461,20 @@ def test_streamed_combine_matches_cta_merge(lib, tmp_path):
         assert rel_err(a, b) <= 5e-6, f
 
 
+def test_streamed_combine_timeout_is_an_error(lib):
+    """A split-kernel state that is never published (debug hook) makes the streamed
+    combine give up after ~1 s and the call fail with TD_ECUDA."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TD_DEBUG_REVERSE="4")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "stream_timeout_check.py")], capture_output=True,
+                       text=True, timeout=300, env=env, cwd=root)
+    print(r.stdout[-2000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+
+
 def test_worker_place_matches_generate(td, oracle):
     import torch
     q, k, v = make_inputs(oracle, 21, 2, 8, 4, 3000, 128, BF16)
