@@ -88,6 +88,9 @@ def main():
             # the first point also pays one-time costs (NCCL's lazily loaded kernels,
             # connection setup): it gets a longer warm-up
             for _ in range(args.warmup if not first else max(args.warmup, 30)):
+                if flush:  # (the flush's own first-use costs stay out of the timed steps too)
+                    with torch.cuda.stream(stream):
+                        torch.sum(scratch, dim=0, out=sink)
                 fn(q.data_ptr(), n_q, out.data_ptr(), 1.0, flags)
             barrier()
             if world > 1:  # release every rank's first step together (see bench.align_streams)
