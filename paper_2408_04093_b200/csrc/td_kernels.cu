@@ -888,7 +888,9 @@ __global__ void __launch_bounds__(W * 32, 1)
 template <int T, int W, int E, int G>
 __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
     constexpr int D = 128;
-    static_assert(T == 32, "one token per lane after the reduce-scatter");
+    // T = 32: lane j ends the reduce-scatter with token j; T = 16: lanes j and j + 16
+    // both hold token j (the half-warp butterfly plus one exchange across halves)
+    static_assert(T == 32 || T == 16, "32 or 16 tokens per tile");
     static_assert(E >= 2, "a tile's K and V entries are in flight together");
     constexpr int TILE_BYTES = T * D * 4;
     extern __shared__ uint8_t smem_raw[];
@@ -1024,7 +1026,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
             }
             // reduce-scatter: after step k, lane bit k selects the kept half
 #pragma unroll
-            for (int k = 16; k >= 1; k >>= 1) {
+            for (int k = T / 2; k >= 1; k >>= 1) {
                 const bool up = (lane & k) != 0;
 #pragma unroll
                 for (int i = 0; i < k; ++i) {
@@ -1033,7 +1035,8 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
                     part[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
                 }
             }
-            sc[h] = lane < nvalid ? part[0] * a.scale_log2 : -CUDART_INF_F;
+            if (T == 16) part[0] += __shfl_xor_sync(0xffffffffu, part[0], 16);  // the other half-warp's dims
+            sc[h] = (lane % T) < nvalid ? part[0] * a.scale_log2 : -CUDART_INF_F;
         }
         float p[G];
 #pragma unroll
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__(W * 32, 1) k1_f32(const K1Args a) {
             const float cr = fast_exp2(m[h] - mn);
             m[h] = mn;
             p[h] = fast_exp2(sc[h] - mn);
-            l[h] = l[h] * cr + p[h];
+            l[h] = l[h] * cr + (lane < T ? p[h] : 0.f);  // (T = 16: each token's p sits on two lanes)
             o[h][0] *= cr;
             o[h][1] *= cr;
             o[h][2] *= cr;
@@ -2440,14 +2443,14 @@ __global__ void k6_seeded_fill(int dtype, void* dst, uint64_t seed, double half_
 namespace {
 
 constexpr int kBf16Tile = 32;
-constexpr int kF32Tile = 32;
-// k1_f32 geometry: warps x half-tile ring entries (a 32-token K or V tile, 16 KB).
-// TD_F32_CFG = 0 (4 x 2, default), 1 (2 x 6), 2 (6 x 2), 3 (1 x 12), 4 (4 x 3),
-// 5 (3 x 4: round 1's 3 warps x 2 K+V stages), 6 (5 x 2), 7 (3 x 3).
-// cfg1 (profiles/r2_cfg1/geometry/): 4 x 2 streams 64K fp32 tokens in 17.4 us
-// (ncu, clean L2) against 18.8 for 3 x 4; 6 x 2 and 5 x 2 sit in between.
-constexpr int kF32Warps[8] = {4, 2, 6, 1, 4, 3, 5, 3};
-constexpr int kF32Entries[8] = {2, 6, 2, 12, 3, 4, 2, 3};
+// k1_f32 geometry: tokens per tile x warps x ring entries (a K or a V tile each).
+// TD_F32_CFG = 0 (32 x 4 x 2, default), 1 (32 x 2 x 6), 2 (32 x 6 x 2), 3 (16 x 4 x 4),
+// 4 (32 x 4 x 3), 5 (32 x 3 x 4: round 1's 3 warps x 2 K+V stages), 6 (16 x 6 x 4),
+// 7 (16 x 8 x 2). cfg1 (profiles/r2_cfg1/geometry/): 32 x 4 x 2 streams 64K fp32
+// tokens in 17.4 us (ncu, clean L2) against 18.8 for 32 x 3 x 4.
+constexpr int kF32Tiles[8] = {32, 32, 32, 16, 32, 32, 16, 16};
+constexpr int kF32Warps[8] = {4, 2, 6, 4, 4, 3, 6, 8};
+constexpr int kF32Entries[8] = {2, 6, 2, 4, 3, 4, 4, 2};
 int f32_cfg() {
     static const int c = [] { const char* e = std::getenv("TD_F32_CFG"); return e ? std::atoi(e) & 7 : 0; }();
     return c;
@@ -2464,7 +2467,9 @@ template <int D>
 size_t bf16_smem() {
     return size_t(bf16_warps(D)) * bf16_stages(D) * bf16_stage_bytes(D) + 1024;
 }
-size_t f32_smem() { return size_t(kF32Warps[f32_cfg()]) * kF32Entries[f32_cfg()] * kF32Tile * 128 * 4 + 128; }
+size_t f32_smem() {
+    return size_t(kF32Warps[f32_cfg()]) * kF32Entries[f32_cfg()] * kF32Tiles[f32_cfg()] * 128 * 4 + 128;
+}
 
 }  // namespace
 
@@ -2636,7 +2641,7 @@ bool plan_split(int dtype, int64_t b, int n_q, int n_kv, int64_t t, int d, int s
         p.warps = bf16_warps(d);
     } else if (f32_ok) {
         p.kernel = 2;
-        p.tile = kF32Tile;
+        p.tile = kF32Tiles[f32_cfg()];
         p.warps = f32_warps();
     } else {
         p.kernel = 0;
@@ -2825,23 +2830,23 @@ cudaError_t launch_k1(const SplitPlan& p, const K1Args& a, const CUtensorMap* tm
     } else if (p.kernel == 2) {
         const size_t sm = f32_smem();
         switch (p.group) {
-#define TD_LAUNCH_F32_WS(GG, WW, SS)                                        \
+#define TD_LAUNCH_F32_WS(GG, TT, WW, SS)                                        \
     {                                                                       \
-        auto kern = k1_f32<kF32Tile, WW, SS, GG>;                           \
+        auto kern = k1_f32<TT, WW, SS, GG>;                                 \
         if ((e = set_smem(kern, sm)) != cudaSuccess) return e;              \
         if ((e = launch_pdl(kern, p.ctas, WW * 32, sm, st, p.pdl, a)) != cudaSuccess) return e; \
     }
 #define TD_LAUNCH_F32(GG)                                                   \
     case GG:                                                                \
         switch (f32_cfg()) {                                                \
-        case 1: TD_LAUNCH_F32_WS(GG, 2, 6) break;                           \
-        case 2: TD_LAUNCH_F32_WS(GG, 6, 2) break;                           \
-        case 3: TD_LAUNCH_F32_WS(GG, 1, 12) break;                          \
-        case 4: TD_LAUNCH_F32_WS(GG, 4, 3) break;                           \
-        case 5: TD_LAUNCH_F32_WS(GG, 3, 4) break;                           \
-        case 6: TD_LAUNCH_F32_WS(GG, 5, 2) break;                           \
-        case 7: TD_LAUNCH_F32_WS(GG, 3, 3) break;                           \
-        default: TD_LAUNCH_F32_WS(GG, 4, 2) break;                          \
+        case 1: TD_LAUNCH_F32_WS(GG, 32, 2, 6) break;                       \
+        case 2: TD_LAUNCH_F32_WS(GG, 32, 6, 2) break;                       \
+        case 3: TD_LAUNCH_F32_WS(GG, 16, 4, 4) break;                       \
+        case 4: TD_LAUNCH_F32_WS(GG, 32, 4, 3) break;                       \
+        case 5: TD_LAUNCH_F32_WS(GG, 32, 3, 4) break;                       \
+        case 6: TD_LAUNCH_F32_WS(GG, 16, 6, 4) break;                       \
+        case 7: TD_LAUNCH_F32_WS(GG, 16, 8, 2) break;                       \
+        default: TD_LAUNCH_F32_WS(GG, 32, 4, 2) break;                      \
         }                                                                   \
         break;
             TD_LAUNCH_F32(1)
@@ -2998,18 +3003,18 @@ const void* k1_function(const SplitPlan& p) {
         }
     }
     if (p.kernel == 2) {
-#define TD_F32_FN(WW, EE) \
-    (p.group == 1 ? reinterpret_cast<const void*>(k1_f32<kF32Tile, WW, EE, 1>) \
-                  : reinterpret_cast<const void*>(k1_f32<kF32Tile, WW, EE, 2>))
+#define TD_F32_FN(TT, WW, EE) \
+    (p.group == 1 ? reinterpret_cast<const void*>(k1_f32<TT, WW, EE, 1>) \
+                  : reinterpret_cast<const void*>(k1_f32<TT, WW, EE, 2>))
         switch (f32_cfg()) {
-        case 1: return TD_F32_FN(2, 6);
-        case 2: return TD_F32_FN(6, 2);
-        case 3: return TD_F32_FN(1, 12);
-        case 4: return TD_F32_FN(4, 3);
-        case 5: return TD_F32_FN(3, 4);
-        case 6: return TD_F32_FN(5, 2);
-        case 7: return TD_F32_FN(3, 3);
-        default: return TD_F32_FN(4, 2);
+        case 1: return TD_F32_FN(32, 2, 6);
+        case 2: return TD_F32_FN(32, 6, 2);
+        case 3: return TD_F32_FN(16, 4, 4);
+        case 4: return TD_F32_FN(32, 4, 3);
+        case 5: return TD_F32_FN(32, 3, 4);
+        case 6: return TD_F32_FN(16, 6, 4);
+        case 7: return TD_F32_FN(16, 8, 2);
+        default: return TD_F32_FN(32, 4, 2);
         }
 #undef TD_F32_FN
     }
