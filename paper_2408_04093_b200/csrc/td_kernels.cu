@@ -122,7 +122,8 @@ struct K1Args {
     unsigned sepoch;
     int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
     int spoll;  // chunk flags (TD_K2_STREAM_POLL): 0 each warp waits for its batch, 1 one warp per
-                // block polls them all, 2 each warp folds its ready prefix as it grows
+                // block polls them all, 2 each warp folds its ready prefix as it grows, 3 as 0
+                // with relaxed polls backing off to 256 ns
     int* serr;  // set when a streamed K2 gave up waiting for a state (mapped host memory)
     Tail tail;
 };
@@ -1575,16 +1576,24 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
 // Waits until every lane's candidate flag (idx >= 0) carries this launch's
 // epoch; bounded (~1 s of clocks, then *err if given) so a missing state cannot
 // hang the GPU. Afterwards every lane may read every lane's candidate.
-__device__ __forceinline__ void wait_flags(const unsigned* f, int idx, unsigned ep, int spin, int* err) {
+__device__ __forceinline__ void wait_flags(const unsigned* f, int idx, unsigned ep, int spin, int* err,
+                                           bool relaxed = false) {
     const long long t0 = clock64();
     for (;;) {
-        const bool ok = idx < 0 || ld_acquire_gpu(f + idx) == ep;
+        bool ok = true;
+        if (idx >= 0) {
+            unsigned v;
+            if (relaxed) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f + idx) : "memory");
+            else v = ld_acquire_gpu(f + idx);
+            ok = v == ep;
+        }
         if (__all_sync(0xffffffffu, ok)) break;
         if (clock64() - t0 > (1ll << 31)) {
             if (err) *reinterpret_cast<volatile int*>(err) = 1;
             break;
         }
         __nanosleep(spin);
+        if (relaxed) spin = min(2 * spin, 256);  // back off while the chunks still stream
     }
     __syncwarp();
     __threadfence();  // the states behind every lane's flag, for every lane
@@ -1749,7 +1758,7 @@ __device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Co
             off = static_cast<int>(fs * g + h);
             fi = static_cast<int>(int64_t(a.ctas) * W + fs);
         }
-        if (!a.spoll) wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
+        if (a.spoll == 0 || a.spoll == 3) wait_flags(a.sflag, fi, a.sepoch, a.sspin, err, a.spoll == 3);
         fold_any(a.fslot_m, a.fslot_l, a.fslot_o, off, n, col, D, M, L, acc);
     }
 }
