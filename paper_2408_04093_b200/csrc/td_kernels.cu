@@ -121,9 +121,6 @@ struct K1Args {
     unsigned* sflag;
     unsigned sepoch;
     int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
-    int spoll;  // chunk flags (TD_K2_STREAM_POLL): 0 each warp waits for its batch, 1 one warp per
-                // block polls them all, 2 each warp folds its ready prefix as it grows, 3 as 0
-                // with relaxed polls backing off to 256 ns
     int* serr;  // set when a streamed K2 gave up waiting for a state (mapped host memory)
     Tail tail;
 };
@@ -1576,24 +1573,16 @@ __global__ void __launch_bounds__(K2_THREADS) k2_combine_cols(const K1Args a) {
 // Waits until every lane's candidate flag (idx >= 0) carries this launch's
 // epoch; bounded (~1 s of clocks, then *err if given) so a missing state cannot
 // hang the GPU. Afterwards every lane may read every lane's candidate.
-__device__ __forceinline__ void wait_flags(const unsigned* f, int idx, unsigned ep, int spin, int* err,
-                                           bool relaxed = false) {
+__device__ __forceinline__ void wait_flags(const unsigned* f, int idx, unsigned ep, int spin, int* err) {
     const long long t0 = clock64();
     for (;;) {
-        bool ok = true;
-        if (idx >= 0) {
-            unsigned v;
-            if (relaxed) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f + idx) : "memory");
-            else v = ld_acquire_gpu(f + idx);
-            ok = v == ep;
-        }
+        const bool ok = idx < 0 || ld_acquire_gpu(f + idx) == ep;
         if (__all_sync(0xffffffffu, ok)) break;
         if (clock64() - t0 > (1ll << 31)) {
             if (err) *reinterpret_cast<volatile int*>(err) = 1;
             break;
         }
         __nanosleep(spin);
-        if (relaxed) spin = min(2 * spin, 256);  // back off while the chunks still stream
     }
     __syncwarp();
     __threadfence();  // the states behind every lane's flag, for every lane
@@ -1637,38 +1626,6 @@ __device__ __forceinline__ void fold_batch(const float* bm, const float* bl, con
     M = Mn;
 }
 
-// As fold_batch, but the n states are merged one at a time in order (the loads are
-// still issued together): the result does not depend on how the candidates were
-// split into calls, so a fold of whatever prefix is ready stays reproducible.
-template <int NB>
-__device__ __forceinline__ void fold_seq(const float* bm, const float* bl, const float* bo, int off, int n,
-                                         int col, int D, float& M, float& L, float& acc) {
-    const int lane = threadIdx.x & 31;
-    float ml = -CUDART_INF_F, ll = 0.f;
-    if (lane < n) {
-        ml = __ldcg(bm + off);
-        ll = __ldcg(bl + off);
-    }
-    float ov[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-        const int ok = __shfl_sync(0xffffffffu, off, k);
-        ov[k] = (k < n && col < D) ? __ldcg(bo + int64_t(ok) * D + col) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-        const float mk = __shfl_sync(0xffffffffu, ml, k), lk = __shfl_sync(0xffffffffu, ll, k);
-        if (k < n && mk != -CUDART_INF_F) {
-            const float Mn = fmaxf(M, mk);
-            const float cs = M == -CUDART_INF_F ? 0.f : fast_exp2(M - Mn);
-            const float e = fast_exp2(mk - Mn);
-            L = L * cs + e * lk;
-            acc = acc * cs + e * ov[k];
-            M = Mn;
-        }
-    }
-}
-
 __device__ __forceinline__ void fold_any(const float* bm, const float* bl, const float* bo, int off, int n, int col,
                                          int D, float& M, float& L, float& acc) {
     if (n <= 8) fold_batch<8>(bm, bl, bo, off, n, col, D, M, L, acc);
@@ -1705,51 +1662,7 @@ __device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Co
         fold_any(a.slot_m, a.slot_l, a.slot_o, off, n, col, D, M, L, acc);
     }
     const int nf = cv.nf;
-    if (a.spoll == 1) {  // warp 0 alone polls the row's chunk flags; the others wait at the barrier
-        if (warp == 0)
-            for (int k0 = 0; k0 < nf; k0 += 32)
-                wait_flags(a.sflag, k0 + lane < nf ? static_cast<int>(int64_t(a.ctas) * W + bh * a.fslots + k0 + lane) : -1,
-                           a.sepoch, a.sspin, err);
-        __syncthreads();
-        __threadfence();
-    }
     const int nc = nf > warp ? (nf - warp + WS - 1) / WS : 0;
-    if (a.spoll == 2) {
-        // fold the ready prefix of the warp's chunks as it grows (backing off while
-        // nothing new is ready), so the last chunk leaves a fold of one or two states
-        const long long t0 = clock64();
-        int spin = a.sspin;
-        for (int j0 = 0; j0 < nc;) {
-            const int n = min(32, nc - j0);
-            int off = 0;
-            bool ready = true;
-            if (lane < n) {
-                const int64_t fs = bh * a.fslots + warp + int64_t(j0 + lane) * WS;
-                off = static_cast<int>(fs * g + h);
-                ready = ld_acquire_gpu(a.sflag + int64_t(a.ctas) * W + fs) == a.sepoch;
-            }
-            const unsigned notready = __ballot_sync(0xffffffffu, !ready);
-            const int m = notready ? __ffs(notready) - 1 : 32;  // ready prefix (lanes >= n count as ready)
-            const int take = min(m, n);
-            if (take == 0) {
-                if (clock64() - t0 > (1ll << 31)) {
-                    if (err) *reinterpret_cast<volatile int*>(err) = 1;
-                    break;
-                }
-                __nanosleep(spin);
-                spin = min(2 * spin, 1024);
-                continue;
-            }
-            __syncwarp();
-            __threadfence();
-            if (take <= 4) fold_seq<4>(a.fslot_m, a.fslot_l, a.fslot_o, off, take, col, D, M, L, acc);
-            else if (take <= 16) fold_seq<16>(a.fslot_m, a.fslot_l, a.fslot_o, off, take, col, D, M, L, acc);
-            else fold_seq<32>(a.fslot_m, a.fslot_l, a.fslot_o, off, take, col, D, M, L, acc);
-            j0 += take;
-            spin = a.sspin;
-        }
-        return;
-    }
     for (int j0 = 0; j0 < nc; j0 += 32) {
         const int n = min(32, nc - j0);
         int off = 0, fi = -1;
@@ -1758,7 +1671,7 @@ __device__ __forceinline__ void stream_fold(const K1Args& a, int64_t r, const Co
             off = static_cast<int>(fs * g + h);
             fi = static_cast<int>(int64_t(a.ctas) * W + fs);
         }
-        if (a.spoll == 0 || a.spoll == 3) wait_flags(a.sflag, fi, a.sepoch, a.sspin, err, a.spoll == 3);
+        wait_flags(a.sflag, fi, a.sepoch, a.sspin, err);
         fold_any(a.fslot_m, a.fslot_l, a.fslot_o, off, n, col, D, M, L, acc);
     }
 }
@@ -2547,8 +2460,6 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.sepoch = p.sepoch;
     static const int sspin = [] { const char* e = std::getenv("TD_K2_STREAM_SLEEP"); return e ? std::atoi(e) : 64; }();
     a.sspin = sspin;
-    static const int spoll = [] { const char* e = std::getenv("TD_K2_STREAM_POLL"); return e ? std::atoi(e) : 0; }();
-    a.spoll = spoll;
     if (p.pool_tiles > 0) {
         unsigned* cnt = p.counters;  // [2 parities][bh_count] pool, then [2][bh_count] foreign
         a.pool_ctr = cnt + p.parity * p.bh_count;
