@@ -1832,10 +1832,6 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         // allreduce(sum), n/d in one kernel over the ranks' symmetric windows
         if (int rc2 = exchange_failed(ctx)) return rc2;
         if (int rc2 = nccl_dev_open(ctx, rows, d)) return rc2;
-        if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok, ctx->row_max, ctx->lse,
-                              ctx->out_local, (flags & TD_TIME_KERNELS) != 0, ctx->cur_phase ? ctx : nullptr)))
-            return rc;
-        phase_mark(ctx);
         float* dst = ctx->out;
         if (!(flags & TD_HOST_IO)) dst = out;
         else if (!(flags & TD_BF16_OUT) && xchg_in_place(rows, d)) if (float* m = mapped_host(ctx, out)) dst = m;
@@ -1847,10 +1843,33 @@ int td_tree_decode(td_context* ctx, const void* q, int64_t n_q, double scale, in
         xa.max_rows = ctx->nx_rows;
         xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));
         xa.error = ctx->x_err;
-        TD_CUDA(td::launch_literal_combine(ctx->lse, ctx->out_local, xa, rows, static_cast<int>(d), dst, ctx->stream));
+        // with the streamed combine the two rounds run inside the combine kernel
+        // (TD_NCCL_FUSED=0: K2 then K2n, two kernels)
+        static const bool fused = [] { const char* e = std::getenv("TD_NCCL_FUSED"); return !e || std::atoi(e) != 0; }();
+        if (fused && td::stream_plan(plan) && rows * 4 <= std::min<int64_t>(plan.ctas, xa.max_blocks) &&
+            !(flags & (TD_TIME_KERNELS | TD_TIME_PHASES))) {
+            const CUtensorMap* pk = plan.kernel == 1 ? &ctx->tmk : nullptr;
+            const CUtensorMap* pv = plan.kernel == 1 ? &ctx->tmv : nullptr;
+            TD_CUDA(td::launch_decode_literal(plan, qd, ctx->k.p, ctx->v.p, static_cast<float>(scale), pk, pv,
+                                              ctx->ws.p, xa, dst, ctx->stream));
+            launched(ctx, plan);
+            ctx->kv_safe = plan.app_k ? plan.app_pos : ctx->len;
+            ctx->last_kernels = 2;  // K1 + the combine kernel
+            ctx->last_kv_bytes = 2.0 * double(ctx->b) * double(ctx->n_kv) * double(ctx->len) * double(d) *
+                                 td::dtype_bytes(ctx->dtype);
+            ctx->last_split_kernel = plan.kernel;
+        } else {
+            if ((rc = run_partial(ctx, plan, qd, ctx->k.p, ctx->v.p, ctx->len, scale, ctx->tm_ok, ctx->row_max,
+                                  ctx->lse, ctx->out_local, (flags & TD_TIME_KERNELS) != 0,
+                                  ctx->cur_phase ? ctx : nullptr)))
+                return rc;
+            phase_mark(ctx);
+            TD_CUDA(td::launch_literal_combine(ctx->lse, ctx->out_local, xa, rows, static_cast<int>(d), dst,
+                                               ctx->stream));
+            ctx->last_kernels += 1;
+        }
         ctx->nx_epoch = xa.epoch;
         phase_mark(ctx);
-        ctx->last_kernels += 1;
         if (int rc2 = deliver_out(ctx, dst, rows, out, flags)) return rc2;
         return (flags & TD_HOST_IO) ? exchange_failed(ctx) : TD_OK;
     }

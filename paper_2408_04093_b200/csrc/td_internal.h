@@ -183,6 +183,13 @@ bool make_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int d, in
 // K2n: allreduce(max) + partial_to_numerator + allreduce(sum) + n/d of K2's
 // per-row (lse, out) over the ranks' symmetric NCCL windows (xa.peers: every
 // rank's window base, from launch_lsa_peers); programmatic dependent of K2.
+// K1 + the streamed split K2x with the paper-literal two-round combine inside it
+// (kTailLiteral: K2n's protocol over the NCCL window of xa, no extra kernel);
+// cudaErrorInvalidValue when the plan has no streamed combine or too many rows.
+cudaError_t launch_decode_literal(const SplitPlan& plan, const void* q, const void* k, const void* v, float scale,
+                                  const CUtensorMap* tmk, const CUtensorMap* tmv, void* workspace,
+                                  const XchgArgs& xa, float* out, cudaStream_t stream, cudaEvent_t ev0 = nullptr,
+                                  cudaEvent_t ev1 = nullptr);
 cudaError_t launch_literal_combine(const float* lse, const float* o, const XchgArgs& xa, int64_t rows, int d,
                                    float* out, cudaStream_t stream);
 // Words of one rank's K2n window: A [2][p][max_rows] + B [2][p][max_rows][d + 1].

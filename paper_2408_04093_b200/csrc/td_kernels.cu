@@ -48,7 +48,10 @@ struct Xchg {
 };
 
 // What K2 does with the merged rows.
-enum TailMode { kTailPartial = 0, kTailFinal = 1, kTailExchange = 2 };
+// kTailLiteral (streamed split K2x only): the paper-literal two collective rounds
+// (allreduce(max) of lse, then allreduce(sum) of [n | d]) over an NCCL symmetric
+// window, inside the combine kernel -- K2n's protocol without its kernel boundary.
+enum TailMode { kTailPartial = 0, kTailFinal = 1, kTailExchange = 2, kTailLiteral = 3 };
 struct Tail {
     int mode;
     float* row_max;      // [b][n_q]      (partial)
@@ -2003,6 +2006,9 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
     const int D = a.d, g = a.group, st = a.maxseg * g;
     const unsigned par = x.epoch & 1u;
     const int64_t stride = x.max_rows * int64_t(D + 1);
+    float lit_val = 0.f, lit_lse = -CUDART_INF_F;  // kTailLiteral: this block's unit (warp 0)
+    int64_t lit_row = -1;
+    int lit_col = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {  // merge + push
         const int64_t r = u / Q;
         const int col = static_cast<int>(u % Q) * 32 + lane;
@@ -2077,7 +2083,16 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
                 if (col < D) st_ll(dst + col, val, x.epoch);
                 if (lane == 0 && col == 0) st_ll(dst + D, lse, x.epoch);
             };
-            if (x.pull) {
+            if (SF && a.tail.mode == kTailLiteral) {
+                // round 1 of the literal combine: this rank's lse of the row into slot
+                // (parity, rank) of region A of every rank's window (one unit per block)
+                lit_val = val;
+                lit_lse = lse;
+                lit_row = orow;
+                lit_col = col;
+                if (lane == 0 && col == 0)
+                    for (int q = 0; q < x.p; ++q) st_ll(peers[q] + (int64_t(par) * x.p + x.rank) * x.max_rows + orow, lse, x.epoch);
+            } else if (x.pull) {
                 push(peers[x.rank] + off);
             } else {
 #pragma unroll
@@ -2088,7 +2103,64 @@ __global__ void __launch_bounds__(32 * WS) k2_exchange_split(const K1Args a) {
         }
         __syncthreads();
     }
-    if (warp == 0) {
+    if (SF && a.tail.mode == kTailLiteral) {
+        if (warp == 0 && lit_row >= 0) {
+            // round 1 receive: max over the p ranks' lse of the row
+            const uint2* ownw = peers[x.rank];
+            float m = -CUDART_INF_F;
+            for (int k = lane; k < x.p; k += 32)
+                m = fmaxf(m, ld_ll(ownw + (int64_t(par) * x.p + k) * x.max_rows + lit_row, x.epoch, x.error));
+#pragma unroll
+            for (int s2 = 16; s2 >= 1; s2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s2));
+            // partial_to_numerator, then round 2: [n | d] into slot (parity, rank) of region B
+            const float wgt = lit_lse == -CUDART_INF_F ? 0.f : expf(lit_lse - m);
+            const float nv = lit_val * wgt;
+            const int64_t b0 = 2 * int64_t(x.p) * x.max_rows;
+            const int64_t sstride = x.max_rows * int64_t(D + 1);
+            const int64_t boff = b0 + (int64_t(par) * x.p + x.rank) * sstride + lit_row * (D + 1);
+            for (int q = 0; q < x.p; ++q) {
+                uint2* dst = (q < PMAX ? pp[q] : peers[q]) + boff;
+                if (lit_col < D) st_ll(dst + lit_col, nv, x.epoch);
+                if (lane == 0 && lit_col == 0) st_ll(dst + D, wgt, x.epoch);
+            }
+            // round 2 receive: sum the p sources' [n | d] (the first PMAX as one batch), n / d
+            const uint2* base = ownw + b0 + int64_t(par) * x.p * sstride + lit_row * (D + 1);
+            uint2 wd[PMAX], wn[PMAX];
+            const long long t0 = clock64();
+            for (;;) {
+                bool all = true;
+#pragma unroll
+                for (int k = 0; k < PMAX; ++k) {
+                    if (k >= x.p) continue;
+                    wd[k] = ld_word(base + k * sstride + D);
+                    if (lit_col < D) wn[k] = ld_word(base + k * sstride + lit_col);
+                }
+#pragma unroll
+                for (int k = 0; k < PMAX; ++k) {
+                    if (k >= x.p) continue;
+                    all &= wd[k].y == x.epoch;
+                    if (lit_col < D) all &= wn[k].y == x.epoch;
+                }
+                if (__all_sync(0xffffffffu, all)) break;
+                if (clock64() - t0 > (1ll << 32)) {  // ~2 s: a rank never arrived
+                    *reinterpret_cast<volatile int*>(x.error) = 1 | (255 << 8) | (x.rank << 16);
+                    break;
+                }
+            }
+            float den = 0.f, num = 0.f;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) {
+                if (k >= x.p) continue;
+                den += __uint_as_float(wd[k].x);
+                if (lit_col < D) num += __uint_as_float(wn[k].x);
+            }
+            for (int k = PMAX; k < x.p; ++k) {
+                den += ld_ll(base + k * sstride + D, x.epoch, x.error);
+                if (lit_col < D) num += ld_ll(base + k * sstride + lit_col, x.epoch, x.error);
+            }
+            if (lit_col < D) a.tail.out[lit_row * D + lit_col] = num / den;
+        }
+    } else if (warp == 0) {
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {  // exact combine of the p partials
             const int64_t r = u / Q;
             const int col = static_cast<int>(u % Q) * 32 + lane;
@@ -3029,6 +3101,26 @@ unsigned grid_for(int64_t n, int threads) {
     return static_cast<unsigned>(g);
 }
 }  // namespace
+
+cudaError_t launch_decode_literal(const SplitPlan& p, const void* q, const void* k, const void* v, float scale,
+                                  const CUtensorMap* tmk, const CUtensorMap* tmv, void* ws, const XchgArgs& xa,
+                                  float* out, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+    K1Args a = make_args(p, q, k, v, scale, ws);
+    if (!a.sflag || a.bh_count * a.group * 4 > xa.max_blocks || a.bh_count * a.group * 4 > a.ctas)
+        return cudaErrorInvalidValue;  // the fused literal combine needs the streamed split K2x, one unit per block
+    a.tail.mode = kTailLiteral;
+    a.tail.out = out;
+    a.tail.x.peers = xa.peers;
+    a.tail.x.p = xa.p;
+    a.tail.x.rank = xa.rank;
+    a.tail.x.epoch = xa.epoch;
+    a.tail.x.max_rows = xa.max_rows;
+    a.tail.x.error = xa.error;
+    a.tail.x.pull = 0;
+    cudaError_t e = launch_k1(p, a, tmk, tmv, st, ev0, ev1);
+    if (e != cudaSuccess) return e;
+    return launch_k2(a, xa.max_blocks, true, st);
+}
 
 cudaError_t launch_literal_combine(const float* lse, const float* o, const XchgArgs& xa, int64_t rows, int d,
                                    float* out, cudaStream_t st) {
