@@ -2962,16 +2962,18 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
         return cudaLaunchKernelEx(&cfg, k2_combine_split<4, 4>, a);
     }
     // many rows (rows x 4 > the block cap, e.g. cfg4's 1024): (row, quarter) warp units
-    // over 4-warp blocks, one block per SM, launched after K1 completes -- no
-    // programmatic overlap, so no parked K2 warps next to K1, and four times the
-    // warps of the single-warp PDL launch below. cfg4: 1214.5 / 1215.7 vs 1225.1 /
-    // 1226.1 us at N=1, 352.8 / 353.0 vs 362.9 / 364.3 at N=4 (profiles/r2_k2_wide/);
+    // over 4-warp blocks, TD_K2_WIDE (2) blocks per SM (the exchange: at most its
+    // co-resident warp budget), launched after K1 completes -- no programmatic
+    // overlap, so no parked K2 warps next to K1, and 4-8 times the warps of the
+    // single-warp PDL launch below. cfg4 at N=1: 1210.3 (2 per SM) / 1214.5-1221.1 (1)
+    // / 1225.1-1226.1 us (PDL); N=4: 352.3-353.5 vs 362.9-364.3 (profiles/r2_k2_wide/);
     // TD_K2_WIDE=0 restores the PDL launch
-    static const int wide = [] { const char* e = std::getenv("TD_K2_WIDE"); return e ? std::atoi(e) : 1; }();
+    static const int wide = [] { const char* e = std::getenv("TD_K2_WIDE"); return e ? std::atoi(e) : 2; }();
     if (wide && a.d == 128 && force_w == 0 && rows * 4 > limit && !a.dbg && !stream) {
         const int64_t units = rows * 4;
         int64_t blk = (units + 3) / 4;
-        const int64_t bcap = std::min<int64_t>(a.ctas > 0 ? a.ctas : 1, std::max<int64_t>(1, max_blocks / 4));
+        const int64_t bcap = std::min<int64_t>(int64_t(wide) * (a.ctas > 0 ? a.ctas : 1),  // wide blocks per SM
+                                               std::max<int64_t>(1, max_blocks / 4));
         if (blk > bcap) blk = bcap;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(blk));
