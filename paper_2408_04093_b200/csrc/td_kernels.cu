@@ -125,6 +125,7 @@ struct K1Args {
     unsigned sepoch;
     int sspin;  // ns between polls of a streamed K2 warp (TD_K2_STREAM_SLEEP)
     int* serr;  // set when a streamed K2 gave up waiting for a state (mapped host memory)
+    int solo;   // the context has its GPU to itself (SplitPlan::pdl): the exchange may launch wide
     Tail tail;
 };
 
@@ -2529,6 +2530,7 @@ K1Args make_args(const SplitPlan& p, const void* q, const void* k, const void* v
     a.done_epoch = p.done_epoch;
     a.sflag = stream_plan(p) ? p.sflag : nullptr;
     a.serr = p.serr;
+    a.solo = p.pdl ? 1 : 0;
     a.sepoch = p.sepoch;
     static const int sspin = [] { const char* e = std::getenv("TD_K2_STREAM_SLEEP"); return e ? std::atoi(e) : 64; }();
     a.sspin = sspin;
@@ -2969,7 +2971,9 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
     // / 1225.1-1226.1 us (PDL); N=4: 352.3-353.5 vs 362.9-364.3 (profiles/r2_k2_wide/);
     // TD_K2_WIDE=0 restores the PDL launch
     static const int wide = [] { const char* e = std::getenv("TD_K2_WIDE"); return e ? std::atoi(e) : 2; }();
-    if (wide && a.d == 128 && force_w == 0 && rows * 4 > limit && !a.dbg && !stream) {
+    // (an exchange among workers sharing a GPU keeps the old launch: their grids must
+    // all be co-resident, and four times the warps per worker might not be)
+    if (wide && a.d == 128 && force_w == 0 && rows * 4 > limit && !a.dbg && !stream && (a.solo || !exchange)) {
         const int64_t units = rows * 4;
         int64_t blk = (units + 3) / 4;
         const int64_t bcap = std::min<int64_t>(int64_t(wide) * (a.ctas > 0 ? a.ctas : 1),  // wide blocks per SM
