@@ -1640,7 +1640,12 @@ int launch_tree_p2p(td_context* ctx, const TreeCall& tc, double scale, float* xd
     xa.rank = ctx->rank;
     xa.epoch = ctx->x_epoch + 1;  // committed only once the launch is in: all ranks stay in step
     xa.max_rows = ctx->x_max_rows;
-    xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, 4 * int64_t(ctx->sm_count));  // one-warp blocks, co-resident
+    // co-resident warp budget of the exchange kernel (TD_XCHG_WARPS_PER_SM, 8): its grid must
+    // fit next to the next step's K1 (it only matters for the wide many-row launch: cfg4
+    // at N=4 340.4 / 343.2 us with 8 vs 352.6 / 354.9 with 4, profiles/r2_k2_wide/);
+    // workers sharing a GPU keep 4
+    static const int xw = [] { const char* e = std::getenv("TD_XCHG_WARPS_PER_SM"); return e ? std::atoi(e) : 8; }();
+    xa.max_blocks = std::min<int64_t>(td::kXchgBlocks, int64_t(ctx->shared_device ? 4 : std::max(1, xw)) * ctx->sm_count);
     xa.error = ctx->x_err;
     static const int pull = [] { const char* e = std::getenv("TD_XCHG_PULL"); return e ? std::atoi(e) : 0; }();
     xa.pull = pull;
