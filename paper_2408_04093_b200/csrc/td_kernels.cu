@@ -2964,13 +2964,13 @@ cudaError_t launch_k2(const K1Args& a, int64_t max_blocks, bool exchange, cudaSt
         return cudaLaunchKernelEx(&cfg, k2_combine_split<4, 4>, a);
     }
     // many rows (rows x 4 > the block cap, e.g. cfg4's 1024): (row, quarter) warp units
-    // over 4-warp blocks, TD_K2_WIDE (2) blocks per SM (the exchange: at most its
+    // over 4-warp blocks, TD_K2_WIDE (4) blocks per SM (the exchange: at most its
     // co-resident warp budget), launched after K1 completes -- no programmatic
-    // overlap, so no parked K2 warps next to K1, and 4-8 times the warps of the
-    // single-warp PDL launch below. cfg4 at N=1: 1210.3 (2 per SM) / 1214.5-1221.1 (1)
-    // / 1225.1-1226.1 us (PDL); N=4: 352.3-353.5 vs 362.9-364.3 (profiles/r2_k2_wide/);
-    // TD_K2_WIDE=0 restores the PDL launch
-    static const int wide = [] { const char* e = std::getenv("TD_K2_WIDE"); return e ? std::atoi(e) : 2; }();
+    // overlap, so no parked K2 warps next to K1, and 4-16 times the warps of the
+    // single-warp PDL launch below. cfg4 at N=1: 1201.9-1203.7 (4 per SM) / 1207.2-1210.3
+    // (2) / 1214.5-1221.1 (1) / 1225.1-1226.1 us (PDL); N=4: 340.4-343.2 vs 362.9-364.3
+    // (profiles/r2_k2_wide/); TD_K2_WIDE=0 restores the PDL launch
+    static const int wide = [] { const char* e = std::getenv("TD_K2_WIDE"); return e ? std::atoi(e) : 4; }();
     // (an exchange among workers sharing a GPU keeps the old launch: their grids must
     // all be co-resident, and four times the warps per worker might not be)
     if (wide && a.d == 128 && force_w == 0 && rows * 4 > limit && !a.dbg && !stream && (a.solo || !exchange)) {
